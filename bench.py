@@ -1,0 +1,341 @@
+"""Benchmark of the HWSDA per-generation population loop on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): cascaded-THG, congruent LiNbO3
+(Jundt, 25 C), 1404 nm pump, L = 10^4 um, t = 1 um -> D = 10,000 domains,
+NP = 1,024, a 1,000-generation run_hybrid; synthetic inputs are the seeded
+initial population itself (init_population from stream (seed, 0, i)).
+
+A step is one HWSDA generation.  W warm-up generations run untimed, then
+exactly K generations are timed with CUDA events on the engine stream,
+bracketed by a barrier and torch.cuda.synchronize(); the max over ranks is
+reported.  `value` is domain-fitness evaluations per second,
+(2 NP - k) * D * K / t, with the population resident in HBM.  The genome pool
+(2 x NP x D f64 = 164 MB) exceeds the 126 MB L2, so no extra flush is done.
+
+Extra keys: `roofline` (dominant kernel, measured live with CUDA events),
+`cpu_baseline` (the CPU oracle port on this host's cores, bounded sample),
+`e2e` (the public run_hybrid() call end to end: engine creation, table
+upload, all generations, trace + best read back), `clocks`, `stages`.
+
+`--impl reference` times the reference's CPU algorithm (the oracle port in
+oracle/, all host threads) on the same config and metric.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "domain-fitness evals/sec (HWSDA generation loop, C2 NP=1024 D=10^4)"
+UNIT = "domain-evals/s"
+NP, D, G_RUN, SEED = 1024, 10_000, 1000, 0
+THICKNESS_UM, PUMP_NM = 1.0, 1404.0
+FLOP_PER_EVAL = 10  # complex add + complex mul + complex add per domain
+DE_BYTES_PER_GENE = 40  # x_i, x_r1, x_r2, x_r3 read + trial written, f64
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_objective(q, mode="fast"):
+    spec = q.ObjectiveSpec("single_thg", (PUMP_NM,))
+    return q.make_objective(spec, q.default_dispersion(25.0), THICKNESS_UM, D, mode=mode)
+
+
+def evals_per_generation(k=4):
+    return (2 * NP - k) * D
+
+
+def cpu_baseline(threads: int = 0, target_s: float = 12.0):
+    """The CPU oracle port on this host: bounded sample of C2 generations."""
+    from oracle import oracle as O
+    from paper_2511_01255_b200 import tables as T
+
+    tb = T.build_tables("thg", THICKNESS_UM, D, T.phase_mismatches(T.default_dispersion(25.0), PUMP_NM))
+    P = O.Problem("thg", tb.e1[None], tb.b[None], np.array([tb.w]), np.array([tb.hconst]), tb.normalization)
+    t0 = time.perf_counter()
+    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=0)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=2)
+    per_gen = max((time.perf_counter() - t0 - t_init) / 2, 1e-4)
+    gens = int(min(max(target_s / per_gen, 3), 200))
+    t0 = time.perf_counter()
+    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=gens)
+    dt = time.perf_counter() - t0 - t_init
+    cores = threads if threads > 0 else O.max_threads()
+    return {"value": evals_per_generation() * gens / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle/qpm_oracle.c run_hybrid C2 generations 1..{gens} of a {G_RUN}-generation run "
+                      f"(init excluded), {cores} pthreads", "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    from oracle import oracle as O
+    from paper_2511_01255_b200 import tables as T
+
+    tb = T.build_tables("thg", THICKNESS_UM, D, T.phase_mismatches(T.default_dispersion(25.0), PUMP_NM))
+    P = O.Problem("thg", tb.e1[None], tb.b[None], np.array([tb.w]), np.array([tb.hconst]), tb.normalization)
+    G = max(G_RUN, args.warmup + args.steps)
+    t0 = time.perf_counter()
+    O.run(P, "hybrid", NP, G, SEED, stop_after=args.warmup)
+    t_w = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.run(P, "hybrid", NP, G, SEED, stop_after=args.warmup + args.steps)
+    t_wk = time.perf_counter() - t0
+    dt = max(t_wk - t_w, 1e-9)
+    value = evals_per_generation() * args.steps / dt
+    cores = O.max_threads()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded init_population)",
+            "config": {"workload": "C2 run_hybrid NP=1024 D=10000 THG 1404nm t=1um, 1000 generations",
+                       "NP": NP, "D": D, "generations": G, "timed_generations": [args.warmup + 1,
+                                                                               args.warmup + args.steps]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"oracle/qpm_oracle.c (C restatement of qpmdesign run_hybrid, pinned "
+                                       f"bit-exact to the reference) generations {args.warmup + 1}.."
+                                       f"{args.warmup + args.steps}, {cores} pthreads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db):
+    """Roofline of the dominant stage (largest mean ms per generation)."""
+    name, ms = max(stages, key=lambda s: s[1])
+    if name.startswith("fitness"):
+        evals = NP * D  # the engine evaluates NP rows per fitness launch
+        achieved = evals * FLOP_PER_EVAL / (ms * 1e-3) / 1e12
+        peak = sm_count * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        roof = {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "peak_basis": f"nominal FP64 CUDA-core peak ({sm_count} SMs x 64 DFMA/clk "
+                                                       f"x 2 x sm_max_mhz from MEASURED_PEAKS.json)",
+                "algorithmic_unit": f"{FLOP_PER_EVAL} flop per domain-eval x NP*D = {evals} evals per launch"}
+    elif name == "de_trial":
+        nbytes = NP * D * DE_BYTES_PER_GENE
+        achieved = nbytes / (ms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
+                "algorithmic_unit": f"{DE_BYTES_PER_GENE} B per gene x NP*D"}
+    else:
+        nbytes = NP * D * 8
+        achieved = nbytes / (ms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
+                "algorithmic_unit": "8 B per gene x NP*D"}
+    roof["ms_per_launch"] = ms
+    roof["share_of_step"] = ms / ms_gen_total if ms_gen_total > 0 else None
+    t = traffic_db.get(name) if traffic_db else None
+    roof["traffic"] = t
+    return roof
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = env_rank()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2511_01255_b200 as q
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    peaks, peaks_kind = measured_peaks()
+    obj = build_objective(q)
+    de, gwo, sch = q.DEParams(), q.GWOParams(), q.Schedules()
+    G = max(G_RUN, args.warmup + args.steps)
+    stream = torch.cuda.Stream(dev)
+    # replicas with per-rank seeds until the sharded engine lands
+    eng = q.Engine(obj, "hybrid", pop_size=NP, generations=G, seed=SEED + rank, de=de, gwo=gwo, sch=sch,
+                   stream=stream)
+    eng.init()
+    eng.step(args.warmup)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        eng.step(args.steps)
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = start.elapsed_time(end)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    launches = eng.launches_per_generation * args.steps
+    trace = eng.trace(0, args.warmup + args.steps + 1)
+    best_after = float(trace[-1, 1])
+    del eng
+
+    # per-stage breakdown of the same workload, CUDA events on the engine stream
+    prof_gens = 20
+    eng2 = q.Engine(obj, "hybrid", pop_size=NP, generations=G, seed=SEED, de=de, gwo=gwo, sch=sch, stream=stream)
+    eng2.init()
+    eng2.step(args.warmup)
+    stages = eng2.profile(prof_gens)
+    torch.cuda.synchronize()
+    del eng2
+    traffic_db = {}
+    tpath = os.path.join(ROOT, "profiles", "traffic_bytes_per_launch.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic_db = json.load(fh)
+    ms_gen = ms / args.steps
+    roof = stage_roofline(stages, sum(s[1] for s in stages), peaks, peaks_kind, sm_count, traffic_db)
+
+    # end to end through the public API (host buffers, everything inside the clock)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = q.run_hybrid(obj, dimension=D, pop_size=NP, generations=args.steps, seed=SEED)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    h2d = (args.steps + 1) * 8 * 8 + 256
+    d2h = (args.steps + 1) * 5 * 8 + D * 9 + 8 + 64
+    e2e = {"value": evals_per_generation() * args.steps * world / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+           "what": "public run_hybrid(objective, generations=K) call: engine allocation, schedule upload, init, "
+                   "K generations, trace + best individual read back", "seconds": e2e_s,
+           "best_fitness": res.best.fitness}
+
+    if rank == 0:
+        cpu = cpu_baseline() if (world == 1 and not args.no_cpu_baseline) else None
+        value = evals_per_generation() * args.steps * world / (ms * 1e-3)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_gen, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded init_population, C2 shape)",
+                "config": {"workload": "C2 run_hybrid NP=1024 D=10000 THG 1404nm t=1um, 1000 generations",
+                           "NP": NP, "D": D, "generations": G, "fitness_mode": "fast",
+                           "timed_generations": [args.warmup + 1, args.warmup + args.steps],
+                           "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                           "l2": "genome pool 164 MB > 126 MB L2; no flush"},
+                "generations_per_s": 1e3 / ms_gen * world, "best_after_timed": best_after,
+                "roofline": roof, "stages": [{"name": n, "ms": m} for n, m in stages],
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
+                "peaks": peaks_kind}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=950)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * qpm_b200.h -- C ABI of the B200-native HWSDA population engine.
+ *
+ * One shared library (paper_2511_01255_b200/libqpm_b200.so, sm_100a) exports
+ * everything below.  Plain pointers and sizes only; no torch or C++ types
+ * cross the boundary.  Every entry point returns QPM_OK (0) or a negative
+ * status; qpm_last_error() returns a message for the calling thread.  Device
+ * pointers are CUDA global memory on the current device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Nothing allocates on the
+ * per-generation path: problems and engines allocate once at creation.
+ *
+ * Which reference interface each group replaces (paths relative to
+ * /root/reference/pkg/src/qpmdesign/):
+ *
+ *   qpm_uniform_fill, qpm_fold_key  -> _kernels.uniform_fill (_kernels.py:144-151,
+ *                                      87-98), rng.fold_key (rng.py:31-36)
+ *   qpm_problem_*                   -> ShgEvaluator/ThgEvaluator tables
+ *                                      (physics.py:277-356) + PatternObjective
+ *                                      (objectives.py:72-123)
+ *   qpm_fitness_bits, qpm_evaluate_block_host
+ *                                   -> PatternObjective.evaluate_block
+ *                                      (objectives.py:110-120) via
+ *                                      _kernels.thg_abs_block / shg_abs_block
+ *                                      (_kernels.py:134-142, 168-169)
+ *   qpm_sum_block_host              -> _kernels.thg_block / shg_block
+ *                                      (_kernels.py:124-132)
+ *   qpm_pack_signs                  -> Individual.from_genome projection
+ *                                      (optimizer.py:52-56), bit-packed
+ *   qpm_reduce_best                 -> parexec.reduce_best (parexec.py:123-154)
+ *   qpm_engine_*                    -> optimizer.run_hybrid / run_de / run_gwo
+ *                                      (optimizer.py:400-616) including
+ *                                      de_mutate/de_crossover/de_select,
+ *                                      rank_leaders, gwo_discrete_update,
+ *                                      gwo_reference_update, adaptive_f_update
+ */
+#ifndef QPM_B200_H
+#define QPM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QPM_OK 0
+#define QPM_ERR_ARG -1
+#define QPM_ERR_CUDA -2
+#define QPM_ERR_STATE -3
+#define QPM_ERR_NCCL -4
+
+#define QPM_PROCESS_SHG 0
+#define QPM_PROCESS_THG 1
+
+/* fitness arithmetic: exact replays numba's sequential per-domain order
+ * bit-for-bit (parity tool); fast is the segmented FP64 quad-table scan. */
+#define QPM_MODE_FAST 0
+#define QPM_MODE_EXACT 1
+
+#define QPM_ALGO_HYBRID 0
+#define QPM_ALGO_DE 1
+#define QPM_ALGO_GWO 2
+
+/* columns of the per-generation schedule table (host-computed with Python
+ * float arithmetic so device decisions equal the reference's) */
+#define QPM_SCHED_F_ENV 0   /* f_min + (f_max - f_min) cos(pi g / 2G)      optimizer.py:290 */
+#define QPM_SCHED_DECAY 1   /* 1 - decay_strength (g/G)^2                   optimizer.py:166-168 */
+#define QPM_SCHED_P_DIST 2  /* p_dist0 (1 - g/G)                            optimizer.py:157-158 */
+#define QPM_SCHED_P_SL 3    /* p_sl0 (1 - g/G)                              optimizer.py:160-161 */
+#define QPM_SCHED_P_FLIP 4  /* p_flip0 (1 - g/G)                            optimizer.py:163-164 */
+#define QPM_SCHED_EARLY 5   /* 1.0 if g/G < phase_split                     optimizer.py:170-171 */
+#define QPM_SCHED_A_NOW 6   /* a_final + (a - a_final)(1 - g/G)   (run_gwo) optimizer.py:563-564 */
+#define QPM_SCHED_COLS 8
+
+const char *qpm_last_error(void);
+int qpm_version(void);
+/* number of SMs and compute capability of the current device */
+int qpm_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/* ------------------------------------------------------------------ RNG */
+uint64_t qpm_fold_key(int64_t seed, int npath, const int64_t *path);
+int qpm_uniform_fill(uint64_t key, uint64_t start, int64_t n, double *out_dev, void *stream);
+
+/* -------------------------------------------------------------- problem */
+typedef struct qpm_problem qpm_problem;
+
+/* Tables are host arrays, complex values interleaved (re, im):
+ *   e1[n_wl][D][2], b[n_wl][D][2] (THG only, else NULL),
+ *   w[n_wl][2] (w12 for THG, w1 for SHG), hconst[n_wl][2] (THG, else NULL).
+ * scale: divisor applied to |d_eff| (L or L^2/2), 1.0 for raw.
+ * multi: 1 for the multi-wavelength objective -(sum|g0-g| + beta(max-min)). */
+int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int64_t D, const double *e1,
+                       const double *b, const double *w, const double *hconst, double scale, double g0,
+                       double beta);
+int qpm_problem_destroy(qpm_problem *p);
+/* u32 words per bit-packed row (domains padded to a multiple of 128) */
+int64_t qpm_problem_row_words(const qpm_problem *p);
+
+/* pack int8 +/-1 rows [rows][D] into bit rows (bit 1 = -1) of stride row_words */
+int qpm_pack_signs(const int8_t *signs_dev, int64_t rows, int64_t D, uint32_t *bits_dev, int64_t row_words,
+                   void *stream);
+
+/* fitness of bit-packed rows.  row_index (device, may be NULL): row r reads
+ * bits_dev + row_index[r] * row_words.  out_dev: f64 [rows]. */
+int qpm_fitness_bits(qpm_problem *p, const uint32_t *bits_dev, int64_t row_words, const int32_t *row_index_dev,
+                     int64_t rows, double *out_dev, int mode, void *stream);
+
+/* host-buffer plugin path: int8 [rows][D] host -> f64 [rows] host (sync) */
+int qpm_evaluate_block_host(qpm_problem *p, const int8_t *signs, int64_t rows, double *out, int mode);
+/* complex kernel sums (thg_block / shg_block) of wavelength wl, host in/out:
+ * out[rows][2]; always the exact numba order */
+int qpm_sum_block_host(qpm_problem *p, int wl, const int8_t *signs, int64_t rows, double *out);
+
+/* -------------------------------------------------------------- leaders */
+/* top-k indices by (-value, index) of values_dev[n]; idx_out_dev int32 [k]; k <= 64 */
+int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out_dev, void *stream);
+
+/* --------------------------------------------------------------- engine */
+typedef struct {
+    int algorithm; /* QPM_ALGO_* */
+    int fitness_mode;
+    int64_t NP, G;
+    int64_t seed;
+    /* DEParams (optimizer.py:84-101) */
+    double f_max, f_min, cr, x_min, x_max;
+    /* GWOParams (optimizer.py:104-133) */
+    int leader_count;
+    double discreteness_factor;
+    int divide_by_leader_count;
+    /* Schedules thresholds (optimizer.py:136-155) */
+    double theta_low_frac, theta_high_frac, range_trigger_frac;
+    double explore_boost, exploit_factor, conv_threshold;
+    int conv_window;
+    int adaptive_branches;
+    /* run_gwo bounds and a0 (trace row 0) */
+    double gwo_lo, gwo_hi, gwo_a0;
+    /* row shard owned by this rank [row_lo, row_hi); 0, NP for one GPU */
+    int64_t row_lo, row_hi;
+} qpm_run_params;
+
+typedef struct qpm_engine qpm_engine;
+
+/* sched: host [G+1][QPM_SCHED_COLS] (see QPM_SCHED_*).  The problem must
+ * outlive the engine.  stream is captured by the engine's generation graph. */
+int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params *params, const double *sched,
+                      void *stream);
+int qpm_engine_destroy(qpm_engine *e);
+/* device bytes held by the engine */
+int64_t qpm_engine_device_bytes(const qpm_engine *e);
+/* init_population + generation-0 evaluation and trace row (async) */
+int qpm_engine_init(qpm_engine *e);
+/* run n generations (async; CUDA-graph replays when use_graph != 0) */
+int qpm_engine_step(qpm_engine *e, int64_t n, int use_graph);
+/* select the final best (top-1 of the current population, or best-ever for
+ * run_gwo) into the result buffer (async) */
+int qpm_engine_finalize(qpm_engine *e);
+int qpm_engine_generation(const qpm_engine *e, int64_t *g_done);
+/* copies (synchronous on the engine stream) */
+int qpm_engine_read_trace(qpm_engine *e, int64_t first_row, int64_t n_rows, double *host_rows);
+int qpm_engine_read_best(qpm_engine *e, double *genome, int8_t *proj, double *fitness);
+int qpm_engine_read_population(qpm_engine *e, double *genome, double *fitness);
+/* run n generations eagerly with CUDA events between the stages of each
+ * generation (advances the run); stage_ms[k] = mean ms of stage k, names
+ * are written as n_stages fixed-width strings of name_len bytes */
+int qpm_engine_profile(qpm_engine *e, int64_t n, double *stage_ms, int *n_stages, char *names, int name_len);
+/* kernel launches issued by one generation of this engine */
+int qpm_engine_launches_per_generation(const qpm_engine *e);
+/* device pointer to the fitness vector of individuals [NP] (for tests) */
+int qpm_engine_fitness_ptr(qpm_engine *e, double **fit_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QPM_B200_H */

@@ -1,0 +1,59 @@
+"""Build the sm_100a shared library in-tree (nvcc; no GPU needed to compile).
+
+    python -m paper_2511_01255_b200.build
+
+The library lands next to this file (paper_2511_01255_b200/libqpm_b200.so),
+so it ships to the GPU box with the repo snapshot.  -fmad=false keeps every
+multiply and add separately rounded (the reference's arithmetic); kernels
+that want FMAs call fma() explicitly.
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libqpm_b200.so")
+SOURCES = ["qpm_fitness.cu", "qpm_engine.cu"]
+HEADERS = ["qpm_common.cuh", "qpm_internal.cuh", os.path.join("..", "..", "include", "qpm_b200.h")]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-shared",
+              "-cudart", "static", "-Xptxas", "-v"]
+
+
+def nvcc() -> str:
+    path = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(path):
+        raise RuntimeError("nvcc not found; the CUDA 12.9 toolkit is required to build libqpm_b200.so")
+    return path
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    tmp = LIB + ".tmp"
+    cmd = [nvcc()] + NVCC_FLAGS + ARCH + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, LIB)
+    log = os.path.join(HERE, "csrc", "ptxas.log")
+    with open(log, "w") as fh:
+        fh.write(res.stderr)
+    if verbose:
+        print(res.stderr, file=sys.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,587 @@
+// qpm_fitness.cu -- cascaded-THG / SHG / multi-wavelength fitness on B200.
+//
+// Reference: PatternObjective.evaluate_block (objectives.py:110-120) ->
+// ThgEvaluator.deff_abs_block (physics.py:352-356) -> numba _thg_sum_nb
+// (_kernels.py:114-122):
+//
+//     acc = sum_j s_j * P_j * b_j,   P_j = sum_{x<j} s_x * e1_x
+//     fitness = |w12 * acc + hconst| / (L^2/2)
+//
+// Two device paths:
+//
+// * EXACT (parity tool): one thread per (row, wavelength) walks the domains
+//   in order with numba's arithmetic (int8 sign promoted to complex(s, 0),
+//   unfused complex products), so acc is bit-identical to the reference.
+//
+// * FAST (product): the domain axis is cut into quads of 4 domains.  For a
+//   quad with signs s0..s3 and relative signs sigma_k = s0 s_k, the three
+//   quantities a prefix scan needs are s0-flips of 8-entry tables indexed by
+//   sigma (built once per problem):
+//       sum s_k b_k           = s0 * B[sigma]
+//       sum s_k e1_k          = s0 * E[sigma]
+//       sum_{k<l} s_k s_l e1_k b_l = I[sigma]
+//   so each quad costs acc += P*sB + I (4 DFMA + 2 DADD), P += sE (2 DADD),
+//   T += sB (2 DADD): 10 FP64 instructions per 4 domain-evals instead of the
+//   direct form's 8 per domain.  The sign flip is an integer XOR on the high
+//   word.  A quad's 8 entries are one 128-byte shared-memory row, so any
+//   lane pattern is bank-conflict free.  Rows map to lanes (256 rows per CTA),
+//   the table chunk for 32 quads (12 KB) is staged in shared memory and
+//   shared by all 256 rows.  Segments of the domain axis run in parallel and
+//   are stitched by k_fit_finish:  acc = sum_s (acc_s + C_s T_s),
+//   C_s = sum_{s'<s} P_s', in a fixed order, so fitness is a pure function of
+//   the row bits (required: 18% of selections compare identical projections).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "qpm_common.cuh"
+#include "qpm_internal.cuh"
+
+namespace qpm {
+
+// ------------------------------------------------------------ error state
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+// ------------------------------------------------------------ small kernels
+__global__ void k_uniform_fill(uint64_t key, uint64_t start, int64_t n, double *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < n; i += stride) out[i] = draw_u(key, start + (uint64_t)i);
+}
+
+// int8 +/-1 rows -> bit rows; one warp per output word
+__global__ void k_pack_signs(const int8_t *__restrict__ signs, int64_t rows, int64_t D, uint32_t *__restrict__ bits,
+                             int64_t W) {
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    int64_t total = rows * W;
+    if (warp >= total) return;
+    int64_t r = warp / W, w = warp % W;
+    int64_t j = w * 32 + lane;
+    bool neg = j < D && signs[r * D + j] < 0;
+    uint32_t word = __ballot_sync(0xffffffffu, neg);
+    if (lane == 0) bits[r * W + w] = word;
+}
+
+// quad tables: entry rel (bit k-1 set <=> s_k != s_0) of B, E, I for quad q
+__global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__restrict__ b, int64_t D,
+                              int64_t nquads, int n_wl, int thg, double2 *__restrict__ qt) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nquads * n_wl) return;
+    int64_t lam = t / nquads, q = t % nquads;
+    double er[4], ei[4], br[4], bi[4];
+    for (int k = 0; k < 4; ++k) {
+        int64_t j = 4 * q + k;
+        bool in = j < D;
+        double2 e = in ? e1[lam * D + j] : make_double2(0.0, 0.0);
+        double2 bb = (in && thg) ? b[lam * D + j] : make_double2(0.0, 0.0);
+        er[k] = e.x;
+        ei[k] = e.y;
+        br[k] = bb.x;
+        bi[k] = bb.y;
+    }
+    double2 *out = qt + (lam * nquads + q) * kQuadEntries;
+    for (int rel = 0; rel < 8; ++rel) {
+        double sg[4] = {1.0, (rel & 1) ? -1.0 : 1.0, (rel & 2) ? -1.0 : 1.0, (rel & 4) ? -1.0 : 1.0};
+        double Br = 0, Bi = 0, Er = 0, Ei = 0, Ir = 0, Ii = 0;
+        for (int k = 0; k < 4; ++k) {
+            Br += sg[k] * br[k];
+            Bi += sg[k] * bi[k];
+            Er += sg[k] * er[k];
+            Ei += sg[k] * ei[k];
+        }
+        for (int l = 1; l < 4; ++l)
+            for (int k = 0; k < l; ++k) {
+                double s = sg[k] * sg[l];
+                double pr = er[k] * br[l] - ei[k] * bi[l];
+                double pi = er[k] * bi[l] + ei[k] * br[l];
+                Ir += s * pr;
+                Ii += s * pi;
+            }
+        out[rel] = make_double2(Br, Bi);
+        out[8 + rel] = make_double2(Er, Ei);
+        out[16 + rel] = make_double2(Ir, Ii);
+    }
+}
+
+// ------------------------------------------------------------ exact path
+// one thread per (row, wavelength); numba's _thg_sum_nb / _shg_sum_nb order
+__global__ void k_fit_exact(const double2 *__restrict__ e1, const double2 *__restrict__ b, int64_t D, int thg,
+                            const uint32_t *__restrict__ bits, int64_t W, const int32_t *__restrict__ row_index,
+                            int64_t rows, double *__restrict__ part) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int lam = blockIdx.y;
+    if (r >= rows) return;
+    const uint32_t *rb = bits + (int64_t)(row_index ? row_index[r] : r) * W;
+    const double2 *el = e1 + (int64_t)lam * D;
+    const double2 *bl = thg ? b + (int64_t)lam * D : nullptr;
+    double ar = 0.0, ai = 0.0, pr = 0.0, pi = 0.0;
+    uint32_t word = 0;
+    for (int64_t j = 0; j < D; ++j) {
+        if ((j & 31) == 0) word = rb[j >> 5];
+        double sd = ((word >> (j & 31)) & 1u) ? -1.0 : 1.0;
+        double2 e = el[j];
+        if (thg) {
+            double spr = sd * pr - 0.0 * pi;
+            double spi = sd * pi + 0.0 * pr;
+            double2 bb = bl[j];
+            double tr = spr * bb.x - spi * bb.y;
+            double ti = spr * bb.y + spi * bb.x;
+            ar += tr;
+            ai += ti;
+            pr += sd * e.x - 0.0 * e.y;
+            pi += sd * e.y + 0.0 * e.x;
+        } else {
+            ar += sd * e.x - 0.0 * e.y;
+            ai += sd * e.y + 0.0 * e.x;
+        }
+    }
+    double *o = part + ((int64_t)lam * rows + r) * kPartDoubles;
+    o[0] = ar;
+    o[1] = ai;
+    o[2] = 0.0;
+    o[3] = 0.0;
+    o[4] = 0.0;
+    o[5] = 0.0;
+}
+
+// ------------------------------------------------------------ fast path
+template <bool THG>
+__global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,
+                                                          int64_t nchunks, int seg_chunks, int S,
+                                                          const uint32_t *__restrict__ bits, int64_t W,
+                                                          const int32_t *__restrict__ row_index, int64_t rows,
+                                                          double *__restrict__ part) {
+    __shared__ __align__(128) double2 tab[kQuadsPerChunk * kQuadEntries];  // 12 KB
+    const int s = blockIdx.x;
+    const int lam = blockIdx.z;
+    const int tid = threadIdx.x;
+    const int64_t r = (int64_t)blockIdx.y * kFitThreads + tid;
+    const bool active = r < rows;
+    const uint4 *rb = reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? row_index[r] : r) : 0) * W);
+    const double2 *qtl = qt + (int64_t)lam * nquads * kQuadEntries;
+    double ar = 0.0, ai = 0.0, pr = 0.0, pi = 0.0, tr = 0.0, ti = 0.0;
+    const int64_t c0 = (int64_t)s * seg_chunks;
+    const int64_t c1 = c0 + seg_chunks < nchunks ? c0 + seg_chunks : nchunks;
+    for (int64_t c = c0; c < c1; ++c) {
+        __syncthreads();
+        const double2 *src = qtl + c * (kQuadsPerChunk * kQuadEntries);
+#pragma unroll
+        for (int k = 0; k < (kQuadsPerChunk * kQuadEntries) / kFitThreads; ++k)
+            tab[k * kFitThreads + tid] = src[k * kFitThreads + tid];
+        uint4 w4 = active ? rb[c] : make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        const uint32_t words[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int q = 0; q < kQuadsPerChunk; ++q) {
+            const uint32_t nib = (words[q >> 3] >> (4 * (q & 7))) & 0xFu;
+            const uint32_t s0 = nib & 1u;
+            const uint32_t rel = ((nib ^ (0u - s0)) >> 1) & 7u;
+            const uint64_t m = sign_mask64(s0);
+            const double2 *tq = tab + q * kQuadEntries;
+            const double2 E = tq[8 + rel];
+            const double ser = flip_if(E.x, m), sei = flip_if(E.y, m);
+            if (THG) {
+                const double2 B = tq[rel];
+                const double2 I = tq[16 + rel];
+                const double sbr = flip_if(B.x, m), sbi = flip_if(B.y, m);
+                ar = fma(pr, sbr, ar);
+                ar = fma(-pi, sbi, ar);
+                ar += I.x;
+                ai = fma(pr, sbi, ai);
+                ai = fma(pi, sbr, ai);
+                ai += I.y;
+                tr += sbr;
+                ti += sbi;
+            }
+            pr += ser;
+            pi += sei;
+        }
+    }
+    if (!active) return;
+    double *o = part + (((int64_t)lam * rows + r) * S + s) * kPartDoubles;
+    if (THG) {
+        o[0] = ar;
+        o[1] = ai;
+        o[2] = pr;
+        o[3] = pi;
+        o[4] = tr;
+        o[5] = ti;
+    } else {  // SHG: the sum is the prefix itself
+        o[0] = pr;
+        o[1] = pi;
+        o[2] = 0.0;
+        o[3] = 0.0;
+        o[4] = 0.0;
+        o[5] = 0.0;
+    }
+}
+
+// stitch segments, apply w/hconst, |.| (glibc hypot), scale, objective
+__global__ void k_fit_finish(const double *__restrict__ part, int S, int64_t rows, int n_wl,
+                             const double2 *__restrict__ w, const double2 *__restrict__ h, int thg, double scale,
+                             int multi, double g0, double beta, double *__restrict__ gains,
+                             double *__restrict__ out) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    double gmax = 0.0, gmin = 0.0;
+    for (int lam = 0; lam < n_wl; ++lam) {
+        const double *p = part + ((int64_t)lam * rows + r) * S * kPartDoubles;
+        double ar = p[0], ai = p[1], cr = p[2], ci = p[3];
+        for (int s = 1; s < S; ++s) {
+            const double *q = p + (int64_t)s * kPartDoubles;
+            double xr = fma(cr, q[4], fma(-ci, q[5], q[0]));
+            double xi = fma(cr, q[5], fma(ci, q[4], q[1]));
+            ar += xr;
+            ai += xi;
+            cr += q[2];
+            ci += q[3];
+        }
+        double2 ww = w[lam];
+        double zr = ww.x * ar - ww.y * ai;
+        double zi = ww.x * ai + ww.y * ar;
+        if (thg) {
+            double2 hh = h[lam];
+            zr += hh.x;
+            zi += hh.y;
+        }
+        double g = hypot_glibc(zr, zi);
+        if (scale != 1.0) g /= scale;
+        if (!multi) {
+            out[r] = g;
+            return;
+        }
+        if (lam == 0 || g > gmax) gmax = g;
+        if (lam == 0 || g < gmin) gmin = g;
+        gains[r * n_wl + lam] = g;
+    }
+    double *dv = gains + r * n_wl;
+    for (int lam = 0; lam < n_wl; ++lam) dv[lam] = fabs(g0 - dv[lam]);
+    double f = pairwise_sum_seq(dv, n_wl);
+    f += beta * (gmax - gmin);
+    out[r] = -f;
+}
+
+// ------------------------------------------------------------ top-k
+// parexec.reduce_best: k best by (-value, index), one CTA; k rounds of a
+// block-wide argmax over each thread's locally sorted candidates.
+constexpr int kTopkThreads = 512;
+constexpr int kTopkMax = 8;
+
+struct Cand {
+    double v;
+    int32_t i;
+};
+__device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
+    if (a.i < 0) return false;
+    if (b.i < 0) return true;
+    return a.v > b.v || (a.v == b.v && a.i < b.i);
+}
+
+__global__ void __launch_bounds__(kTopkThreads) k_topk(const double *__restrict__ vals, int64_t n, int k,
+                                                       int32_t *__restrict__ idx_out) {
+    Cand loc[kTopkMax];
+    for (int t = 0; t < kTopkMax; ++t) loc[t] = {0.0, -1};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        Cand c = {vals[i], (int32_t)i};
+        if (!better(c, loc[k - 1])) continue;
+        int pos = k - 1;
+        while (pos > 0 && better(c, loc[pos - 1])) {
+            loc[pos] = loc[pos - 1];
+            --pos;
+        }
+        loc[pos] = c;
+    }
+    __shared__ Cand red[kTopkThreads / 32];
+    __shared__ Cand win;
+    int head = 0;
+    for (int t = 0; t < k; ++t) {
+        Cand c = head < k ? loc[head] : Cand{0.0, -1};
+        for (int off = 16; off > 0; off >>= 1) {
+            Cand o;
+            o.v = __shfl_down_sync(0xffffffffu, c.v, off);
+            o.i = __shfl_down_sync(0xffffffffu, c.i, off);
+            if (better(o, c)) c = o;
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Cand best = red[0];
+            for (int wv = 1; wv < (int)(blockDim.x >> 5); ++wv)
+                if (better(red[wv], best)) best = red[wv];
+            win = best;
+            idx_out[t] = best.i;
+        }
+        __syncthreads();
+        if (head < k && loc[head].i == win.i && win.i >= 0) ++head;
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ launchers
+int problem_reserve(Problem *p, int64_t rows) {
+    if (rows <= p->part_rows) return QPM_OK;
+    if (p->part) cudaFree(p->part);
+    if (p->gains) cudaFree(p->gains);
+    p->part = nullptr;
+    p->gains = nullptr;
+    int64_t S = std::max<int64_t>(p->S, 1);
+    size_t bytes = (size_t)p->n_wl * rows * S * kPartDoubles * sizeof(double);
+    QPM_CUDA_TRY(cudaMalloc(&p->part, bytes));
+    QPM_CUDA_TRY(cudaMalloc(&p->gains, (size_t)rows * p->n_wl * sizeof(double)));
+    p->part_rows = rows;
+    p->device_bytes += (int64_t)bytes + rows * p->n_wl * 8;
+    return QPM_OK;
+}
+
+int launch_fitness(Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index, int64_t rows,
+                   double *out, int mode, cudaStream_t stream, int *launches) {
+    QPM_ARG_CHECK(row_words == p->W, "row_words must equal qpm_problem_row_words()");
+    QPM_ARG_CHECK(rows >= 0, "rows >= 0");
+    if (rows == 0) return QPM_OK;
+    QPM_ARG_CHECK(rows <= p->part_rows, "rows exceed the reserved fitness scratch");
+    const int thg = p->process == QPM_PROCESS_THG;
+    int S;
+    if (mode == QPM_MODE_EXACT) {
+        S = 1;
+        dim3 grid((unsigned)((rows + 127) / 128), (unsigned)p->n_wl);
+        k_fit_exact<<<grid, 128, 0, stream>>>(p->e1, p->b, p->D, thg, bits, p->W, row_index, rows, p->part);
+    } else {
+        S = p->S;
+        dim3 grid((unsigned)S, (unsigned)((rows + kFitThreads - 1) / kFitThreads), (unsigned)p->n_wl);
+        if (thg)
+            k_fit_fast<true><<<grid, kFitThreads, 0, stream>>>(p->qt, p->nquads, p->nchunks, p->seg_chunks, S,
+                                                               bits, p->W, row_index, rows, p->part);
+        else
+            k_fit_fast<false><<<grid, kFitThreads, 0, stream>>>(p->qt, p->nquads, p->nchunks, p->seg_chunks, S,
+                                                                bits, p->W, row_index, rows, p->part);
+    }
+    QPM_LAUNCH_CHECK();
+    k_fit_finish<<<(unsigned)((rows + 127) / 128), 128, 0, stream>>>(p->part, S, rows, p->n_wl, p->w, p->h, thg,
+                                                                     p->scale, p->multi, p->g0, p->beta, p->gains,
+                                                                     out);
+    QPM_LAUNCH_CHECK();
+    if (launches) *launches += 2;
+    return QPM_OK;
+}
+
+int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out, cudaStream_t stream) {
+    QPM_ARG_CHECK(n >= 1, "cannot reduce an empty list");
+    QPM_ARG_CHECK(k >= 1 && k <= n && k <= kTopkMax, "k must be in [1, min(n, 8)]");
+    k_topk<<<1, kTopkThreads, 0, stream>>>(values, n, k, idx_out);
+    QPM_LAUNCH_CHECK();
+    return QPM_OK;
+}
+
+int launch_pack(const int8_t *signs, int64_t rows, int64_t D, uint32_t *bits, int64_t W, cudaStream_t stream) {
+    int64_t warps = rows * W;
+    if (warps == 0) return QPM_OK;
+    int64_t threads = warps * 32;
+    k_pack_signs<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(signs, rows, D, bits, W);
+    QPM_LAUNCH_CHECK();
+    return QPM_OK;
+}
+
+static int host_path_reserve(Problem *p, int64_t rows) {
+    if (!p->hp_stream) QPM_CUDA_TRY(cudaStreamCreateWithFlags(&p->hp_stream, cudaStreamNonBlocking));
+    if (rows > p->hp_rows) {
+        cudaFree(p->hp_signs);
+        cudaFree(p->hp_bits);
+        cudaFree(p->hp_out);
+        p->hp_signs = nullptr;
+        p->hp_bits = nullptr;
+        p->hp_out = nullptr;
+        QPM_CUDA_TRY(cudaMalloc(&p->hp_signs, (size_t)rows * p->D));
+        QPM_CUDA_TRY(cudaMalloc(&p->hp_bits, (size_t)rows * p->W * 4));
+        QPM_CUDA_TRY(cudaMalloc(&p->hp_out, (size_t)rows * 2 * sizeof(double)));
+        p->hp_rows = rows;
+    }
+    return problem_reserve(p, rows);
+}
+
+}  // namespace qpm
+
+using namespace qpm;
+
+// ======================================================================
+// C ABI
+// ======================================================================
+extern "C" {
+
+const char *qpm_last_error(void) { return g_last_error.c_str(); }
+
+int qpm_version(void) { return 10000; }
+
+int qpm_device_info(int *sm_count, int *cc_major, int *cc_minor) {
+    int dev = 0;
+    QPM_CUDA_TRY(cudaGetDevice(&dev));
+    if (sm_count) QPM_CUDA_TRY(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev));
+    if (cc_major) QPM_CUDA_TRY(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (cc_minor) QPM_CUDA_TRY(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+    return QPM_OK;
+}
+
+uint64_t qpm_fold_key(int64_t seed, int npath, const int64_t *path) {
+    uint64_t h = mix64((uint64_t)seed);
+    for (int k = 0; k < npath; ++k) h = mix64(h + kGold + (uint64_t)path[k]);
+    return h;
+}
+
+int qpm_uniform_fill(uint64_t key, uint64_t start, int64_t n, double *out_dev, void *stream) {
+    QPM_ARG_CHECK(n >= 0 && (n == 0 || out_dev), "n >= 0 and out_dev");
+    if (n == 0) return QPM_OK;
+    int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    k_uniform_fill<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(key, start, n, out_dev);
+    QPM_LAUNCH_CHECK();
+    return QPM_OK;
+}
+
+int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int64_t D, const double *e1,
+                       const double *b, const double *w, const double *hconst, double scale, double g0,
+                       double beta) {
+    QPM_ARG_CHECK(out, "out");
+    QPM_ARG_CHECK(process == QPM_PROCESS_SHG || process == QPM_PROCESS_THG, "process");
+    QPM_ARG_CHECK(n_wl >= 1 && n_wl <= 65535, "n_wl in [1, 65535]");
+    QPM_ARG_CHECK(D >= 1, "D >= 1");
+    QPM_ARG_CHECK(e1 && w, "e1 and w tables");
+    QPM_ARG_CHECK(process == QPM_PROCESS_SHG || (b && hconst), "THG needs b and hconst tables");
+    auto *h = new qpm_problem();
+    Problem &p = h->p;
+    p.process = process;
+    p.multi = multi ? 1 : 0;
+    p.n_wl = n_wl;
+    p.D = D;
+    p.W = round_up((D + 31) / 32, 4);
+    p.nquads = p.W * 8;
+    p.nchunks = p.W / 4;
+    // segments: one 128-domain chunk per segment for a single wavelength;
+    // longer segments when the wavelength axis already supplies parallelism
+    p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, n_wl));
+    p.S = (int)((p.nchunks + p.seg_chunks - 1) / p.seg_chunks);
+    p.scale = scale;
+    p.g0 = g0;
+    p.beta = beta;
+    size_t tab = (size_t)n_wl * D * sizeof(double2);
+    size_t qtb = (size_t)n_wl * p.nquads * kQuadEntries * sizeof(double2);
+    auto fail = [&](int code) {
+        qpm_problem_destroy(h);
+        return code;
+    };
+    if (cudaMalloc(&p.e1, tab) != cudaSuccess) return fail((set_error("cudaMalloc e1"), QPM_ERR_CUDA));
+    if (cudaMalloc(&p.b, tab) != cudaSuccess) return fail((set_error("cudaMalloc b"), QPM_ERR_CUDA));
+    if (cudaMalloc(&p.qt, qtb) != cudaSuccess) return fail((set_error("cudaMalloc quad tables"), QPM_ERR_CUDA));
+    if (cudaMalloc(&p.w, n_wl * sizeof(double2)) != cudaSuccess) return fail((set_error("cudaMalloc w"), QPM_ERR_CUDA));
+    if (cudaMalloc(&p.h, n_wl * sizeof(double2)) != cudaSuccess) return fail((set_error("cudaMalloc h"), QPM_ERR_CUDA));
+    p.device_bytes = (int64_t)(2 * tab + qtb + 2 * n_wl * sizeof(double2));
+    std::vector<double> zeros;
+    if (cudaMemcpy(p.e1, e1, tab, cudaMemcpyHostToDevice) != cudaSuccess) return fail((set_error("upload e1"), QPM_ERR_CUDA));
+    if (b) {
+        if (cudaMemcpy(p.b, b, tab, cudaMemcpyHostToDevice) != cudaSuccess) return fail((set_error("upload b"), QPM_ERR_CUDA));
+    } else if (cudaMemset(p.b, 0, tab) != cudaSuccess) {
+        return fail((set_error("memset b"), QPM_ERR_CUDA));
+    }
+    if (cudaMemcpy(p.w, w, n_wl * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail((set_error("upload w"), QPM_ERR_CUDA));
+    if (hconst) {
+        if (cudaMemcpy(p.h, hconst, n_wl * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess)
+            return fail((set_error("upload hconst"), QPM_ERR_CUDA));
+    } else if (cudaMemset(p.h, 0, n_wl * sizeof(double2)) != cudaSuccess) {
+        return fail((set_error("memset h"), QPM_ERR_CUDA));
+    }
+    int64_t nt = p.nquads * n_wl;
+    k_build_quads<<<(unsigned)((nt + 127) / 128), 128>>>(p.e1, p.b, D, p.nquads, n_wl,
+                                                          process == QPM_PROCESS_THG, p.qt);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        return fail((set_error("building quad tables failed"), QPM_ERR_CUDA));
+    *out = h;
+    return QPM_OK;
+}
+
+int qpm_problem_destroy(qpm_problem *h) {
+    if (!h) return QPM_OK;
+    Problem &p = h->p;
+    cudaFree(p.e1);
+    cudaFree(p.b);
+    cudaFree(p.qt);
+    cudaFree(p.w);
+    cudaFree(p.h);
+    cudaFree(p.part);
+    cudaFree(p.gains);
+    cudaFree(p.hp_signs);
+    cudaFree(p.hp_bits);
+    cudaFree(p.hp_out);
+    if (p.hp_stream) cudaStreamDestroy(p.hp_stream);
+    delete h;
+    return QPM_OK;
+}
+
+int64_t qpm_problem_row_words(const qpm_problem *h) { return h ? h->p.W : -1; }
+
+int qpm_pack_signs(const int8_t *signs_dev, int64_t rows, int64_t D, uint32_t *bits_dev, int64_t row_words,
+                   void *stream) {
+    QPM_ARG_CHECK(rows >= 0 && D >= 1 && row_words * 32 >= D, "shape");
+    return launch_pack(signs_dev, rows, D, bits_dev, row_words, (cudaStream_t)stream);
+}
+
+int qpm_fitness_bits(qpm_problem *h, const uint32_t *bits_dev, int64_t row_words, const int32_t *row_index_dev,
+                     int64_t rows, double *out_dev, int mode, void *stream) {
+    QPM_ARG_CHECK(h, "problem");
+    int rc = problem_reserve(&h->p, rows);
+    if (rc) return rc;
+    return launch_fitness(&h->p, bits_dev, row_words, row_index_dev, rows, out_dev, mode, (cudaStream_t)stream,
+                          nullptr);
+}
+
+int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, double *out, int mode) {
+    QPM_ARG_CHECK(h && signs && out, "problem, signs, out");
+    QPM_ARG_CHECK(rows >= 1, "batch items must be non-empty");
+    Problem &p = h->p;
+    int rc = host_path_reserve(&p, rows);
+    if (rc) return rc;
+    QPM_CUDA_TRY(cudaMemcpyAsync(p.hp_signs, signs, (size_t)rows * p.D, cudaMemcpyHostToDevice, p.hp_stream));
+    rc = launch_pack(p.hp_signs, rows, p.D, p.hp_bits, p.W, p.hp_stream);
+    if (rc) return rc;
+    rc = launch_fitness(&p, p.hp_bits, p.W, nullptr, rows, p.hp_out, mode, p.hp_stream, nullptr);
+    if (rc) return rc;
+    QPM_CUDA_TRY(cudaMemcpyAsync(out, p.hp_out, (size_t)rows * sizeof(double), cudaMemcpyDeviceToHost, p.hp_stream));
+    QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
+    return QPM_OK;
+}
+
+int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows, double *out) {
+    QPM_ARG_CHECK(h && signs && out, "problem, signs, out");
+    QPM_ARG_CHECK(rows >= 1, "rows >= 1");
+    Problem &p = h->p;
+    QPM_ARG_CHECK(wl >= 0 && wl < p.n_wl, "wavelength index");
+    int rc = host_path_reserve(&p, rows);
+    if (rc) return rc;
+    QPM_CUDA_TRY(cudaMemcpyAsync(p.hp_signs, signs, (size_t)rows * p.D, cudaMemcpyHostToDevice, p.hp_stream));
+    rc = launch_pack(p.hp_signs, rows, p.D, p.hp_bits, p.W, p.hp_stream);
+    if (rc) return rc;
+    const int thg = p.process == QPM_PROCESS_THG;
+    k_fit_exact<<<(unsigned)((rows + 127) / 128), 128, 0, p.hp_stream>>>(
+        p.e1 + (int64_t)wl * p.D, thg ? p.b + (int64_t)wl * p.D : nullptr, p.D, thg, p.hp_bits, p.W, nullptr, rows,
+        p.part);
+    QPM_LAUNCH_CHECK();
+    // part rows are [acc.r, acc.i, 0, 0, 0, 0]; gather the first two doubles
+    QPM_CUDA_TRY(cudaMemcpy2DAsync(out, 2 * sizeof(double), p.part, kPartDoubles * sizeof(double),
+                                   2 * sizeof(double), (size_t)rows, cudaMemcpyDeviceToHost, p.hp_stream));
+    QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
+    return QPM_OK;
+}
+
+int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out_dev, void *stream) {
+    return launch_reduce_best(values_dev, n, k, idx_out_dev, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// qpm_internal.cuh -- host-side internals shared by the .cu translation units.
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/qpm_b200.h"
+
+namespace qpm {
+
+void set_error(const char *fmt, ...);
+
+#define QPM_CUDA_TRY(expr)                                                                           \
+    do {                                                                                             \
+        cudaError_t _e = (expr);                                                                     \
+        if (_e != cudaSuccess) {                                                                     \
+            ::qpm::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+            return QPM_ERR_CUDA;                                                                     \
+        }                                                                                            \
+    } while (0)
+
+#define QPM_LAUNCH_CHECK()                                                                                 \
+    do {                                                                                                   \
+        cudaError_t _e = cudaGetLastError();                                                               \
+        if (_e != cudaSuccess) {                                                                           \
+            ::qpm::set_error("%s:%d kernel launch failed: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \
+            return QPM_ERR_CUDA;                                                                           \
+        }                                                                                                  \
+    } while (0)
+
+#define QPM_ARG_CHECK(cond, msg)                               \
+    do {                                                       \
+        if (!(cond)) {                                         \
+            ::qpm::set_error("invalid argument: %s", (msg));   \
+            return QPM_ERR_ARG;                                \
+        }                                                      \
+    } while (0)
+
+constexpr int kFitThreads = 256;      // rows per fast-fitness CTA (one lane per row)
+constexpr int kQuadsPerChunk = 32;    // 128 domains = 4 u32 words per chunk
+constexpr int kQuadEntries = 24;      // B[8], E[8], I[8] complex entries per quad
+constexpr int kPartDoubles = 6;       // acc, P, T (complex) per (row, wavelength, segment)
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// device-resident problem (one PatternObjective)
+struct Problem {
+    int process = 1, multi = 0, n_wl = 1;
+    int64_t D = 0;
+    int64_t W = 0;        // u32 words per bit row (multiple of 4)
+    int64_t nquads = 0;   // W * 8
+    int64_t nchunks = 0;  // W / 4
+    int seg_chunks = 1;   // chunks per fast-scan segment
+    int S = 1;            // segments per row
+    double scale = 1.0, g0 = 2.0, beta = 1.0;
+    double2 *e1 = nullptr;  // [n_wl][D]
+    double2 *b = nullptr;   // [n_wl][D] (thg)
+    double2 *qt = nullptr;  // [n_wl][nquads][24]
+    double2 *w = nullptr;   // [n_wl]
+    double2 *h = nullptr;   // [n_wl]
+    // scratch for fitness launches, sized by reserve()
+    double *part = nullptr;
+    int64_t part_rows = 0;
+    double *gains = nullptr;
+    // host plugin path buffers
+    int8_t *hp_signs = nullptr;
+    uint32_t *hp_bits = nullptr;
+    double *hp_out = nullptr;
+    int64_t hp_rows = 0;
+    cudaStream_t hp_stream = nullptr;
+    int64_t device_bytes = 0;
+};
+
+int problem_reserve(Problem *p, int64_t rows);
+// launch the fitness of `rows` bit rows (row_index may be null) into out
+int launch_fitness(Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index, int64_t rows,
+                   double *out, int mode, cudaStream_t stream, int *launches);
+int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out, cudaStream_t stream);
+
+}  // namespace qpm
+
+struct qpm_problem {
+    qpm::Problem p;
+};

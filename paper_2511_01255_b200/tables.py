@@ -221,3 +221,34 @@ def cos_envelope(f_min: float, f_max: float, g: int, total: int) -> float:
     """f_min + (f_max - f_min) cos(pi g / 2G) with Python's libm cos (optimizer.py:290)."""
     progress = g / total if total > 0 else 0.0
     return f_min + (f_max - f_min) * math.cos(0.5 * math.pi * progress)
+
+
+@dataclass(frozen=True)
+class DomainPattern:
+    """Equal-thickness +/-1 domain sequence (reference physics.py:43-83)."""
+
+    thickness_um: float
+    signs: np.ndarray
+
+    def __post_init__(self):
+        if not self.thickness_um > 0:
+            raise ValueError(f"domain thickness must be > 0, got {self.thickness_um}")
+        raw = np.asarray(self.signs)
+        if raw.ndim != 1 or raw.size < 1:
+            raise ValueError("signs must be a non-empty 1-d sequence")
+        s8 = raw.astype(np.int8)
+        if not np.array_equal(s8, raw) or not np.all(np.abs(s8) == 1):
+            raise ValueError("every domain sign must be exactly +1 or -1")
+        s8.setflags(write=False)
+        object.__setattr__(self, "signs", s8)
+
+    @property
+    def count(self) -> int:
+        return int(self.signs.size)
+
+    @property
+    def length_um(self) -> float:
+        return self.count * self.thickness_um
+
+    def flipped(self) -> "DomainPattern":
+        return DomainPattern(self.thickness_um, -self.signs)
