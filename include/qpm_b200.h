@@ -141,7 +141,8 @@ typedef struct {
 typedef struct qpm_engine qpm_engine;
 
 /* sched: host [G+1][QPM_SCHED_COLS] (see QPM_SCHED_*).  The problem must
- * outlive the engine.  stream is captured by the engine's generation graph. */
+ * outlive the engine.  stream is captured by the engine's generation graph;
+ * NULL makes the engine create (and own) a non-blocking stream. */
 int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params *params, const double *sched,
                       void *stream);
 int qpm_engine_destroy(qpm_engine *e);

@@ -548,6 +548,7 @@ struct Engine {
     int launches = 0;
     int64_t g_done = 0;
     bool initialized = false;
+    bool owns_stream = false;
     int64_t device_bytes = 0;
     std::vector<void *> allocs;
 };
@@ -665,6 +666,10 @@ static int enqueue_generation(Engine *e, int *launches, StageMarks *pm = nullptr
 }
 
 static void engine_free(Engine *e) {
+    if (e->owns_stream && e->stream) {
+        cudaStreamSynchronize(e->stream);
+        cudaStreamDestroy(e->stream);
+    }
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
     for (void *p : e->allocs) cudaFree(p);
@@ -697,6 +702,15 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     e->prob = &prob->p;
     e->P = *P;
     e->stream = (cudaStream_t)stream;
+    if (!e->stream) {
+        // graphs cannot be captured on the legacy default stream: own a stream
+        if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            set_error("cudaStreamCreateWithFlags failed");
+            delete e;
+            return QPM_ERR_CUDA;
+        }
+        e->owns_stream = true;
+    }
     RunConsts &c = e->c;
     c.algorithm = P->algorithm;
     c.NP = P->NP;
@@ -796,7 +810,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
 
 int qpm_engine_destroy(qpm_engine *h) {
     if (!h) return QPM_OK;
-    if (h->e->stream) cudaStreamSynchronize(h->e->stream);
+    if (h->e->stream && !h->e->owns_stream) cudaStreamSynchronize(h->e->stream);
     engine_free(h->e);
     delete h;
     return QPM_OK;

@@ -228,7 +228,8 @@ class Engine:
         self.NP = int(pop_size)
         self.G = int(generations)
         self.D = objective.dimension
-        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
+        self.stream = stream if stream is not None else torch.cuda.Stream(dev)
         mode = fitness_mode or objective.mode
         from .objectives import MODES
         from .rng import signed64
