@@ -242,7 +242,7 @@ def run_ours(args):
     obj = build_objective(q)
     de, gwo, sch = q.DEParams(), q.GWOParams(), q.Schedules()
     G = max(G_RUN, args.warmup + args.steps)
-    stream = torch.cuda.Stream(dev)
+    stream = torch.cuda.Stream(dev, priority=min(torch.cuda.Stream.priority_range()))
     # replicas with per-rank seeds until the sharded engine lands
     eng = q.Engine(obj, "hybrid", pop_size=NP, generations=G, seed=SEED + rank, de=de, gwo=gwo, sch=sch,
                    stream=stream)

@@ -2,23 +2,34 @@
 // run_de / run_gwo, optimizer.py:400-592) for one B200.
 //
 // HBM layout (one engine):
-//   genome  f64 [2 NP][Dp]   slot pool; individual i lives in slot_of[i],
-//                            its trial / candidate is written to spare_of[i]
-//                            and acceptance swaps the two ids (no row copies)
+//   genome  f64 [2 NP][Dp]   slot pool; individual i lives in slot_of[i], its
+//                            trial / candidate goes to spare_of[i] and
+//                            acceptance swaps the two ids (no row copies)
 //   bits    u32 [2 NP][W]    sign bits of each slot (bit 1 <=> gene < 0)
-//   fit     f64 [NP]         fitness of individual i;  cand f64 [NP]
-//   keys    u64 [NP]         fold_key(seed, g, i) of the current generation
-//   picks   int4 [NP]        r1, r2, r3 and the index-draw count m (DE)
+//   slot_bin u8 [2 NP]       1 = the slot holds a wolf candidate whose genome is
+//                            exactly +/-1 (optimizer.py:376): its f64 row is
+//                            never written, readers expand the bits instead
+//   planes  u32 [NP][W][8]   per-gene wolf draw outcomes as bit-planes (k_de_trial)
+//   fit, cand f64 [NP]; keys u64 [NP]; picks int4 [NP] (r1, r2, r3, m)
 //   sched   f64 [G+1][8]     per-generation scalars, host-computed
-//   trace   f64 [G+1][5]     (g, best, mean, F|a, pop_std) rows
+//   trace   f64 [G+1][5]     (g, best, mean, F|a, pop_std)
 //   state   EngineState      g, F, window, leaders, best-ever bookkeeping
 // Dp = W * 32 with W a multiple of 4, so rows start on 512-byte boundaries.
 //
-// Every generation is a fixed launch sequence that reads g and F from
-// device memory, so one CUDA graph replays it for all generations with no
-// host round trip.  Decisions reproduce the reference bit-for-bit given the
-// same fitness values:
-//   - stream positions follow Appendix A of SURVEY.md (de_mutate rejection
+// One hybrid generation is 8 launches, all reading g and F from device
+// memory so a single CUDA graph replays every generation:
+//   k_de_trial      DE index draws (thread 0 of each block), crossover mask,
+//                   trial genome + bits, AND the wolf phase's three random
+//                   draws per gene folded into a 1-byte decision code.  The
+//                   kernel is HBM-bound; the splitmix64 integer work of the
+//                   wolf phase rides in its shadow.
+//   fitness x2      segmented quad-table scan + warp-parallel stitch
+//   k_select_topk   greedy selection + top-k leaders (one CTA)
+//   k_gwo_apply     leader vote per gene from the codes -> candidate bits
+//   fitness x2
+//   k_select_stats  wolf selection + np.max/mean/std replica + F update
+// Decisions reproduce the reference bit-for-bit given the same fitness:
+//   - stream positions follow SURVEY.md Appendix A (de_mutate rejection
 //     draws 0..m-1, j_rand at m, mask m+1..m+D, wolf block from m+1+D);
 //   - DE arithmetic x_r1 + F (x_r2 - x_r3) is unfused (-fmad=false);
 //   - u < p comparisons are exact integer compares on the 53-bit mantissa;
@@ -35,13 +46,15 @@ namespace qpm {
 
 constexpr int kMaxLeaders = 8;
 constexpr int kMaxWindow = 256;
-constexpr int kRowThreads = 256;   // threads per row-block in the elementwise kernels
-constexpr int kGenesPerThread = 4; // genes per thread (strided by kRowThreads)
+constexpr int kRowThreads = 256;    // threads per row-block in the elementwise kernels
+constexpr int kGenesPerThread = 4;  // genes per thread (strided by kRowThreads)
 constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
-constexpr int kStatsThreads = 512;
+constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
+constexpr int64_t kStatsSmemMaxNP = 12288;  // 2 x NP doubles of dynamic smem (<= 192 KB)
 
 struct EngineState {
-    int64_t g;  // generation computed next (0 before init)
+    int64_t g;       // generation computed next (0 before init)
+    int64_t g_plan;  // generation the planner draws next
     double F;
     double best_prev;
     double baseline_std;
@@ -51,9 +64,26 @@ struct EngineState {
     int32_t win_len;
     int32_t pad0;
     int32_t leaders[kMaxLeaders];
-    uint64_t thr_plus[kMaxLeaders + 1];  // u_plus < p_plus(count) thresholds
+    uint64_t thr_plus[kMaxLeaders + 1];  // u_plus < p_plus(count) thresholds, nondecreasing
     uint8_t win[kMaxWindow];
 };
+
+// u < p as a compare on the raw 64-bit mix:  (mix >> 11) < T  <=>
+// mix <= ((T - 1) << 11 | 0x7ff) for 1 <= T <= 2^53; T = 0 never passes.
+struct Thr {
+    uint64_t le;
+    uint32_t never;
+};
+__host__ __device__ __forceinline__ Thr make_thr(uint64_t T) {
+    Thr t;
+    t.never = T == 0;
+    if (T >= kTwo53)
+        t.le = ~0ULL;  // p >= 1: every draw passes
+    else
+        t.le = T == 0 ? 0 : (((T - 1) << 11) | 0x7ffULL);
+    return t;
+}
+__device__ __forceinline__ bool passes(const Thr &t, uint64_t mix) { return !t.never && mix <= t.le; }
 
 struct RunConsts {
     int algorithm;
@@ -69,44 +99,61 @@ struct RunConsts {
     int conv_window;
     int adaptive;
     double gwo_a0;
-    int64_t n_leaf;  // pairwise-sum leaves of an NP-vector
+    // numpy pairwise-sum tree of an NP-vector: leaves, then internal nodes by height
+    int32_t n_leaf, n_levels;
+    Thr thr_cr;      // u <= CR (de_crossover)
+    int plus_dyadic; // K = 4 and p_plus(c) = c/4 exactly: plus level = 1 + floor(4u)
+    Thr thr_plus[5]; // u_plus < p_plus(count), count = 0..K (hybrid K <= 4)
 };
 
-// ---------------------------------------------------------------- init
-__global__ void __launch_bounds__(kRowThreads) k_init_population(RunConsts c, double *__restrict__ genome,
-                                                                 uint32_t *__restrict__ bits,
-                                                                 int32_t *__restrict__ slot_of,
-                                                                 int32_t *__restrict__ spare_of) {
-    const int64_t i = blockIdx.y;
-    const uint64_t key = fold_key3(c.seed, 0, (uint64_t)i);  // stream (seed, 0, i), optimizer.py:223
-    double *row = genome + i * c.Dp;
-    uint32_t *brow = bits + i * c.W;
-#pragma unroll
-    for (int it = 0; it < kGenesPerThread; ++it) {
-        const int64_t j = (int64_t)blockIdx.x * kGenesPerBlock + it * kRowThreads + threadIdx.x;
-        bool neg = false;
-        if (j < c.D) {
-            const double x = c.x_lo + draw_u(key, (uint64_t)j) * c.x_span;
-            row[j] = x;
-            neg = !(x >= 0.0);
-        }
-        const uint32_t word = __ballot_sync(0xffffffffu, neg);
-        if ((threadIdx.x & 31) == 0 && j < c.Dp) brow[j >> 5] = word;
+// pairwise-sum tree (host-built, see build_tree): leaf l covers
+// [leaf_off[l], leaf_off[l+1]); internal node t (id n_leaf + t) adds nodes
+// kid[2t] + kid[2t+1]; level h holds internal nodes [lvl[h], lvl[h+1]).
+struct SumTree {
+    const int32_t *leaf_off;
+    const int32_t *kid;
+    const int32_t *lvl;
+    double *val;  // [2 n_leaf - 1]
+};
+
+// ---------------------------------------------------------------- helpers
+// draw at counter position p1 = pos + 1 (< 2^32): mix(key + p1 * GOLD).  The
+// 32 x 64 product is one IMAD.WIDE.U32 (key as addend) plus one IMAD on the
+// FMA pipe; the ALU pipe, which the xorshifts saturate, is left alone.
+__device__ __forceinline__ uint64_t mix_at(uint64_t key, uint32_t p1) { return mix64(key + (uint64_t)p1 * kGold); }
+
+// per-generation wolf thresholds (host-built from the schedule table)
+struct GenThr {
+    Thr sl, dist, flip;
+    uint32_t early;
+    uint32_t pad;
+};
+
+// a genome row that is either f64 or, for wolf candidates, +/-1 bits
+struct RowRef {
+    const double *f;
+    const uint32_t *b;
+    __device__ __forceinline__ double at(int j) const {
+        if (f) return f[j];
+        return ((b[j >> 5] >> (j & 31)) & 1u) ? -1.0 : 1.0;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        slot_of[i] = (int32_t)i;
-        spare_of[i] = (int32_t)(c.NP + i);
+};
+
+__device__ __forceinline__ RowRef row_ref(const RunConsts &c, int64_t slot, const uint8_t *slot_bin,
+                                          const double *genome, const uint32_t *bits) {
+    RowRef r;
+    if (slot_bin[slot]) {
+        r.f = nullptr;
+        r.b = bits + slot * c.W;
+    } else {
+        r.f = genome + slot * c.Dp;
+        r.b = nullptr;
     }
+    return r;
 }
 
-// ---------------------------------------------------------------- DE
-// de_mutate index draws (optimizer.py:229-247) + j_rand (optimizer.py:258)
-__global__ void k_de_draws(RunConsts c, const EngineState *__restrict__ st, uint64_t *__restrict__ keys,
-                           int4 *__restrict__ picks, int32_t *__restrict__ jrand) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= c.NP) return;
-    const uint64_t key = fold_key3(c.seed, (uint64_t)st->g, (uint64_t)i);
-    keys[i] = key;
+// de_mutate index draws (optimizer.py:229-247) and j_rand (optimizer.py:258)
+__device__ void de_row_draws(const RunConsts &c, uint64_t key, int64_t i, int4 &pk, int32_t &jr) {
     int64_t r[3];
     int n = 0;
     uint64_t m = 0;
@@ -117,199 +164,440 @@ __global__ void k_de_draws(RunConsts c, const EngineState *__restrict__ st, uint
         for (int t = 0; t < n; ++t) dup |= cand == r[t];
         if (!dup) r[n++] = cand;
     }
-    picks[i] = make_int4((int)r[0], (int)r[1], (int)r[2], (int)m);
-    jrand[i] = (int32_t)randint(key, m, c.D);
+    pk = make_int4((int)r[0], (int)r[1], (int)r[2], (int)m);
+    jr = (int32_t)randint(key, m, c.D);
 }
 
-// de_crossover (optimizer.py:250-262): trial_j = (u_j <= CR or j == j_rand)
-// ? x_r1 + F (x_r2 - x_r3) : x_i, written to the spare slot with its bits.
-__global__ void __launch_bounds__(kRowThreads) k_de_trial(RunConsts c, const EngineState *__restrict__ st,
-                                                          const uint64_t *__restrict__ keys,
-                                                          const int4 *__restrict__ picks,
-                                                          const int32_t *__restrict__ jrand,
-                                                          const int32_t *__restrict__ slot_of,
-                                                          const int32_t *__restrict__ spare_of,
-                                                          double *__restrict__ genome, uint32_t *__restrict__ bits) {
-    const int64_t i = blockIdx.y;
-    const int4 pk = picks[i];
-    const uint64_t key = keys[i];
-    const int64_t jr = jrand[i];
-    const double F = st->F;
-    const double *xi = genome + (int64_t)slot_of[i] * c.Dp;
-    const double *x1 = genome + (int64_t)slot_of[pk.x] * c.Dp;
-    const double *x2 = genome + (int64_t)slot_of[pk.y] * c.Dp;
-    const double *x3 = genome + (int64_t)slot_of[pk.z] * c.Dp;
-    const int64_t out_slot = spare_of[i];
-    double *out = genome + out_slot * c.Dp;
-    uint32_t *bout = bits + out_slot * c.W;
-    const uint64_t base = (uint64_t)pk.w + 1;
+
+// ---------------------------------------------------------------- wolf planes
+// gwo_discrete_update (optimizer.py:335-376) needs, per gene, the outcome of
+// at most three draws of the 6 x D block:
+//   row 0 social;  row 1 pick (social) | 2 disturb (early) | 5 flip (late);
+//   row 3 state | 4 plus (early, not disturbed).
+// They are recorded as 8 bit-planes per 32-gene word (one ballot each):
+//   0 social   1-2 pick   3 disturbed|flipped   4 state (+1)
+//   5-7 plus level L = #{c <= K : u_plus >= p_plus(c)}  (p_plus is
+//   nondecreasing in c, so u_plus < p_plus(count) <=> count >= L).
+// The leader vote is then evaluated 32 genes at a time with bit-sliced logic.
+constexpr int kPlanes = 8;
+
+// bit-sliced leader vote of one 32-gene word.  ld[t]: leader t's sign bits
+// (1 = -1); pl: the word's 8 planes.  Returns the candidate's sign bits.
+template <int K>
+__device__ __forceinline__ uint32_t wolf_word(const uint32_t *ld, const uint32_t *pl, bool early) {
+    // count of +1 leaders per gene, as bits s2 s1 s0
+    const uint32_t z0 = ~ld[0], z1 = ~ld[1], z2 = ~ld[2];
+    uint32_t s0 = z0 ^ z1 ^ z2;
+    uint32_t s1 = (z0 & z1) | (z0 & z2) | (z1 & z2);
+    uint32_t s2 = 0;
+    if (K == 4) {
+        const uint32_t z3 = ~ld[3];
+        const uint32_t cy = s0 & z3;
+        s0 ^= z3;
+        s2 = s1 & cy;
+        s1 ^= cy;
+    }
+    const uint32_t soc = pl[0], p0 = pl[1], p1 = pl[2], f2 = pl[3], st = pl[4];
+    uint32_t plus;
+    if (early) {
+        // count >= L, three-bit unsigned compare
+        const uint32_t l0 = pl[5], l1 = pl[6], l2 = pl[7];
+        const uint32_t ge0 = s0 | ~l0;
+        const uint32_t ge1 = (s1 & ~l1) | (~(s1 ^ l1) & ge0);
+        const uint32_t ge2 = (s2 & ~l2) | (~(s2 ^ l2) & ge1);
+        plus = (f2 & st) | (~f2 & ge2);
+    } else {
+        uint32_t maj;
+        if (K == 4)
+            maj = s2 | (s1 & s0) | (s1 & ~s0 & ~s2 & st);  // >= 3 of 4, or a 2-2 tie broken by state
+        else
+            maj = s1;  // >= 2 of 3
+        plus = maj ^ f2;
+    }
+    const uint32_t l3 = K == 4 ? ld[3] : ld[0];
+    const uint32_t lp = (p1 & ((p0 & l3) | (~p0 & ld[2]))) | (~p1 & ((p0 & ld[1]) | (~p0 & ld[0])));
+    return (soc & lp) | (~soc & ~plus);
+}
+
+template <int K, bool EARLY>
+__device__ __forceinline__ uint32_t wolf_lane_bits(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p1,
+                                                   uint32_t D) {
+    // returns the gene's 8 plane bits packed low to high
+    const uint64_t u1 = mix_at(key, p1);
+    const bool soc = passes(t.sl, u1);
+    const uint64_t u2 = mix_at(key, p1 + (soc ? D : (EARLY ? 2 * D : 5 * D)));
+    uint32_t pick;
+    if (K == 4) {
+        pick = (uint32_t)(u2 >> 62);  // int(u * 4) = m53 >> 51, exact
+    } else {
+        const int pv = (int)((double)(u2 >> 11) * kTwoM53 * (double)K);
+        pick = (uint32_t)(pv < K - 1 ? pv : K - 1);
+    }
+    const bool flag2 = passes(EARLY ? t.dist : t.flip, u2);
+    const uint64_t u3 = mix_at(key, p1 + ((EARLY && !flag2) ? 4 * D : 3 * D));
+    uint32_t L = 0;
+    if (EARLY) {
+        if (K == 4 && c.plus_dyadic) {
+            L = 1u + (uint32_t)(u3 >> 62);  // thresholds c/4: L = 1 + floor(4u)
+        } else {
+#pragma unroll
+            for (int cc = 0; cc <= K; ++cc) L += passes(c.thr_plus[cc], u3) ? 0u : 1u;
+        }
+    }
+    const uint32_t st = (int64_t)u3 >= 0 ? 1u : 0u;  // u < 0.5 <=> top bit clear
+    return (soc ? 1u : 0u) | (pick << 1) | ((flag2 ? 1u : 0u) << 3) | (st << 4) | (L << 5);
+}
+
+// ---------------------------------------------------------------- planner
+// Everything random in generation g depends only on (seed, g, i, position):
+// the planner draws generation g+1's DE indices, crossover mask (1 bit per
+// gene) and wolf planes (8 bits per gene) on a low-priority side stream while
+// generation g's dependent chain (trial -> fitness -> select -> wolf ->
+// fitness -> stats) runs on the main stream.  Buffers alternate by g & 1.
+//
+// Draw arithmetic is trimmed to what each decision needs: splitmix64's last
+// step z ^= z >> 31 leaves bits 63..33 untouched, so top-bit decisions (state,
+// pick, dyadic plus level) read the high word of the second product only,
+// and u < p compares decide on the high word, falling back to the full
+// 64-bit value only when the high words tie (probability 2^-32).
+struct PlanArgs {
+    EngineState *st;
+    const GenThr *gthr;
+    uint64_t *keys;    // [2][NP]
+    int4 *picks;       // [2][NP]  r1, r2, r3, m
+    int32_t *jrand;    // [2][NP]
+    uint32_t *mask;    // [2][NP][W]
+    uint32_t *planes;  // [2][NP][W][8]
+};
+
+__device__ __forceinline__ uint64_t mix_pre2(uint64_t key, uint32_t p1) {
+    uint64_t z = key + (uint64_t)p1 * kGold;
+    z = (z ^ (z >> 30)) * kMix1;
+    return z ^ (z >> 27);
+}
+__device__ __forceinline__ uint32_t mix_hi2(uint64_t x) {  // high word of x * kMix2
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    return __umulhi(lo, (uint32_t)kMix2) + lo * (uint32_t)(kMix2 >> 32) + hi * (uint32_t)kMix2;
+}
+// u < p for the draw whose pre-product state is x and product high word h
+__device__ __forceinline__ bool passes_hi(const Thr &t, uint64_t x, uint32_t h) {
+    const uint32_t ho = h ^ (h >> 31);
+    const uint32_t hl = (uint32_t)(t.le >> 32);
+    bool r = ho < hl;
+    if (ho == hl) {
+        const uint64_t z = x * kMix2;
+        r = (z ^ (z >> 31)) <= t.le;
+    }
+    return !t.never && r;
+}
+
+__global__ void k_plan_rows(RunConsts c, PlanArgs a) {
+    const int64_t g = a.st->g_plan;
+    if (g > c.G) return;
+    const int64_t b = g & 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.NP; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = fold_key3(c.seed, (uint64_t)g, (uint64_t)i);
+        int4 pk;
+        int32_t jr;
+        de_row_draws(c, key, i, pk, jr);
+        a.keys[b * c.NP + i] = key;
+        a.picks[b * c.NP + i] = pk;
+        a.jrand[b * c.NP + i] = jr;
+    }
+}
+
+template <int K, bool EARLY, bool FULL>
+__device__ __forceinline__ void plan_chunk(const RunConsts &c, const PlanArgs &a, const GenThr &t, int64_t b,
+                                           int64_t i, int jc) {
+    const uint64_t key = a.keys[b * c.NP + i];
+    const int4 pk = a.picks[b * c.NP + i];
+    const int jr = a.jrand[b * c.NP + i];
+    const uint32_t p_mask = (uint32_t)pk.w + 2;                  // m + 1 + j, plus one
+    const uint32_t p_wolf = (uint32_t)pk.w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
+    const uint32_t D = (uint32_t)c.D;
+    uint32_t *mrow = a.mask + (b * c.NP + i) * c.W;
+    uint32_t *prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int it = 0; it < kGenesPerThread; ++it) {
-        const int64_t j = (int64_t)blockIdx.x * kGenesPerBlock + it * kRowThreads + threadIdx.x;
-        bool neg = false;
-        if (j < c.D) {
-            const bool take = draw53(key, base + (uint64_t)j) < c.cr_thr || j == jr;
-            double v;
-            if (take) {
-                const double d = x2[j] - x3[j];
-                v = x1[j] + F * d;
-            } else {
-                v = xi[j];
+        const int j = jc + it * kRowThreads + threadIdx.x;
+        if (!FULL && j - lane >= (int)c.Dp) break;
+        const bool in = FULL || j < (int)c.D;
+        bool take = false;
+        if (in) {
+            const uint64_t x = mix_pre2(key, p_mask + (uint32_t)j);
+            take = passes_hi(c.thr_cr, x, mix_hi2(x)) || j == jr;
+        }
+        const uint32_t mword = __ballot_sync(0xffffffffu, take);
+        const int w = (j - lane) >> 5;
+        if (K > 0) {
+            bool soc = false, f2 = false, st = false;
+            uint32_t pick = 0, L = 0;
+            if (in) {
+                const uint32_t p0 = p_wolf + (uint32_t)j;
+                const uint64_t x1 = mix_pre2(key, p0);
+                soc = passes_hi(t.sl, x1, mix_hi2(x1));
+                const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)));
+                const uint32_t h2 = mix_hi2(x2);
+                if (K == 4) {
+                    pick = h2 >> 30;  // int(u * 4) = top two bits
+                } else {
+                    const uint64_t z = x2 * kMix2;
+                    const int pv = (int)((double)((z ^ (z >> 31)) >> 11) * kTwoM53 * (double)K);
+                    pick = (uint32_t)(pv < K - 1 ? pv : K - 1);
+                }
+                f2 = passes_hi(EARLY ? t.dist : t.flip, x2, h2);
+                const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D));
+                const uint32_t h3 = mix_hi2(x3);
+                st = (h3 >> 31) == 0u;  // u < 0.5
+                if (EARLY) {
+                    if (K == 4 && c.plus_dyadic) {
+                        L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
+                    } else {
+#pragma unroll
+                        for (int cc = 0; cc <= K; ++cc) L += passes_hi(c.thr_plus[cc], x3, h3) ? 0u : 1u;
+                    }
+                }
             }
+            const uint32_t w0 = __ballot_sync(0xffffffffu, soc);
+            const uint32_t w1 = __ballot_sync(0xffffffffu, (pick & 1u) != 0u);
+            const uint32_t w2 = __ballot_sync(0xffffffffu, (pick & 2u) != 0u);
+            const uint32_t w3 = __ballot_sync(0xffffffffu, f2);
+            const uint32_t w4 = __ballot_sync(0xffffffffu, st);
+            const uint32_t w5 = __ballot_sync(0xffffffffu, (L & 1u) != 0u);
+            const uint32_t w6 = __ballot_sync(0xffffffffu, (L & 2u) != 0u);
+            const uint32_t w7 = __ballot_sync(0xffffffffu, (L & 4u) != 0u);
+            if (lane == 0) {
+                uint4 *dst = reinterpret_cast<uint4 *>(prow + w * kPlanes);
+                dst[0] = make_uint4(w0, w1, w2, w3);
+                dst[1] = make_uint4(w4, w5, w6, w7);
+            }
+        }
+        if (lane == 0) mrow[w] = mword;
+    }
+}
+
+// one CTA per (row, 1024-gene chunk) so the block scheduler can interleave
+// these low-priority CTAs with the main stream's kernels
+template <int K>
+__global__ void __launch_bounds__(kRowThreads) k_plan_draws(RunConsts c, PlanArgs a) {
+    const int64_t g = a.st->g_plan;
+    if (g > c.G) return;
+    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
+    const int64_t i = blockIdx.x / nchunk;
+    const int jc = (int)(blockIdx.x % nchunk) * kGenesPerBlock;
+    const GenThr t = a.gthr[g];
+    const bool full = jc + kGenesPerBlock <= (int)c.D;
+    const int64_t b = g & 1;
+    if (K > 0 && t.early) {
+        if (full)
+            plan_chunk<K, true, true>(c, a, t, b, i, jc);
+        else
+            plan_chunk<K, true, false>(c, a, t, b, i, jc);
+    } else {
+        if (full)
+            plan_chunk<K, false, true>(c, a, t, b, i, jc);
+        else
+            plan_chunk<K, false, false>(c, a, t, b, i, jc);
+    }
+}
+
+__global__ void k_plan_bump(EngineState *st) { st->g_plan += 1; }
+
+// ---------------------------------------------------------------- init
+__global__ void __launch_bounds__(kRowThreads) k_init_population(RunConsts c, double *__restrict__ genome,
+                                                                 uint32_t *__restrict__ bits,
+                                                                 int32_t *__restrict__ slot_of,
+                                                                 int32_t *__restrict__ spare_of) {
+    const int64_t i = blockIdx.y;
+    const uint64_t key = fold_key3(c.seed, 0, (uint64_t)i);  // stream (seed, 0, i), optimizer.py:223
+    double *row = genome + i * c.Dp;
+    uint32_t *brow = bits + i * c.W;
+    for (int jb = 0; jb < (int)c.Dp; jb += kGenesPerBlock)
+#pragma unroll
+        for (int it = 0; it < kGenesPerThread; ++it) {
+            const int j = jb + it * kRowThreads + threadIdx.x;
+            bool neg = false;
+            if (j < (int)c.D) {
+                const double x = c.x_lo + (double)(mix_at(key, (uint32_t)j + 1) >> 11) * kTwoM53 * c.x_span;
+                row[j] = x;
+                neg = !(x >= 0.0);
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, neg);
+            if ((threadIdx.x & 31) == 0 && j < (int)c.Dp) brow[j >> 5] = word;
+        }
+    if (threadIdx.x == 0) {
+        slot_of[i] = (int32_t)i;
+        spare_of[i] = (int32_t)(c.NP + i);
+    }
+}
+
+// ---------------------------------------------------------------- DE trial
+// de_mutate + de_crossover (optimizer.py:229-262) with the planner's indices
+// and mask: trial_j = take_j ? x_r1 + F (x_r2 - x_r3) : x_i, written to the
+// spare slot with its sign bits.  No random draws left here: the kernel
+// streams the genome rows it needs (HBM-bound).  Work items are
+// (row, 1024-gene chunk) over a persistent grid.
+struct TrialArgs {
+    const EngineState *st;
+    const GenThr *gthr;
+    int64_t row_lo, n_rows;
+    int filter;  // recompute only foreign rows whose trial won (multi-GPU)
+    int64_t own_lo, own_hi;
+    const double *cand, *fit;
+    const int4 *picks;       // [2][NP]
+    const uint32_t *mask;    // [2][NP][W]
+    const uint32_t *planes;  // [2][NP][W][8]
+    const int32_t *slot_of, *spare_of;
+    uint8_t *slot_bin;
+    double *genome;
+    uint32_t *bits;
+};
+
+template <bool BIN, bool FULL>
+__device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
+                                               double F) {
+    const int4 pk = a.picks[b * c.NP + i];
+    const RowRef xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
+    const RowRef x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
+    const RowRef x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
+    const RowRef x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
+    const int64_t out_slot = a.spare_of[i];
+    double *out = a.genome + out_slot * c.Dp;
+    uint32_t *bout = a.bits + out_slot * c.W;
+    const uint32_t *mrow = a.mask + (b * c.NP + i) * c.W;
+    const int D = (int)c.D;
+    const int lane = threadIdx.x & 31;
+    double va[kGenesPerThread], vb[kGenesPerThread], vc[kGenesPerThread];
+    bool take[kGenesPerThread];
+#pragma unroll
+    for (int it = 0; it < kGenesPerThread; ++it) {
+        const int j = jc + it * kRowThreads + threadIdx.x;
+        va[it] = vb[it] = vc[it] = 0.0;
+        take[it] = false;
+        if (!FULL && j - lane >= (int)c.Dp) continue;
+        take[it] = (mrow[(j - lane) >> 5] >> lane) & 1u;
+        if (!FULL && j >= D) continue;
+        if (take[it]) {
+            va[it] = BIN ? x1.at(j) : x1.f[j];
+            vb[it] = BIN ? x2.at(j) : x2.f[j];
+            vc[it] = BIN ? x3.at(j) : x3.f[j];
+        } else {
+            va[it] = BIN ? xi.at(j) : xi.f[j];
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < kGenesPerThread; ++it) {
+        const int j = jc + it * kRowThreads + threadIdx.x;
+        if (!FULL && j - lane >= (int)c.Dp) break;
+        bool neg = false;
+        if (FULL || j < D) {
+            const double v = take[it] ? va[it] + F * (vb[it] - vc[it]) : va[it];
             out[j] = v;
             neg = !(v >= 0.0);
         }
         const uint32_t word = __ballot_sync(0xffffffffu, neg);
-        if ((threadIdx.x & 31) == 0 && j < c.Dp) bout[j >> 5] = word;
+        if (lane == 0) bout[(j - lane) >> 5] = word;
     }
+    if (jc == 0 && threadIdx.x == 0) a.slot_bin[out_slot] = 0;
 }
 
-// ---------------------------------------------------------------- selection
-// de_select (optimizer.py:265-269): strict >, ties keep the target.  With
-// skip_leaders the k current leaders are not movers (optimizer.py:454).
-__global__ void k_select(RunConsts c, const EngineState *__restrict__ st, int skip_leaders, int unconditional,
-                         const double *__restrict__ cand, double *__restrict__ fit, int32_t *__restrict__ slot_of,
-                         int32_t *__restrict__ spare_of, uint8_t *__restrict__ accepted) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= c.NP) return;
-    if (skip_leaders) {
-        for (int t = 0; t < c.k; ++t)
-            if (st->leaders[t] == i) {
-                accepted[i] = 0;
-                return;
-            }
-    }
-    const double f = cand[i];
-    if (unconditional || f > fit[i]) {
-        const int32_t a = slot_of[i];
-        slot_of[i] = spare_of[i];
-        spare_of[i] = a;
-        fit[i] = f;
-        accepted[i] = 1;
+__global__ void __launch_bounds__(kRowThreads) k_de_trial(RunConsts c, TrialArgs a) {
+    const int64_t g = a.st->g;
+    const int64_t b = g & 1;
+    const double F = a.st->F;
+    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
+    const int64_t i = a.row_lo + blockIdx.x / nchunk;
+    const int jc = (int)(blockIdx.x % nchunk) * kGenesPerBlock;
+    if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
+    const int4 pk = a.picks[b * c.NP + i];
+    const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
+                     a.slot_bin[a.slot_of[pk.z]];
+    const bool full = jc + kGenesPerBlock <= (int)c.D;
+    if (bin) {
+        if (full)
+            de_trial_chunk<true, true>(c, a, b, i, jc, F);
+        else
+            de_trial_chunk<true, false>(c, a, b, i, jc, F);
     } else {
-        accepted[i] = 0;
+        if (full)
+            de_trial_chunk<false, true>(c, a, b, i, jc, F);
+        else
+            de_trial_chunk<false, false>(c, a, b, i, jc, F);
     }
 }
 
-// ---------------------------------------------------------------- GWO (hybrid)
-// gwo_discrete_update (optimizer.py:335-376), draws taken lazily: only the
-// rows of the 6 x D block a gene's branch reads (positions are unchanged).
-__global__ void __launch_bounds__(kRowThreads) k_gwo_discrete(RunConsts c, const EngineState *__restrict__ st,
-                                                              const double *__restrict__ sched,
-                                                              const uint64_t *__restrict__ keys,
-                                                              const int4 *__restrict__ picks,
-                                                              const int32_t *__restrict__ slot_of,
-                                                              const int32_t *__restrict__ spare_of,
-                                                              uint32_t *__restrict__ bits) {
-    const int64_t i = blockIdx.y;
-    const int k = c.k;
-    for (int t = 0; t < k; ++t)
-        if (st->leaders[t] == i) return;  // leaders do not move
-    const int64_t g = st->g;
-    const double *sg = sched + g * QPM_SCHED_COLS;
-    const uint64_t thr_sl = lt_threshold(sg[QPM_SCHED_P_SL]);
-    const uint64_t thr_dist = lt_threshold(sg[QPM_SCHED_P_DIST]);
-    const uint64_t thr_flip = lt_threshold(sg[QPM_SCHED_P_FLIP]);
-    const bool early = sg[QPM_SCHED_EARLY] != 0.0;
-    const uint64_t key = keys[i];
-    const uint64_t base = (uint64_t)picks[i].w + 1 + (uint64_t)c.D;
-    const uint64_t D = (uint64_t)c.D;
-    const uint32_t *lrow[kMaxLeaders];
-    for (int t = 0; t < k; ++t) lrow[t] = bits + (int64_t)slot_of[st->leaders[t]] * c.W;
-    uint32_t *bout = bits + (int64_t)spare_of[i] * c.W;
-    const uint64_t half = 1ULL << 52;  // u_state < 0.5
+// ---------------------------------------------------------------- wolf update
+// One thread per (row, 32-gene word): the candidate's sign word from the
+// leaders' words and the row's 8 planes (bit-sliced, ~30 logic ops per 32
+// genes).  Leaders do not move (optimizer.py:454).
+template <int K>
+__global__ void __launch_bounds__(kRowThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
+    const int64_t g = a.st->g;
+    const bool early = a.gthr[g].early != 0;
+    const uint32_t *planes = a.planes + (g & 1) * c.NP * c.W * kPlanes;
+    const int64_t total = a.n_rows * c.W;
+    int32_t lead[K];
+    const uint32_t *lrow[K];
 #pragma unroll
-    for (int it = 0; it < kGenesPerThread; ++it) {
-        const int64_t j = (int64_t)blockIdx.x * kGenesPerBlock + it * kRowThreads + threadIdx.x;
-        bool neg = false;
-        if (j < c.D) {
-            const int64_t wi = j >> 5;
-            const uint32_t bit = (uint32_t)(j & 31);
-            int cnt_plus = 0;
-            for (int t = 0; t < k; ++t) cnt_plus += ((lrow[t][wi] >> bit) & 1u) ^ 1u;
-            const uint64_t jj = (uint64_t)j;
-            int state;
-            if (draw53(key, base + jj) < thr_sl) {
-                // social learning: copy leader min(int(u_pick k), k - 1)
-                const double up = draw_u(key, base + D + jj);
-                int pick = (int)(up * (double)k);
-                pick = pick < k - 1 ? pick : k - 1;
-                state = ((lrow[pick][wi] >> bit) & 1u) ? -1 : 1;
-            } else if (early) {
-                if (draw53(key, base + 2 * D + jj) < thr_dist)
-                    state = draw53(key, base + 3 * D + jj) < half ? 1 : -1;
-                else
-                    state = draw53(key, base + 4 * D + jj) < st->thr_plus[cnt_plus] ? 1 : -1;
-            } else {
-                int maj;
-                if (2 * cnt_plus > k)
-                    maj = 1;
-                else if (2 * cnt_plus < k)
-                    maj = -1;
-                else
-                    maj = draw53(key, base + 3 * D + jj) < half ? 1 : -1;
-                state = draw53(key, base + 5 * D + jj) < thr_flip ? -maj : maj;
-            }
-            neg = state < 0;
-        }
-        const uint32_t word = __ballot_sync(0xffffffffu, neg);
-        if ((threadIdx.x & 31) == 0 && j < c.Dp) bout[j >> 5] = word;
+    for (int t = 0; t < K; ++t) {
+        lead[t] = a.st->leaders[t];
+        lrow[t] = a.bits + (int64_t)a.slot_of[lead[t]] * c.W;
     }
-}
-
-// accepted wolves: genome = +/-1.0 from their bits (optimizer.py:376)
-__global__ void __launch_bounds__(kRowThreads) k_materialize(RunConsts c, const uint8_t *__restrict__ accepted,
-                                                             const int32_t *__restrict__ slot_of,
-                                                             const uint32_t *__restrict__ bits,
-                                                             double *__restrict__ genome) {
-    const int64_t i = blockIdx.y;
-    if (!accepted[i]) return;
-    const int64_t slot = slot_of[i];
-    const uint32_t *br = bits + slot * c.W;
-    double *row = genome + slot * c.Dp;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = a.row_lo + idx / c.W;
+        const int w = (int)(idx % c.W);
+        bool skip = false;
 #pragma unroll
-    for (int it = 0; it < kGenesPerThread; ++it) {
-        const int64_t j = (int64_t)blockIdx.x * kGenesPerBlock + it * kRowThreads + threadIdx.x;
-        if (j < c.D) row[j] = ((br[j >> 5] >> (j & 31)) & 1u) ? -1.0 : 1.0;
+        for (int t = 0; t < K; ++t) skip |= lead[t] == i;
+        if (skip) continue;
+        if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) continue;
+        uint32_t ld[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) ld[t] = t < K ? lrow[t][w] : 0u;
+        const uint4 *pp = reinterpret_cast<const uint4 *>(planes + (i * c.W + w) * kPlanes);
+        const uint4 q0 = pp[0], q1 = pp[1];
+        const uint32_t pl[kPlanes] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const int rem = (int)c.D - w * 32;
+        const uint32_t valid = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        a.bits[(int64_t)a.spare_of[i] * c.W + w] = wolf_word<K>(ld, pl, early) & valid;
     }
 }
 
-// ---------------------------------------------------------------- GWO (run_gwo)
-__global__ void k_keys(RunConsts c, const EngineState *__restrict__ st, uint64_t *__restrict__ keys) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < c.NP) keys[i] = fold_key3(c.seed, (uint64_t)st->g, (uint64_t)i);
-}
-
+// ---------------------------------------------------------------- run_gwo
 // gwo_reference_update (optimizer.py:302-332) with the three ranked leaders
 __global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, const EngineState *__restrict__ st,
-                                                                const double *__restrict__ sched,
-                                                                const uint64_t *__restrict__ keys,
+                                                                const double *__restrict__ sched, int64_t row_lo,
                                                                 const int32_t *__restrict__ slot_of,
                                                                 const int32_t *__restrict__ spare_of,
+                                                                uint8_t *__restrict__ slot_bin,
                                                                 double *__restrict__ genome,
                                                                 uint32_t *__restrict__ bits) {
-    const int64_t i = blockIdx.y;
+    const int64_t i = row_lo + blockIdx.y;
     for (int t = 0; t < 3; ++t)
         if (st->leaders[t] == i) return;
-    const double a = sched[st->g * QPM_SCHED_COLS + QPM_SCHED_A_NOW];
+    const int64_t g = st->g;
+    const double a = sched[g * QPM_SCHED_COLS + QPM_SCHED_A_NOW];
     const double two_a = 2.0 * a;
-    const uint64_t key = keys[i];
+    const uint64_t key = fold_key3(c.seed, (uint64_t)g, (uint64_t)i);
     const uint64_t D = (uint64_t)c.D;
-    const double *x = genome + (int64_t)slot_of[i] * c.Dp;
-    const double *L0 = genome + (int64_t)slot_of[st->leaders[0]] * c.Dp;
-    const double *L1 = genome + (int64_t)slot_of[st->leaders[1]] * c.Dp;
-    const double *L2 = genome + (int64_t)slot_of[st->leaders[2]] * c.Dp;
+    const RowRef x = row_ref(c, slot_of[i], slot_bin, genome, bits);
+    const RowRef L0 = row_ref(c, slot_of[st->leaders[0]], slot_bin, genome, bits);
+    const RowRef L1 = row_ref(c, slot_of[st->leaders[1]], slot_bin, genome, bits);
+    const RowRef L2 = row_ref(c, slot_of[st->leaders[2]], slot_bin, genome, bits);
     const int64_t out_slot = spare_of[i];
     double *out = genome + out_slot * c.Dp;
     uint32_t *bout = bits + out_slot * c.W;
+    for (int64_t jb = 0; jb < c.Dp; jb += kGenesPerBlock)
 #pragma unroll
     for (int it = 0; it < kGenesPerThread; ++it) {
-        const int64_t j = (int64_t)blockIdx.x * kGenesPerBlock + it * kRowThreads + threadIdx.x;
+        const int64_t j = jb + it * kRowThreads + threadIdx.x;
         bool neg = false;
         if (j < c.D) {
             const uint64_t jj = (uint64_t)j;
-            const double xj = x[j];
-            const double Lm[3] = {L0[j], L1[j], L2[j]};
+            const double xj = x.at(j);
+            const double Lm[3] = {L0.at(j), L1.at(j), L2.at(j)};
             double moved[3];
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
@@ -335,75 +623,177 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, con
         const uint32_t word = __ballot_sync(0xffffffffu, neg);
         if ((threadIdx.x & 31) == 0 && j < c.Dp) bout[j >> 5] = word;
     }
+    if (threadIdx.x == 0) slot_bin[out_slot] = 0;
 }
 
-// ---------------------------------------------------------------- stats
-// numpy pairwise sum of v[0..n): leaves (precomputed on the host, in order)
-// summed in parallel, then the split tree combined by one thread.
-__device__ double block_pairwise(const double *v, int64_t n, const int64_t *leaf_off, int64_t n_leaf,
-                                 double *leafsum) {
-    for (int64_t l = threadIdx.x; l < n_leaf; l += blockDim.x) {
-        const int64_t off = leaf_off[l];
-        const int64_t len = (l + 1 < n_leaf ? leaf_off[l + 1] : n) - off;
-        leafsum[l] = pairwise_leaf(v + off, len);
-    }
-    __syncthreads();
-    __shared__ double result;
-    if (threadIdx.x == 0) {
-        struct Frame {
-            int64_t n;
-            int state;
-            double left;
-        };
-        Frame stk[48];
-        int top = 0;
-        stk[0] = {n, 0, 0.0};
-        double ret = 0.0;
-        int64_t next = 0;
-        while (top >= 0) {
-            Frame &f = stk[top];
-            if (f.n <= 128) {
-                ret = leafsum[next++];
-                --top;
-                continue;
+// ---------------------------------------------------------------- block helpers
+struct Cand {
+    double v;
+    int32_t i;
+};
+__device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
+    if (a.i < 0) return false;
+    if (b.i < 0) return true;
+    return a.v > b.v || (a.v == b.v && a.i < b.i);
+}
+
+// top-K of vals[0..n) by (-value, index) (parexec.reduce_best), whole CTA:
+// K rounds of a block argmax that skips the winners of earlier rounds.
+// Register-light on purpose (1024-thread CTAs get 64 registers).
+template <int K>
+__device__ void block_topk(const double *vals, int64_t n, int32_t *out) {
+    __shared__ double s_v[32];
+    __shared__ int32_t s_i[32];
+    __shared__ int32_t s_win;
+    int32_t taken[K];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+        Cand best = {0.0, -1};
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            bool tk = false;
+#pragma unroll
+            for (int u = 0; u < t; ++u) tk |= taken[u] == (int32_t)i;
+            const Cand cd = {vals[i], (int32_t)i};
+            if (!tk && better(cd, best)) best = cd;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            Cand o;
+            o.v = __shfl_down_sync(0xffffffffu, best.v, off);
+            o.i = __shfl_down_sync(0xffffffffu, best.i, off);
+            if (better(o, best)) best = o;
+        }
+        if (lane == 0) {
+            s_v[warp] = best.v;
+            s_i[warp] = best.i;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            Cand w = lane < nwarps ? Cand{s_v[lane], s_i[lane]} : Cand{0.0, -1};
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                Cand o;
+                o.v = __shfl_down_sync(0xffffffffu, w.v, off);
+                o.i = __shfl_down_sync(0xffffffffu, w.i, off);
+                if (better(o, w)) w = o;
             }
-            int64_t n2 = f.n / 2;
-            n2 -= n2 % 8;
-            if (f.state == 0) {
-                f.state = 1;
-                stk[top + 1] = {n2, 0, 0.0};
-                ++top;
-            } else if (f.state == 1) {
-                f.left = ret;
-                f.state = 2;
-                stk[top + 1] = {f.n - n2, 0, 0.0};
-                ++top;
-            } else {
-                ret = f.left + ret;
-                --top;
+            if (lane == 0) {
+                s_win = w.i;
+                out[t] = w.i;
             }
         }
-        result = ret;
+        __syncthreads();
+        taken[t] = s_win;
+        __syncthreads();
     }
-    __syncthreads();
-    return result;
 }
 
-// np.max / np.mean / np.std of the fitness vector, the convergence window,
-// adaptive_f_update (optimizer.py:277-299, 469-485) and the trace row; or,
-// for run_gwo, the a-coefficient row and best-ever tracking (optimizer.py:586-589).
-__global__ void __launch_bounds__(kStatsThreads) k_stats(RunConsts c, EngineState *__restrict__ st,
-                                                         const double *__restrict__ sched,
-                                                         const double *__restrict__ fit,
-                                                         double *__restrict__ scratch,
-                                                         const int64_t *__restrict__ leaf_off,
-                                                         double *__restrict__ leafsum, double *__restrict__ trace) {
+__device__ void block_topk_k(const double *vals, int64_t n, int k, int32_t *out) {
+    if (k == 4)
+        block_topk<4>(vals, n, out);
+    else if (k == 3)
+        block_topk<3>(vals, n, out);
+    else
+        block_topk<1>(vals, n, out);
+}
+
+// numpy pairwise sum of v[0..n) over the host-built split tree
+__device__ double block_pairwise(const double *v, int64_t n, const RunConsts &c, const SumTree &tr) {
+    for (int l = threadIdx.x; l < c.n_leaf; l += blockDim.x) {
+        const int64_t off = tr.leaf_off[l];
+        tr.val[l] = pairwise_leaf(v + off, tr.leaf_off[l + 1] - off);
+    }
+    __syncthreads();
+    for (int h = 0; h < c.n_levels; ++h) {
+        for (int t = tr.lvl[h] + threadIdx.x; t < tr.lvl[h + 1]; t += blockDim.x)
+            tr.val[c.n_leaf + t] = tr.val[tr.kid[2 * t]] + tr.val[tr.kid[2 * t + 1]];
+        __syncthreads();
+    }
+    const double r = tr.val[c.n_leaf > 1 ? 2 * c.n_leaf - 2 : 0];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------- select + top-k
+// de_select over all individuals (strict >, ties keep the target), then
+// rank_leaders (optimizer.py:437-444).  One CTA.
+__global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, EngineState *__restrict__ st,
+                                                             const double *__restrict__ cand,
+                                                             double *__restrict__ fit, int32_t *__restrict__ slot_of,
+                                                             int32_t *__restrict__ spare_of) {
+    for (int64_t i = threadIdx.x; i < c.NP; i += blockDim.x) {
+        const double f = cand[i];
+        if (f > fit[i]) {
+            const int32_t a = slot_of[i];
+            slot_of[i] = spare_of[i];
+            spare_of[i] = a;
+            fit[i] = f;
+        }
+    }
+    __syncthreads();
+    block_topk_k(fit, c.NP, c.k, st->leaders);
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, EngineState *__restrict__ st,
+                                                              const double *__restrict__ fit, int k) {
+    block_topk_k(fit, c.NP, k, st->leaders);
+}
+
+// ---------------------------------------------------------------- select + stats
+// mode 0: DE selection of everyone (run_de); 1: wolf selection of the
+// non-leaders, accepted slots become +/-1 rows (run_hybrid); 2: unconditional
+// replacement of the non-leaders (run_gwo); 3: none (init).  Then np.max /
+// np.mean / np.std, the convergence window and adaptive_f_update
+// (optimizer.py:277-299, 469-485), or run_gwo's a-row and best-ever tracking
+// (optimizer.py:586-589), and the trace row.  One CTA.
+__global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int mode, EngineState *__restrict__ st,
+                                                              const double *__restrict__ sched,
+                                                              const double *__restrict__ cand,
+                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
+                                                              int32_t *__restrict__ spare_of,
+                                                              uint8_t *__restrict__ slot_bin,
+                                                              double *__restrict__ scratch, SumTree tr,
+                                                              double *__restrict__ trace) {
     const int64_t n = c.NP;
-    // max with its lowest index, and min
+    if (mode != 3) {
+        int32_t lead[kMaxLeaders];
+#pragma unroll
+        for (int t = 0; t < kMaxLeaders; ++t) lead[t] = (mode != 0 && t < c.k) ? st->leaders[t] : -1;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            bool is_leader = false;
+#pragma unroll
+            for (int t = 0; t < kMaxLeaders; ++t) is_leader |= lead[t] == i;
+            if (is_leader) continue;
+            const double f = cand[i];
+            if (mode == 2 || f > fit[i]) {
+                const int32_t a = slot_of[i];
+                const int32_t b = spare_of[i];
+                slot_of[i] = b;
+                spare_of[i] = a;
+                fit[i] = f;
+                if (mode == 1) slot_bin[b] = 1;
+            }
+        }
+        __syncthreads();
+    }
+    // stage the fitness vector (and the squared deviations) in shared memory
+    // when it fits; the pairwise-sum leaves then read on-chip
+    extern __shared__ double s_dyn[];
+    const bool on_chip = n <= kStatsSmemMaxNP;
+    const double *fv = fit;
+    double *sq = scratch;
+    if (on_chip) {
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s_dyn[i] = fit[i];
+        fv = s_dyn;
+        sq = s_dyn + n;
+        __syncthreads();
+    }
+    // max (lowest index on ties) and min
     double mx = -INFINITY, mn = INFINITY;
     int64_t amx = n;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double v = fit[i];
+        const double v = fv[i];
         if (v > mx || (v == mx && i < amx)) {
             mx = v;
             amx = i;
@@ -420,8 +810,8 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(RunConsts c, EngineStat
         }
         mn = omn < mn ? omn : mn;
     }
-    __shared__ double s_mx[kStatsThreads / 32], s_mn[kStatsThreads / 32];
-    __shared__ int64_t s_am[kStatsThreads / 32];
+    __shared__ double s_mx[kCtaThreads / 32], s_mn[kCtaThreads / 32];
+    __shared__ int64_t s_am[kCtaThreads / 32];
     if ((threadIdx.x & 31) == 0) {
         s_mx[threadIdx.x >> 5] = mx;
         s_mn[threadIdx.x >> 5] = mn;
@@ -444,13 +834,13 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(RunConsts c, EngineStat
     mx = s_mx[0];
     mn = s_mn[0];
     amx = s_am[0];
-    const double mean = block_pairwise(fit, n, leaf_off, c.n_leaf, leafsum) / (double)n;
+    const double mean = block_pairwise(fv, n, c, tr) / (double)n;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double d = fit[i] - mean;
-        scratch[i] = d * d;
+        const double d = fv[i] - mean;
+        sq[i] = d * d;
     }
     __syncthreads();
-    const double var = block_pairwise(scratch, n, leaf_off, c.n_leaf, leafsum) / (double)n;
+    const double var = block_pairwise(sq, n, c, tr) / (double)n;
     if (threadIdx.x != 0) return;
     const double sd = sqrt(var);
     const int64_t g = st->g;
@@ -477,23 +867,31 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(RunConsts c, EngineStat
     } else {
         // convergence window: deque(maxlen=conv_window) of best_now > best_prev
         const int cap = c.conv_window;
+        uint8_t win[kMaxWindow];
+        int len = st->win_len;
+        for (int t = 0; t < len; ++t) win[t] = st->win[t];
         const uint8_t improved = mx > st->best_prev ? 1 : 0;
-        if (st->win_len < cap) {
-            st->win[st->win_len++] = improved;
+        if (len < cap) {
+            win[len++] = improved;
         } else {
-            for (int t = 1; t < cap; ++t) st->win[t - 1] = st->win[t];
-            st->win[cap - 1] = improved;
+            for (int t = 1; t < cap; ++t) win[t - 1] = win[t];
+            win[cap - 1] = improved;
         }
-        st->best_prev = mx;
         int cnt = 0;
-        for (int t = 0; t < st->win_len; ++t) cnt += st->win[t];
-        const double conv = st->win_len ? (double)cnt / (double)st->win_len : 1.0;
+        for (int t = 0; t < len; ++t) {
+            cnt += win[t];
+            st->win[t] = win[t];
+        }
+        st->win_len = len;
+        st->best_prev = mx;
+        const double conv = len ? (double)cnt / (double)len : 1.0;
         const double *sg = sched + g * QPM_SCHED_COLS;
+        const double base = st->baseline_std;
         double f = sg[QPM_SCHED_F_ENV];
         if (c.adaptive) {
-            const double tl = c.theta_low_frac * st->baseline_std;
-            const double th = c.theta_high_frac * st->baseline_std;
-            const double rt = c.range_trigger_frac * st->baseline_std;
+            const double tl = c.theta_low_frac * base;
+            const double th = c.theta_high_frac * base;
+            const double rt = c.range_trigger_frac * base;
             if (sd < tl || conv < c.conv_threshold) f *= c.explore_boost;
             if (sd > th || (mx - mn) < rt) f *= c.exploit_factor;
         }
@@ -506,21 +904,28 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(RunConsts c, EngineStat
     st->g = g + 1;
 }
 
-// best row -> result buffer (when the stats/finalize step flagged it)
+// best row -> result buffer (when flagged), expanding +/-1 slots from bits
 __global__ void k_copy_best(RunConsts c, const EngineState *__restrict__ st, const int32_t *__restrict__ slot_of,
-                            const double *__restrict__ genome, const uint32_t *__restrict__ bits,
-                            double *__restrict__ best_genome, uint32_t *__restrict__ best_bits) {
+                            const uint8_t *__restrict__ slot_bin, const double *__restrict__ genome,
+                            const uint32_t *__restrict__ bits, double *__restrict__ best_genome,
+                            uint32_t *__restrict__ best_bits) {
     if (!st->best_flag) return;
     const int64_t slot = slot_of[st->best_idx];
+    const RowRef r = row_ref(c, slot, slot_bin, genome, bits);
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c.Dp; j += (int64_t)gridDim.x * blockDim.x) {
-        best_genome[j] = genome[slot * c.Dp + j];
+        best_genome[j] = j < c.D ? r.at(j) : 0.0;
         if (j < c.W) best_bits[j] = bits[slot * c.W + j];
     }
 }
 
-__global__ void k_finalize_best(EngineState *st, const int32_t *top1) {
-    st->best_idx = top1[0];
-    st->best_flag = 1;
+__global__ void k_finalize_best(RunConsts c, EngineState *st, const double *fit) {
+    // rank_leaders(pop, 1): highest fitness, lowest index on ties
+    __shared__ int32_t top[kMaxLeaders];
+    block_topk<1>(fit, c.NP, top);
+    if (threadIdx.x == 0) {
+        st->best_idx = top[0];
+        st->best_flag = 1;
+    }
 }
 
 __global__ void k_reset_flag(EngineState *st) { st->best_flag = 0; }
@@ -533,12 +938,18 @@ struct Engine {
     cudaStream_t stream = nullptr;
     double *genome = nullptr;
     uint32_t *bits = nullptr;
-    int32_t *slot_of = nullptr, *spare_of = nullptr, *jrand = nullptr, *top1 = nullptr;
-    double *fit = nullptr, *cand = nullptr, *scratch = nullptr, *leafsum = nullptr;
-    int64_t *leaf_off = nullptr;
+    uint8_t *slot_bin = nullptr;
+    uint32_t *planes = nullptr, *mask = nullptr;  // [2][...] by generation parity
+    GenThr *gthr = nullptr;
+    cudaStream_t side = nullptr;  // low-priority planner stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int32_t *slot_of = nullptr, *spare_of = nullptr, *jrand = nullptr;
+    double *fit = nullptr, *cand = nullptr, *scratch = nullptr;
+    int32_t *tree_i = nullptr;
+    double *tree_v = nullptr;
+    SumTree tree{};
     uint64_t *keys = nullptr;
     int4 *picks = nullptr;
-    uint8_t *accepted = nullptr;
     double *sched = nullptr, *trace = nullptr;
     EngineState *st = nullptr;
     double *best_genome = nullptr;
@@ -546,6 +957,7 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
+    int trial_grid = 148, apply_grid = 148, plan_grid = 148;
     int64_t g_done = 0;
     bool initialized = false;
     bool owns_stream = false;
@@ -562,19 +974,67 @@ static int dalloc(Engine *e, T **p, size_t count) {
     return QPM_OK;
 }
 
-static void pairwise_leaves(int64_t off, int64_t n, std::vector<int64_t> &out) {
+// numpy's pairwise split tree of an n-vector: leaves in order (ids
+// 0..L-1), internal nodes grouped by height so children precede parents
+struct HostTree {
+    std::vector<int32_t> leaf_off, kid, lvl;
+};
+
+struct TmpNode {
+    int height, left, right;
+    int64_t off;
+};
+
+static int tree_rec(int64_t off, int64_t n, std::vector<TmpNode> &nodes) {
     if (n <= 128) {
-        out.push_back(off);
-        return;
+        nodes.push_back({0, -1, -1, off});
+        return (int)nodes.size() - 1;
     }
     int64_t n2 = n / 2;
     n2 -= n2 % 8;
-    pairwise_leaves(off, n2, out);
-    pairwise_leaves(off + n2, n - n2, out);
+    const int a = tree_rec(off, n2, nodes);
+    const int b = tree_rec(off + n2, n - n2, nodes);
+    nodes.push_back({1 + std::max(nodes[a].height, nodes[b].height), a, b, off});
+    return (int)nodes.size() - 1;
 }
 
-static dim3 row_grid(const Engine *e) {
-    return dim3((unsigned)((e->c.Dp + kGenesPerBlock - 1) / kGenesPerBlock), (unsigned)e->c.NP);
+static HostTree build_tree(int64_t n) {
+    std::vector<TmpNode> nodes;
+    tree_rec(0, n, nodes);
+    HostTree t;
+    int max_h = 0;
+    for (const TmpNode &v : nodes) max_h = std::max(max_h, v.height);
+    std::vector<int> final_id(nodes.size(), -1);
+    int next = 0;
+    for (size_t v = 0; v < nodes.size(); ++v)
+        if (nodes[v].height == 0) {
+            final_id[v] = next++;
+            t.leaf_off.push_back((int32_t)nodes[v].off);
+        }
+    const int nleaf = next;
+    t.lvl.push_back(0);
+    std::vector<int> order;
+    for (int h = 1; h <= max_h; ++h) {
+        for (size_t v = 0; v < nodes.size(); ++v)
+            if (nodes[v].height == h) {
+                final_id[v] = next++;
+                order.push_back((int)v);
+            }
+        t.lvl.push_back(next - nleaf);
+    }
+    for (int v : order) {
+        t.kid.push_back(final_id[nodes[v].left]);
+        t.kid.push_back(final_id[nodes[v].right]);
+    }
+    t.leaf_off.push_back((int32_t)n);  // sentinel
+    return t;
+}
+
+// one CTA per row; the CTA strides over the row's genes, so per-row setup
+// (key folding, index draws, slot lookups) is paid once per row
+static dim3 row_grid(const Engine *e, int64_t rows) {
+    (void)e;
+    return dim3(1u, (unsigned)rows);
 }
 
 // optional per-stage event marks (qpm_engine_profile)
@@ -590,75 +1050,133 @@ struct StageMarks {
     }
 };
 
+static size_t stats_smem_bytes(const RunConsts &c) {
+    return c.NP <= kStatsSmemMaxNP ? (size_t)2 * c.NP * sizeof(double) : 0;
+}
+
+static int launch_select_stats(Engine *e, int mode, cudaStream_t s) {
+    k_select_stats<<<1, kCtaThreads, stats_smem_bytes(e->c), s>>>(e->c, mode, e->st, e->sched, e->cand, e->fit,
+                                                                  e->slot_of, e->spare_of, e->slot_bin, e->scratch,
+                                                                  e->tree, e->trace);
+    QPM_LAUNCH_CHECK();
+    return QPM_OK;
+}
+
+static TrialArgs trial_args(const Engine *e, int64_t row_lo, int64_t n_rows) {
+    TrialArgs a;
+    a.st = e->st;
+    a.gthr = e->gthr;
+    a.row_lo = row_lo;
+    a.n_rows = n_rows;
+    a.filter = 0;
+    a.own_lo = 0;
+    a.own_hi = e->c.NP;
+    a.cand = e->cand;
+    a.fit = e->fit;
+    a.picks = e->picks;
+    a.mask = e->mask;
+    a.planes = e->planes;
+    a.slot_of = e->slot_of;
+    a.spare_of = e->spare_of;
+    a.slot_bin = e->slot_bin;
+    a.genome = e->genome;
+    a.bits = e->bits;
+    return a;
+}
+
+static PlanArgs plan_args(const Engine *e) {
+    PlanArgs a;
+    a.st = e->st;
+    a.gthr = e->gthr;
+    a.keys = e->keys;
+    a.picks = e->picks;
+    a.jrand = e->jrand;
+    a.mask = e->mask;
+    a.planes = e->planes;
+    return a;
+}
+
+// the planner for generation st->g_plan on stream s (then g_plan += 1)
+static int enqueue_planner(Engine *e, cudaStream_t s) {
+    const RunConsts &c = e->c;
+    const PlanArgs pa = plan_args(e);
+    k_plan_rows<<<(unsigned)((c.NP + 127) / 128), 128, 0, s>>>(c, pa);
+    const unsigned items = (unsigned)(c.NP * ((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock));
+    if (c.algorithm == QPM_ALGO_HYBRID && c.k == 4)
+        k_plan_draws<4><<<items, kRowThreads, 0, s>>>(c, pa);
+    else if (c.algorithm == QPM_ALGO_HYBRID)
+        k_plan_draws<3><<<items, kRowThreads, 0, s>>>(c, pa);
+    else
+        k_plan_draws<0><<<items, kRowThreads, 0, s>>>(c, pa);
+    k_plan_bump<<<1, 1, 0, s>>>(e->st);
+    QPM_LAUNCH_CHECK();
+    return QPM_OK;
+}
+
 // one generation's launch sequence
 static int enqueue_generation(Engine *e, int *launches, StageMarks *pm = nullptr) {
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
-    const unsigned nb = (unsigned)((c.NP + 255) / 256);
     int n = 0;
     int rc;
     auto mark = [&](const char *next) {
         if (pm) pm->mark(s, next);
     };
+    const int64_t NP = c.NP;
     if (c.algorithm == QPM_ALGO_GWO) {
         mark("topk");
-        rc = launch_reduce_best(e->fit, c.NP, 3, e->st->leaders, s);  // rank_leaders(pop, 3)
-        if (rc) return rc;
+        k_topk_leaders<<<1, kCtaThreads, 0, s>>>(c, e->st, e->fit, 3);  // rank_leaders(pop, 3)
         mark("gwo_continuous");
-        k_keys<<<nb, 256, 0, s>>>(c, e->st, e->keys);
-        k_gwo_continuous<<<row_grid(e), kRowThreads, 0, s>>>(c, e->st, e->sched, e->keys, e->slot_of, e->spare_of,
-                                                             e->genome, e->bits);
-        QPM_LAUNCH_CHECK();
-        n += 3;
-        mark("fitness");
-        rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, c.NP, e->cand, e->P.fitness_mode, s, &n);
-        if (rc) return rc;
-        mark("replace");
-        k_select<<<nb, 256, 0, s>>>(c, e->st, 1, 1, e->cand, e->fit, e->slot_of, e->spare_of, e->accepted);
-        mark("stats");
-        k_stats<<<1, kStatsThreads, 0, s>>>(c, e->st, e->sched, e->fit, e->scratch, e->leaf_off, e->leafsum,
-                                            e->trace);
-        k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->genome, e->bits, e->best_genome, e->best_bits);
-        QPM_LAUNCH_CHECK();
-        n += 3;
-    } else {
-        mark("de_draws");
-        k_de_draws<<<nb, 256, 0, s>>>(c, e->st, e->keys, e->picks, e->jrand);
-        mark("de_trial");
-        k_de_trial<<<row_grid(e), kRowThreads, 0, s>>>(c, e->st, e->keys, e->picks, e->jrand, e->slot_of, e->spare_of,
-                                                       e->genome, e->bits);
+        k_gwo_continuous<<<row_grid(e, NP), kRowThreads, 0, s>>>(c, e->st, e->sched, 0, e->slot_of, e->spare_of,
+                                                                 e->slot_bin, e->genome, e->bits);
         QPM_LAUNCH_CHECK();
         n += 2;
-        mark("fitness_de");
-        rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, c.NP, e->cand, e->P.fitness_mode, s, &n);
+        mark("fitness");
+        rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, NP, e->cand, e->P.fitness_mode, s, &n);
         if (rc) return rc;
-        mark("select_de");
-        k_select<<<nb, 256, 0, s>>>(c, e->st, 0, 0, e->cand, e->fit, e->slot_of, e->spare_of, e->accepted);
+        mark("replace_stats");
+        if ((rc = launch_select_stats(e, 2, s))) return rc;
+        k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,
+                                       e->best_bits);
+        QPM_LAUNCH_CHECK();
+        n += 2;
+    } else {
+        const bool hybrid = c.algorithm == QPM_ALGO_HYBRID;
+        const TrialArgs ta = trial_args(e, 0, NP);
+        // fork: the planner draws generation g+1 on the side stream
+        QPM_CUDA_TRY(cudaEventRecord(e->ev_fork, s));
+        QPM_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+        if ((rc = enqueue_planner(e, e->side))) return rc;
+        QPM_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
+        n += 3;
+        mark("de_trial");
+        k_de_trial<<<(unsigned)(NP * ((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock)), kRowThreads, 0, s>>>(c, ta);
         QPM_LAUNCH_CHECK();
         n += 1;
-        if (c.algorithm == QPM_ALGO_HYBRID) {
-            mark("topk");
-            rc = launch_reduce_best(e->fit, c.NP, c.k, e->st->leaders, s);  // rank_leaders(pop, k)
-            if (rc) return rc;
-            mark("gwo_discrete");
-            k_gwo_discrete<<<row_grid(e), kRowThreads, 0, s>>>(c, e->st, e->sched, e->keys, e->picks, e->slot_of,
-                                                               e->spare_of, e->bits);
+        mark("fitness_de");
+        rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, NP, e->cand, e->P.fitness_mode, s, &n);
+        if (rc) return rc;
+        if (hybrid) {
+            mark("select_topk");
+            k_select_topk<<<1, kCtaThreads, 0, s>>>(c, e->st, e->cand, e->fit, e->slot_of, e->spare_of);
+            mark("gwo_apply");
+            if (c.k == 4)
+                k_gwo_apply<4><<<e->apply_grid, kRowThreads, 0, s>>>(c, ta);
+            else
+                k_gwo_apply<3><<<e->apply_grid, kRowThreads, 0, s>>>(c, ta);
             QPM_LAUNCH_CHECK();
             n += 2;
             mark("fitness_gwo");
-            rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, c.NP, e->cand, e->P.fitness_mode, s, &n);
+            rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, NP, e->cand, e->P.fitness_mode, s, &n);
             if (rc) return rc;
-            mark("select_gwo");
-            k_select<<<nb, 256, 0, s>>>(c, e->st, 1, 0, e->cand, e->fit, e->slot_of, e->spare_of, e->accepted);
-            k_materialize<<<row_grid(e), kRowThreads, 0, s>>>(c, e->accepted, e->slot_of, e->bits, e->genome);
-            QPM_LAUNCH_CHECK();
-            n += 2;
+            mark("select_stats");
+            if ((rc = launch_select_stats(e, 1, s))) return rc;
+        } else {
+            mark("select_stats");
+            if ((rc = launch_select_stats(e, 0, s))) return rc;
         }
-        mark("stats");
-        k_stats<<<1, kStatsThreads, 0, s>>>(c, e->st, e->sched, e->fit, e->scratch, e->leaf_off, e->leafsum,
-                                            e->trace);
-        QPM_LAUNCH_CHECK();
         n += 1;
+        QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
     }
     mark(nullptr);
     if (launches) *launches = n;
@@ -670,6 +1188,12 @@ static void engine_free(Engine *e) {
         cudaStreamSynchronize(e->stream);
         cudaStreamDestroy(e->stream);
     }
+    if (e->side) {
+        cudaStreamSynchronize(e->side);
+        cudaStreamDestroy(e->side);
+    }
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
     for (void *p : e->allocs) cudaFree(p);
@@ -697,19 +1221,32 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
                   "leader_count must be 3 or 4");
     QPM_ARG_CHECK(P->conv_window >= 1 && P->conv_window <= kMaxWindow, "conv_window in [1, 256]");
     QPM_ARG_CHECK(P->row_lo == 0 && P->row_hi == P->NP, "sharded rows need the multi-GPU engine");
-    QPM_ARG_CHECK(P->NP < (1LL << 31), "NP < 2^31");
+    QPM_ARG_CHECK(P->NP < (1LL << 30), "NP < 2^30");
     Engine *e = new Engine();
     e->prob = &prob->p;
     e->P = *P;
     e->stream = (cudaStream_t)stream;
     if (!e->stream) {
         // graphs cannot be captured on the legacy default stream: own a stream
-        if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        int lo_p = 0, hi_p = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p);
+        if (cudaStreamCreateWithPriority(&e->stream, cudaStreamNonBlocking, hi_p) != cudaSuccess) {
             set_error("cudaStreamCreateWithFlags failed");
             delete e;
             return QPM_ERR_CUDA;
         }
         e->owns_stream = true;
+    }
+    {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
+        if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            set_error("planner stream/event creation failed");
+            engine_free(e);
+            return QPM_ERR_CUDA;
+        }
     }
     RunConsts &c = e->c;
     c.algorithm = P->algorithm;
@@ -722,6 +1259,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     c.f_max = P->f_max;
     c.f_min = P->f_min;
     c.cr_thr = le_threshold(P->cr);
+    c.thr_cr = make_thr(c.cr_thr);
     if (P->algorithm == QPM_ALGO_GWO) {
         c.x_lo = P->gwo_lo;
         c.x_span = P->gwo_hi - P->gwo_lo;
@@ -741,31 +1279,56 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     c.conv_window = P->conv_window;
     c.adaptive = P->adaptive_branches;
     c.gwo_a0 = P->gwo_a0;
-    std::vector<int64_t> leaves;
-    pairwise_leaves(0, c.NP, leaves);
-    c.n_leaf = (int64_t)leaves.size();
+    if (cudaFuncSetAttribute(k_select_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)std::max<size_t>(stats_smem_bytes(c), 1)) != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(k_select_stats) failed");
+        engine_free(e);
+        return QPM_ERR_CUDA;
+    }
+    {
+        int dev = 0, sms = 148, occ_t = 1, occ_a = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int occ_p = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_de_trial, kRowThreads, 0);
+        if (c.k == 4) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_gwo_apply<4>, kRowThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_plan_draws<4>, kRowThreads, 0);
+        } else {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_gwo_apply<3>, kRowThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_plan_draws<3>, kRowThreads, 0);
+        }
+        e->plan_grid = sms * std::max(occ_p, 1);
+        e->trial_grid = sms * std::max(occ_t, 1);
+        e->apply_grid = sms * std::max(occ_a, 1);
+    }
+    HostTree ht = build_tree(c.NP);
+    c.n_leaf = (int32_t)ht.leaf_off.size() - 1;
+    c.n_levels = (int32_t)ht.lvl.size() - 1;
 
     const int64_t NP = c.NP;
     int rc = QPM_OK;
-#define QPM_ALLOC(ptr, count)                   \
+#define QPM_ALLOC(ptr, count)                     \
     if ((rc = dalloc(e, &(ptr), (count))) != 0) { \
-        engine_free(e);                         \
-        return rc;                              \
+        engine_free(e);                           \
+        return rc;                                \
     }
     QPM_ALLOC(e->genome, (size_t)2 * NP * c.Dp);
     QPM_ALLOC(e->bits, (size_t)2 * NP * c.W);
+    QPM_ALLOC(e->slot_bin, (size_t)2 * NP);
+    QPM_ALLOC(e->planes, P->algorithm == QPM_ALGO_HYBRID ? (size_t)2 * NP * c.W * kPlanes : 16);
+    QPM_ALLOC(e->mask, P->algorithm != QPM_ALGO_GWO ? (size_t)2 * NP * c.W : 16);
+    QPM_ALLOC(e->gthr, (size_t)(P->G + 1));
     QPM_ALLOC(e->slot_of, NP);
     QPM_ALLOC(e->spare_of, NP);
-    QPM_ALLOC(e->jrand, NP);
-    QPM_ALLOC(e->top1, 8);
+    QPM_ALLOC(e->jrand, 2 * NP);
     QPM_ALLOC(e->fit, NP);
     QPM_ALLOC(e->cand, NP);
     QPM_ALLOC(e->scratch, NP);
-    QPM_ALLOC(e->leafsum, leaves.size());
-    QPM_ALLOC(e->leaf_off, leaves.size());
-    QPM_ALLOC(e->keys, NP);
-    QPM_ALLOC(e->picks, NP);
-    QPM_ALLOC(e->accepted, NP);
+    QPM_ALLOC(e->tree_i, ht.leaf_off.size() + ht.kid.size() + ht.lvl.size());
+    QPM_ALLOC(e->tree_v, 2 * (size_t)c.n_leaf);
+    QPM_ALLOC(e->keys, 2 * NP);
+    QPM_ALLOC(e->picks, 2 * NP);
     QPM_ALLOC(e->sched, (size_t)(P->G + 1) * QPM_SCHED_COLS);
     QPM_ALLOC(e->trace, (size_t)(P->G + 1) * 5);
     QPM_ALLOC(e->st, 1);
@@ -776,6 +1339,14 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         engine_free(e);
         return rc;
     }
+    std::vector<int32_t> tree_host;
+    tree_host.insert(tree_host.end(), ht.leaf_off.begin(), ht.leaf_off.end());
+    tree_host.insert(tree_host.end(), ht.kid.begin(), ht.kid.end());
+    tree_host.insert(tree_host.end(), ht.lvl.begin(), ht.lvl.end());
+    e->tree.leaf_off = e->tree_i;
+    e->tree.kid = e->tree_i + ht.leaf_off.size();
+    e->tree.lvl = e->tree_i + ht.leaf_off.size() + ht.kid.size();
+    e->tree.val = e->tree_v;
     // host-side constants of the state: p_plus thresholds (optimizer.py:362-365)
     EngineState hs;
     memset(&hs, 0, sizeof(hs));
@@ -783,19 +1354,35 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         double pp = (double)cnt / (double)c.k;
         if (P->discreteness_factor != 1.0) pp = 0.5 + P->discreteness_factor * (pp - 0.5);
         hs.thr_plus[cnt] = lt_threshold(pp);
+        if (cnt < 5) c.thr_plus[cnt] = make_thr(hs.thr_plus[cnt]);
     }
+    c.plus_dyadic = (c.k == 4 && P->discreteness_factor == 1.0) ? 1 : 0;
     hs.g = 0;
+    hs.g_plan = 1;
     hs.F = P->f_max;
+    // per-generation wolf thresholds from the schedule table (optimizer.py:447-453)
+    std::vector<GenThr> gth((size_t)P->G + 1);
+    for (int64_t g = 0; g <= P->G; ++g) {
+        const double *sg = sched + g * QPM_SCHED_COLS;
+        gth[g].sl = make_thr(lt_threshold(sg[QPM_SCHED_P_SL]));
+        gth[g].dist = make_thr(lt_threshold(sg[QPM_SCHED_P_DIST]));
+        gth[g].flip = make_thr(lt_threshold(sg[QPM_SCHED_P_FLIP]));
+        gth[g].early = sg[QPM_SCHED_EARLY] != 0.0 ? 1u : 0u;
+        gth[g].pad = 0;
+    }
     cudaError_t err = cudaMemcpyAsync(e->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, e->stream);
+    if (err == cudaSuccess)
+        err = cudaMemcpyAsync(e->gthr, gth.data(), sizeof(GenThr) * gth.size(), cudaMemcpyHostToDevice, e->stream);
     if (err == cudaSuccess)
         err = cudaMemcpyAsync(e->sched, sched, sizeof(double) * (P->G + 1) * QPM_SCHED_COLS, cudaMemcpyHostToDevice,
                               e->stream);
     if (err == cudaSuccess)
-        err = cudaMemcpyAsync(e->leaf_off, leaves.data(), sizeof(int64_t) * leaves.size(), cudaMemcpyHostToDevice,
+        err = cudaMemcpyAsync(e->tree_i, tree_host.data(), sizeof(int32_t) * tree_host.size(), cudaMemcpyHostToDevice,
                               e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->trace, 0, sizeof(double) * (P->G + 1) * 5, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->genome, 0, sizeof(double) * 2 * NP * c.Dp, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->bits, 0, sizeof(uint32_t) * 2 * NP * c.W, e->stream);
+    if (err == cudaSuccess) err = cudaMemsetAsync(e->slot_bin, 0, 2 * NP, e->stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
     if (err != cudaSuccess) {
         set_error("engine upload: %s", cudaGetErrorString(err));
@@ -823,13 +1410,15 @@ int qpm_engine_init(qpm_engine *h) {
     Engine *e = h->e;
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
-    k_init_population<<<row_grid(e), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of);
+    k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of);
     QPM_LAUNCH_CHECK();
     int rc = launch_fitness(e->prob, e->bits, c.W, e->slot_of, c.NP, e->fit, e->P.fitness_mode, s, nullptr);
     if (rc) return rc;
-    k_stats<<<1, kStatsThreads, 0, s>>>(c, e->st, e->sched, e->fit, e->scratch, e->leaf_off, e->leafsum, e->trace);
-    k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->genome, e->bits, e->best_genome, e->best_bits);
+    if ((rc = launch_select_stats(e, 3, s))) return rc;
+    k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,
+                                   e->best_bits);
     QPM_LAUNCH_CHECK();
+    if (c.algorithm != QPM_ALGO_GWO && (rc = enqueue_planner(e, s))) return rc;  // generation 1's draws
     e->initialized = true;
     e->g_done = 0;
     return QPM_OK;
@@ -846,8 +1435,7 @@ int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
     if (n == 0) return QPM_OK;
     if (use_graph) {
         if (!e->exec) {
-            cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
-            QPM_CUDA_TRY(cudaStreamBeginCapture(e->stream, mode));
+            QPM_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
             int launches = 0;
             int rc = enqueue_generation(e, &launches);
             cudaGraph_t g = nullptr;
@@ -861,7 +1449,7 @@ int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
                 return QPM_ERR_CUDA;
             }
             e->graph = g;
-            QPM_CUDA_TRY(cudaGraphInstantiate(&e->exec, e->graph, 0));
+            QPM_CUDA_TRY(cudaGraphInstantiateWithFlags(&e->exec, e->graph, cudaGraphInstantiateFlagUseNodePriority));
             e->launches = launches;
         }
         for (int64_t t = 0; t < n; ++t) QPM_CUDA_TRY(cudaGraphLaunch(e->exec, e->stream));
@@ -886,10 +1474,9 @@ int qpm_engine_finalize(qpm_engine *h) {
     }
     const RunConsts &c = e->c;
     if (c.algorithm == QPM_ALGO_GWO) return QPM_OK;  // best-ever is already in the result buffer
-    int rc = launch_reduce_best(e->fit, c.NP, 1, e->top1, e->stream);
-    if (rc) return rc;
-    k_finalize_best<<<1, 1, 0, e->stream>>>(e->st, e->top1);
-    k_copy_best<<<64, 256, 0, e->stream>>>(c, e->st, e->slot_of, e->genome, e->bits, e->best_genome, e->best_bits);
+    k_finalize_best<<<1, kCtaThreads, 0, e->stream>>>(c, e->st, e->fit);
+    k_copy_best<<<64, 256, 0, e->stream>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,
+                                           e->best_bits);
     k_reset_flag<<<1, 1, 0, e->stream>>>(e->st);
     QPM_LAUNCH_CHECK();
     return QPM_OK;
@@ -940,14 +1527,24 @@ int qpm_engine_read_population(qpm_engine *h, double *genome, double *fitness) {
     Engine *e = h->e;
     const RunConsts &c = e->c;
     std::vector<int32_t> slots(c.NP);
+    std::vector<uint8_t> bin(2 * c.NP);
     QPM_CUDA_TRY(cudaMemcpyAsync(slots.data(), e->slot_of, sizeof(int32_t) * c.NP, cudaMemcpyDeviceToHost, e->stream));
+    QPM_CUDA_TRY(cudaMemcpyAsync(bin.data(), e->slot_bin, 2 * c.NP, cudaMemcpyDeviceToHost, e->stream));
     if (fitness)
         QPM_CUDA_TRY(cudaMemcpyAsync(fitness, e->fit, sizeof(double) * c.NP, cudaMemcpyDeviceToHost, e->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
     if (genome) {
-        for (int64_t i = 0; i < c.NP; ++i)
-            QPM_CUDA_TRY(cudaMemcpyAsync(genome + i * c.D, e->genome + (int64_t)slots[i] * c.Dp, sizeof(double) * c.D,
-                                         cudaMemcpyDeviceToHost, e->stream));
+        std::vector<uint32_t> b(c.W);
+        for (int64_t i = 0; i < c.NP; ++i) {
+            const int64_t slot = slots[i];
+            if (bin[slot]) {
+                QPM_CUDA_TRY(cudaMemcpy(b.data(), e->bits + slot * c.W, sizeof(uint32_t) * c.W, cudaMemcpyDeviceToHost));
+                for (int64_t j = 0; j < c.D; ++j) genome[i * c.D + j] = ((b[j >> 5] >> (j & 31)) & 1u) ? -1.0 : 1.0;
+            } else {
+                QPM_CUDA_TRY(cudaMemcpyAsync(genome + i * c.D, e->genome + slot * c.Dp, sizeof(double) * c.D,
+                                             cudaMemcpyDeviceToHost, e->stream));
+            }
+        }
         QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
     }
     return QPM_OK;
@@ -1002,7 +1599,7 @@ int qpm_engine_launches_per_generation(const qpm_engine *h) {
     if (!h) return -1;
     if (h->e->launches) return h->e->launches;
     const int a = h->e->c.algorithm;
-    return a == QPM_ALGO_HYBRID ? 12 : (a == QPM_ALGO_DE ? 6 : 8);
+    return a == QPM_ALGO_HYBRID ? 8 : (a == QPM_ALGO_DE ? 4 : 6);
 }
 
 int qpm_engine_fitness_ptr(qpm_engine *h, double **fit_dev) {

@@ -32,6 +32,7 @@
 //   the row bits (required: 18% of selections compare identical projections).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -156,31 +157,74 @@ __global__ void k_fit_exact(const double2 *__restrict__ e1, const double2 *__res
 }
 
 // ------------------------------------------------------------ fast path
+// TMA (bulk-copy engine) staging of the quad-table chunks: one elected thread
+// arms an mbarrier with the byte count and issues cp.async.bulk; consumers
+// wait on the barrier's phase.  Two buffers, so chunk k+1 streams in while
+// chunk k is scanned.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr int kChunkEntries = kQuadsPerChunk * kQuadEntries;  // 768 double2 = 12 KB
+constexpr uint32_t kChunkBytes = kChunkEntries * sizeof(double2);
+
 template <bool THG>
 __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,
                                                           int64_t nchunks, int seg_chunks, int S,
                                                           const uint32_t *__restrict__ bits, int64_t W,
                                                           const int32_t *__restrict__ row_index, int64_t rows,
                                                           double *__restrict__ part) {
-    __shared__ __align__(128) double2 tab[kQuadsPerChunk * kQuadEntries];  // 12 KB
+    __shared__ __align__(128) double2 tab[2][kChunkEntries];  // 2 x 12 KB
+    __shared__ __align__(8) uint64_t bar[2];
     const int s = blockIdx.x;
     const int lam = blockIdx.z;
     const int tid = threadIdx.x;
     const int64_t r = (int64_t)blockIdx.y * kFitThreads + tid;
     const bool active = r < rows;
-    const uint4 *rb = reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? row_index[r] : r) : 0) * W);
+    const uint4 *rb =
+        reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? row_index[r] : r) : 0) * W);
     const double2 *qtl = qt + (int64_t)lam * nquads * kQuadEntries;
-    double ar = 0.0, ai = 0.0, pr = 0.0, pi = 0.0, tr = 0.0, ti = 0.0;
     const int64_t c0 = (int64_t)s * seg_chunks;
-    const int64_t c1 = c0 + seg_chunks < nchunks ? c0 + seg_chunks : nchunks;
-    for (int64_t c = c0; c < c1; ++c) {
-        __syncthreads();
-        const double2 *src = qtl + c * (kQuadsPerChunk * kQuadEntries);
-#pragma unroll
-        for (int k = 0; k < (kQuadsPerChunk * kQuadEntries) / kFitThreads; ++k)
-            tab[k * kFitThreads + tid] = src[k * kFitThreads + tid];
-        uint4 w4 = active ? rb[c] : make_uint4(0, 0, 0, 0);
-        __syncthreads();
+    const int n = (int)((c0 + seg_chunks < nchunks ? c0 + seg_chunks : nchunks) - c0);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        bulk_load(tab[0], qtl + c0 * kChunkEntries, kChunkBytes, &bar[0]);
+        if (n > 1) bulk_load(tab[1], qtl + (c0 + 1) * kChunkEntries, kChunkBytes, &bar[1]);
+    }
+    double ar = 0.0, ai = 0.0, pr = 0.0, pi = 0.0, tr = 0.0, ti = 0.0;
+    for (int k = 0; k < n; ++k) {
+        const int buf = k & 1;
+        const uint4 w4 = active ? rb[c0 + k] : make_uint4(0, 0, 0, 0);
+        mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
+        const double2 *tb = tab[buf];
         const uint32_t words[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
         for (int q = 0; q < kQuadsPerChunk; ++q) {
@@ -188,7 +232,7 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
             const uint32_t s0 = nib & 1u;
             const uint32_t rel = ((nib ^ (0u - s0)) >> 1) & 7u;
             const uint64_t m = sign_mask64(s0);
-            const double2 *tq = tab + q * kQuadEntries;
+            const double2 *tq = tb + q * kQuadEntries;
             const double2 E = tq[8 + rel];
             const double ser = flip_if(E.x, m), sei = flip_if(E.y, m);
             if (THG) {
@@ -207,6 +251,8 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
             pr += ser;
             pi += sei;
         }
+        __syncthreads();  // every lane is done with tab[buf]
+        if (tid == 0 && k + 2 < n) bulk_load(tab[buf], qtl + (c0 + k + 2) * kChunkEntries, kChunkBytes, &bar[buf]);
     }
     if (!active) return;
     double *o = part + (((int64_t)lam * rows + r) * S + s) * kPartDoubles;
@@ -227,31 +273,71 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
     }
 }
 
-// stitch segments, apply w/hconst, |.| (glibc hypot), scale, objective
-__global__ void k_fit_finish(const double *__restrict__ part, int S, int64_t rows, int n_wl,
-                             const double2 *__restrict__ w, const double2 *__restrict__ h, int thg, double scale,
-                             int multi, double g0, double beta, double *__restrict__ gains,
-                             double *__restrict__ out) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// stitch segments, apply w/hconst, |.| (glibc hypot), scale, objective.
+// One warp per row: lane l stitches a contiguous run of segments, then the
+// 32 runs are stitched by a fixed shuffle tree (deterministic).  Segment
+// concatenation: (a1, P1, T1) . (a2, P2, T2) = (a1 + a2 + P1 T2, P1 + P2, T1 + T2).
+struct Seg {
+    double ar, ai, pr, pi, tr, ti;
+};
+
+__device__ __forceinline__ Seg seg_cat(const Seg &x, const Seg &y) {
+    Seg z;
+    z.ar = (x.ar + y.ar) + fma(x.pr, y.tr, -x.pi * y.ti);
+    z.ai = (x.ai + y.ai) + fma(x.pr, y.ti, x.pi * y.tr);
+    z.pr = x.pr + y.pr;
+    z.pi = x.pi + y.pi;
+    z.tr = x.tr + y.tr;
+    z.ti = x.ti + y.ti;
+    return z;
+}
+
+constexpr int kFinishWarps = 4;
+
+__global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
+    const double *__restrict__ part, int S, int64_t rows, int n_wl, const double2 *__restrict__ w,
+    const double2 *__restrict__ h, int thg, double scale, int multi, double g0, double beta,
+    double *__restrict__ gains, double *__restrict__ out) {
+    const int64_t r = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (r >= rows) return;
+    const int per = (S + 31) / 32;
+    const int s0 = lane * per;
+    const int s1 = s0 + per < S ? s0 + per : S;
     double gmax = 0.0, gmin = 0.0;
     for (int lam = 0; lam < n_wl; ++lam) {
         const double *p = part + ((int64_t)lam * rows + r) * S * kPartDoubles;
-        double ar = p[0], ai = p[1], cr = p[2], ci = p[3];
-        for (int s = 1; s < S; ++s) {
-            const double *q = p + (int64_t)s * kPartDoubles;
-            double xr = fma(cr, q[4], fma(-ci, q[5], q[0]));
-            double xi = fma(cr, q[5], fma(ci, q[4], q[1]));
-            ar += xr;
-            ai += xi;
-            cr += q[2];
-            ci += q[3];
+        double ar, ai;
+        if (S == 1) {
+            ar = p[0];  // exact mode: the row's sum, untouched
+            ai = p[1];
+        } else {
+            Seg acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int s = s0; s < s1; ++s) {
+                const double *q = p + (int64_t)s * kPartDoubles;
+                const Seg y = {q[0], q[1], q[2], q[3], q[4], q[5]};
+                acc = s == s0 ? y : seg_cat(acc, y);
+            }
+            for (int off = 1; off < 32; off <<= 1) {
+                Seg o;
+                o.ar = __shfl_down_sync(0xffffffffu, acc.ar, off);
+                o.ai = __shfl_down_sync(0xffffffffu, acc.ai, off);
+                o.pr = __shfl_down_sync(0xffffffffu, acc.pr, off);
+                o.pi = __shfl_down_sync(0xffffffffu, acc.pi, off);
+                o.tr = __shfl_down_sync(0xffffffffu, acc.tr, off);
+                o.ti = __shfl_down_sync(0xffffffffu, acc.ti, off);
+                const bool has_other = lane + off < 32 && (lane + off) * per < S;
+                if ((lane & (2 * off - 1)) == 0 && has_other) acc = seg_cat(acc, o);
+            }
+            ar = acc.ar;
+            ai = acc.ai;
         }
-        double2 ww = w[lam];
+        if (lane != 0) continue;
+        const double2 ww = w[lam];
         double zr = ww.x * ar - ww.y * ai;
         double zi = ww.x * ai + ww.y * ar;
         if (thg) {
-            double2 hh = h[lam];
+            const double2 hh = h[lam];
             zr += hh.x;
             zi += hh.y;
         }
@@ -265,6 +351,7 @@ __global__ void k_fit_finish(const double *__restrict__ part, int S, int64_t row
         if (lam == 0 || g < gmin) gmin = g;
         gains[r * n_wl + lam] = g;
     }
+    if (lane != 0) return;
     double *dv = gains + r * n_wl;
     for (int lam = 0; lam < n_wl; ++lam) dv[lam] = fabs(g0 - dv[lam]);
     double f = pairwise_sum_seq(dv, n_wl);
@@ -367,9 +454,8 @@ int launch_fitness(Problem *p, const uint32_t *bits, int64_t row_words, const in
                                                                 bits, p->W, row_index, rows, p->part);
     }
     QPM_LAUNCH_CHECK();
-    k_fit_finish<<<(unsigned)((rows + 127) / 128), 128, 0, stream>>>(p->part, S, rows, p->n_wl, p->w, p->h, thg,
-                                                                     p->scale, p->multi, p->g0, p->beta, p->gains,
-                                                                     out);
+    k_fit_finish<<<(unsigned)((rows + kFinishWarps - 1) / kFinishWarps), 32 * kFinishWarps, 0, stream>>>(
+        p->part, S, rows, p->n_wl, p->w, p->h, thg, p->scale, p->multi, p->g0, p->beta, p->gains, out);
     QPM_LAUNCH_CHECK();
     if (launches) *launches += 2;
     return QPM_OK;
@@ -464,9 +550,14 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
     p.W = round_up((D + 31) / 32, 4);
     p.nquads = p.W * 8;
     p.nchunks = p.W / 4;
-    // segments: one 128-domain chunk per segment for a single wavelength;
-    // longer segments when the wavelength axis already supplies parallelism
-    p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, n_wl));
+    // segment length (in 128-domain chunks) depends only on D and the
+    // wavelength count, never on the batch, so fitness stays a pure function
+    // of the row bits; longer segments when wavelengths supply parallelism
+    p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, n_wl > 1 ? 4 * std::min(n_wl, 8) : 4));
+    if (const char *env = getenv("QPM_SEG_CHUNKS")) {  // tuning override (changes fitness rounding only)
+        const int v = atoi(env);
+        if (v >= 1) p.seg_chunks = (int)std::min<int64_t>(p.nchunks, v);
+    }
     p.S = (int)((p.nchunks + p.seg_chunks - 1) / p.seg_chunks);
     p.scale = scale;
     p.g0 = g0;

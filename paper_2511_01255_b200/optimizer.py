@@ -228,8 +228,11 @@ class Engine:
         self.NP = int(pop_size)
         self.G = int(generations)
         self.D = objective.dimension
-        # a dedicated stream: CUDA graphs cannot be captured on the legacy default stream
-        self.stream = stream if stream is not None else torch.cuda.Stream(dev)
+        # a dedicated high-priority stream (CUDA graphs cannot be captured on the
+        # legacy default stream; the engine's planner runs on a low-priority one)
+        if stream is None:
+            stream = torch.cuda.Stream(dev, priority=min(torch.cuda.Stream.priority_range()))
+        self.stream = stream
         mode = fitness_mode or objective.mode
         from .objectives import MODES
         from .rng import signed64
