@@ -103,6 +103,7 @@ struct RunConsts {
     int32_t n_leaf, n_levels;
     Thr thr_cr;      // u <= CR (de_crossover)
     int plus_dyadic; // K = 4 and p_plus(c) = c/4 exactly: plus level = 1 + floor(4u)
+    uint32_t m4;     // = 4, a runtime constant (see xs30_fma)
     Thr thr_plus[5]; // u_plus < p_plus(count), count = 0..K (hybrid K <= 4)
 };
 
@@ -270,9 +271,18 @@ struct PlanArgs {
     uint32_t *planes;  // [2][NP][W][8]
 };
 
-__device__ __forceinline__ uint64_t mix_pre2(uint64_t key, uint32_t p1) {
+// z ^= z >> 30 with the shifts done as multiplies on the FMA pipe (the ALU
+// pipe is the binding one in this kernel); m4 = 4 is a runtime value so
+// ptxas cannot turn the multiplies back into shifts.
+__device__ __forceinline__ uint64_t xs30_fma(uint64_t z, uint32_t m4) {
+    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+    const uint32_t nlo = lo ^ __umulhi(lo, m4) ^ (hi * m4);
+    const uint32_t nhi = hi ^ __umulhi(hi, m4);
+    return ((uint64_t)nhi << 32) | nlo;
+}
+__device__ __forceinline__ uint64_t mix_pre2(uint64_t key, uint32_t p1, uint32_t m4) {
     uint64_t z = key + (uint64_t)p1 * kGold;
-    z = (z ^ (z >> 30)) * kMix1;
+    z = xs30_fma(z, m4) * kMix1;
     return z ^ (z >> 27);
 }
 __device__ __forceinline__ uint32_t mix_hi2(uint64_t x) {  // high word of x * kMix2
@@ -325,7 +335,7 @@ __device__ __forceinline__ void plan_chunk(const RunConsts &c, const PlanArgs &a
         const bool in = FULL || j < (int)c.D;
         bool take = false;
         if (in) {
-            const uint64_t x = mix_pre2(key, p_mask + (uint32_t)j);
+            const uint64_t x = mix_pre2(key, p_mask + (uint32_t)j, c.m4);
             take = passes_hi(c.thr_cr, x, mix_hi2(x)) || j == jr;
         }
         const uint32_t mword = __ballot_sync(0xffffffffu, take);
@@ -335,9 +345,9 @@ __device__ __forceinline__ void plan_chunk(const RunConsts &c, const PlanArgs &a
             uint32_t pick = 0, L = 0;
             if (in) {
                 const uint32_t p0 = p_wolf + (uint32_t)j;
-                const uint64_t x1 = mix_pre2(key, p0);
+                const uint64_t x1 = mix_pre2(key, p0, c.m4);
                 soc = passes_hi(t.sl, x1, mix_hi2(x1));
-                const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)));
+                const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)), c.m4);
                 const uint32_t h2 = mix_hi2(x2);
                 if (K == 4) {
                     pick = h2 >> 30;  // int(u * 4) = top two bits
@@ -347,7 +357,7 @@ __device__ __forceinline__ void plan_chunk(const RunConsts &c, const PlanArgs &a
                     pick = (uint32_t)(pv < K - 1 ? pv : K - 1);
                 }
                 f2 = passes_hi(EARLY ? t.dist : t.flip, x2, h2);
-                const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D));
+                const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c.m4);
                 const uint32_t h3 = mix_hi2(x3);
                 st = (h3 >> 31) == 0u;  // u < 0.5
                 if (EARLY) {
@@ -457,6 +467,8 @@ struct TrialArgs {
 template <bool BIN, bool FULL>
 __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
                                                double F) {
+    // Each lane owns an adjacent gene pair (16-byte loads and stores); a warp
+    // covers 64 genes = 2 mask words and 2 sign words per step.
     const int4 pk = a.picks[b * c.NP + i];
     const RowRef xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
     const RowRef x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
@@ -468,36 +480,68 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const uint32_t *mrow = a.mask + (b * c.NP + i) * c.W;
     const int D = (int)c.D;
     const int lane = threadIdx.x & 31;
-    double va[kGenesPerThread], vb[kGenesPerThread], vc[kGenesPerThread];
-    bool take[kGenesPerThread];
+    const int warp = threadIdx.x >> 5;
+    constexpr int kSteps = kGenesPerBlock / (kRowThreads * 2);  // 2 pair-steps per 1024-gene chunk
+    // all mask words, then all genome loads of the chunk, then the math:
+    // the kernel is bound by memory latency, so keep every load in flight
+    uint32_t mb[kSteps];
 #pragma unroll
-    for (int it = 0; it < kGenesPerThread; ++it) {
-        const int j = jc + it * kRowThreads + threadIdx.x;
-        va[it] = vb[it] = vc[it] = 0.0;
-        take[it] = false;
-        if (!FULL && j - lane >= (int)c.Dp) continue;
-        take[it] = (mrow[(j - lane) >> 5] >> lane) & 1u;
+    for (int st = 0; st < kSteps; ++st) {
+        const int j64 = jc + (st * (kRowThreads / 32) + warp) * 64;
+        mb[st] = 0u;
+        if (FULL || j64 < (int)c.Dp) mb[st] = (mrow[(j64 >> 5) + (lane >> 4)] >> ((2 * lane) & 31)) & 3u;
+    }
+    double2 y[kSteps], p1[kSteps], p2[kSteps], p3[kSteps];
+#pragma unroll
+    for (int st = 0; st < kSteps; ++st) {
+        const int j = jc + (st * (kRowThreads / 32) + warp) * 64 + 2 * lane;
+        y[st] = p1[st] = p2[st] = p3[st] = make_double2(0.0, 0.0);
         if (!FULL && j >= D) continue;
-        if (take[it]) {
-            va[it] = BIN ? x1.at(j) : x1.f[j];
-            vb[it] = BIN ? x2.at(j) : x2.f[j];
-            vc[it] = BIN ? x3.at(j) : x3.f[j];
+        if (BIN) {
+            y[st] = make_double2(xi.at(j), xi.at(j + 1));
+            p1[st] = make_double2(x1.at(j), x1.at(j + 1));
+            p2[st] = make_double2(x2.at(j), x2.at(j + 1));
+            p3[st] = make_double2(x3.at(j), x3.at(j + 1));
         } else {
-            va[it] = BIN ? xi.at(j) : xi.f[j];
+            if (mb[st] != 3u) y[st] = *reinterpret_cast<const double2 *>(xi.f + j);
+            if (mb[st] != 0u) {
+                p1[st] = *reinterpret_cast<const double2 *>(x1.f + j);
+                p2[st] = *reinterpret_cast<const double2 *>(x2.f + j);
+                p3[st] = *reinterpret_cast<const double2 *>(x3.f + j);
+            }
         }
     }
 #pragma unroll
-    for (int it = 0; it < kGenesPerThread; ++it) {
-        const int j = jc + it * kRowThreads + threadIdx.x;
-        if (!FULL && j - lane >= (int)c.Dp) break;
-        bool neg = false;
+    for (int st = 0; st < kSteps; ++st) {
+        const int j64 = jc + (st * (kRowThreads / 32) + warp) * 64;  // this warp's 64-gene span
+        if (!FULL && j64 >= (int)c.Dp) break;
+        const int j = j64 + 2 * lane;
+        bool n0 = false, n1 = false;
         if (FULL || j < D) {
-            const double v = take[it] ? va[it] + F * (vb[it] - vc[it]) : va[it];
-            out[j] = v;
-            neg = !(v >= 0.0);
+            const double v0 = (mb[st] & 1u) ? p1[st].x + F * (p2[st].x - p3[st].x) : y[st].x;
+            double v1 = (mb[st] & 2u) ? p1[st].y + F * (p2[st].y - p3[st].y) : y[st].y;
+            const bool in1 = FULL || j + 1 < D;
+            if (!in1) v1 = 0.0;
+            *reinterpret_cast<double2 *>(out + j) = make_double2(v0, v1);
+            n0 = !(v0 >= 0.0);
+            n1 = in1 && !(v1 >= 0.0);
         }
-        const uint32_t word = __ballot_sync(0xffffffffu, neg);
-        if (lane == 0) bout[(j - lane) >> 5] = word;
+        // sign bits: lane l holds genes 2l, 2l+1 -> interleave two ballots
+        const uint32_t be = __ballot_sync(0xffffffffu, n0);
+        const uint32_t bo = __ballot_sync(0xffffffffu, n1);
+        if (lane < 2) {
+            uint32_t e = lane ? (be >> 16) : (be & 0xffffu);
+            uint32_t o = lane ? (bo >> 16) : (bo & 0xffffu);
+            e = (e | (e << 8)) & 0x00ff00ffu;
+            e = (e | (e << 4)) & 0x0f0f0f0fu;
+            e = (e | (e << 2)) & 0x33333333u;
+            e = (e | (e << 1)) & 0x55555555u;
+            o = (o | (o << 8)) & 0x00ff00ffu;
+            o = (o | (o << 4)) & 0x0f0f0f0fu;
+            o = (o | (o << 2)) & 0x33333333u;
+            o = (o | (o << 1)) & 0x55555555u;
+            bout[(j64 >> 5) + lane] = e | (o << 1);
+        }
     }
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[out_slot] = 0;
 }
@@ -637,56 +681,73 @@ __device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
     return a.v > b.v || (a.v == b.v && a.i < b.i);
 }
 
-// top-K of vals[0..n) by (-value, index) (parexec.reduce_best), whole CTA:
-// K rounds of a block argmax that skips the winners of earlier rounds.
-// Register-light on purpose (1024-thread CTAs get 64 registers).
+// top-K of vals[0..n) by (-value, index) (parexec.reduce_best), whole CTA.
+// Every thread keeps a sorted K-list of its strided elements; lists are
+// merged by a fixed shuffle tree inside each warp, then across warps by warp
+// 0.  Insertion is a static bubble (compare-swap down the list), so the lists
+// stay in registers.  Deterministic: (-value, index) is a total order.
 template <int K>
-__device__ void block_topk(const double *vals, int64_t n, int32_t *out) {
-    __shared__ double s_v[32];
-    __shared__ int32_t s_i[32];
-    __shared__ int32_t s_win;
-    int32_t taken[K];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+__device__ __forceinline__ void topk_insert(Cand (&L)[K], Cand e) {
 #pragma unroll
     for (int t = 0; t < K; ++t) {
-        Cand best = {0.0, -1};
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            bool tk = false;
-#pragma unroll
-            for (int u = 0; u < t; ++u) tk |= taken[u] == (int32_t)i;
-            const Cand cd = {vals[i], (int32_t)i};
-            if (!tk && better(cd, best)) best = cd;
+        if (better(e, L[t])) {
+            const Cand tmp = L[t];
+            L[t] = e;
+            e = tmp;
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            Cand o;
-            o.v = __shfl_down_sync(0xffffffffu, best.v, off);
-            o.i = __shfl_down_sync(0xffffffffu, best.i, off);
-            if (better(o, best)) best = o;
-        }
-        if (lane == 0) {
-            s_v[warp] = best.v;
-            s_i[warp] = best.i;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            Cand w = lane < nwarps ? Cand{s_v[lane], s_i[lane]} : Cand{0.0, -1};
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                Cand o;
-                o.v = __shfl_down_sync(0xffffffffu, w.v, off);
-                o.i = __shfl_down_sync(0xffffffffu, w.i, off);
-                if (better(o, w)) w = o;
-            }
-            if (lane == 0) {
-                s_win = w.i;
-                out[t] = w.i;
-            }
-        }
-        __syncthreads();
-        taken[t] = s_win;
-        __syncthreads();
     }
+}
+
+template <int K>
+__device__ __forceinline__ void topk_warp_merge(Cand (&L)[K]) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        Cand o[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            o[t].v = __shfl_down_sync(0xffffffffu, L[t].v, off);
+            o[t].i = __shfl_down_sync(0xffffffffu, L[t].i, off);
+        }
+        if ((threadIdx.x & 31) + off < 32) {
+#pragma unroll
+            for (int t = 0; t < K; ++t) topk_insert<K>(L, o[t]);
+        }
+    }
+}
+
+template <int K>
+__device__ void block_topk(const double *vals, int64_t n, int32_t *out) {
+    __shared__ double s_v[32][K];
+    __shared__ int32_t s_i[32][K];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // few warps while n is small: the merge tree costs the same per warp
+    const int nwarps = min((int)(blockDim.x >> 5), max(1, (int)((n + 127) / 128)));
+    const int nthr = nwarps * 32;
+    Cand L[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) L[t] = {0.0, -1};
+    if (warp < nwarps) {
+        for (int64_t i = threadIdx.x; i < n; i += nthr) topk_insert<K>(L, Cand{vals[i], (int32_t)i});
+        topk_warp_merge<K>(L);
+    }
+    if (lane == 0 && warp < nwarps) {
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            s_v[warp][t] = L[t].v;
+            s_i[warp][t] = L[t].i;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int t = 0; t < K; ++t) L[t] = lane < nwarps ? Cand{s_v[lane][t], s_i[lane][t]} : Cand{0.0, -1};
+        topk_warp_merge<K>(L);
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < K; ++t) out[t] = L[t].i;
+        }
+    }
+    __syncthreads();
 }
 
 __device__ void block_topk_k(const double *vals, int64_t n, int k, int32_t *out) {
@@ -756,6 +817,12 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
                                                               double *__restrict__ scratch, SumTree tr,
                                                               double *__restrict__ trace) {
     const int64_t n = c.NP;
+    __shared__ EngineState s_state;
+    {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(st);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(&s_state);
+        for (int t = threadIdx.x; t < (int)(sizeof(EngineState) / 4); t += blockDim.x) dst[t] = src[t];
+    }
     if (mode != 3) {
         int32_t lead[kMaxLeaders];
 #pragma unroll
@@ -842,8 +909,12 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     __syncthreads();
     const double var = block_pairwise(sq, n, c, tr) / (double)n;
     if (threadIdx.x != 0) return;
+    // serial tail on the shared-memory copy of the state (fetched at entry);
+    // only the fields this kernel owns are written back (g_plan belongs to
+    // the planner stream)
+    const EngineState &ss = s_state;
     const double sd = sqrt(var);
-    const int64_t g = st->g;
+    const int64_t g = ss.g;
     double *row = trace + g * 5;
     row[0] = (double)g;
     row[1] = mx;
@@ -851,7 +922,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     row[4] = sd;
     if (c.algorithm == QPM_ALGO_GWO) {
         row[3] = g == 0 ? c.gwo_a0 : sched[g * QPM_SCHED_COLS + QPM_SCHED_A_NOW];
-        if (g == 0 || mx > st->best_fit) {
+        if (g == 0 || mx > ss.best_fit) {
             st->best_fit = mx;
             st->best_idx = (int32_t)amx;
             st->best_flag = 1;
@@ -867,26 +938,26 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     } else {
         // convergence window: deque(maxlen=conv_window) of best_now > best_prev
         const int cap = c.conv_window;
-        uint8_t win[kMaxWindow];
-        int len = st->win_len;
-        for (int t = 0; t < len; ++t) win[t] = st->win[t];
-        const uint8_t improved = mx > st->best_prev ? 1 : 0;
-        if (len < cap) {
-            win[len++] = improved;
-        } else {
-            for (int t = 1; t < cap; ++t) win[t - 1] = win[t];
-            win[cap - 1] = improved;
-        }
+        int len = ss.win_len;
+        const uint8_t improved = mx > ss.best_prev ? 1 : 0;
         int cnt = 0;
-        for (int t = 0; t < len; ++t) {
-            cnt += win[t];
-            st->win[t] = win[t];
+        if (len < cap) {
+            for (int t = 0; t < len; ++t) cnt += ss.win[t];
+            st->win[len] = improved;
+            ++len;
+        } else {
+            for (int t = 1; t < cap; ++t) {
+                st->win[t - 1] = ss.win[t];
+                cnt += ss.win[t];
+            }
+            st->win[cap - 1] = improved;
         }
+        cnt += improved;
         st->win_len = len;
         st->best_prev = mx;
         const double conv = len ? (double)cnt / (double)len : 1.0;
         const double *sg = sched + g * QPM_SCHED_COLS;
-        const double base = st->baseline_std;
+        const double base = ss.baseline_std;
         double f = sg[QPM_SCHED_F_ENV];
         if (c.adaptive) {
             const double tl = c.theta_low_frac * base;
@@ -1357,6 +1428,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (cnt < 5) c.thr_plus[cnt] = make_thr(hs.thr_plus[cnt]);
     }
     c.plus_dyadic = (c.k == 4 && P->discreteness_factor == 1.0) ? 1 : 0;
+    c.m4 = 4;
     hs.g = 0;
     hs.g_plan = 1;
     hs.F = P->f_max;
