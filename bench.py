@@ -192,7 +192,7 @@ def run_reference(args):
 
 
 def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db):
-    """Roofline of the dominant stage (largest mean ms per generation)."""
+    """Roofline of the dominant main-stream stage (largest mean ms per generation)."""
     name, ms = max(stages, key=lambda s: s[1])
     if name.startswith("fitness"):
         evals = NP * D  # the engine evaluates NP rows per fitness launch
@@ -235,6 +235,7 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     import paper_2511_01255_b200 as q
+    from paper_2511_01255_b200.distributed import ShardedEngine, broadcast_unique_id, run_sharded
 
     dev = torch.device("cuda", torch.cuda.current_device())
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -242,11 +243,18 @@ def run_ours(args):
     obj = build_objective(q)
     de, gwo, sch = q.DEParams(), q.GWOParams(), q.Schedules()
     G = max(G_RUN, args.warmup + args.steps)
+    np_total = NP * world  # weak scaling: 1,024 rows per GPU
+    evals_gen = (2 * np_total - 4) * D
     stream = torch.cuda.Stream(dev, priority=min(torch.cuda.Stream.priority_range()))
-    # replicas with per-rank seeds until the sharded engine lands
-    eng = q.Engine(obj, "hybrid", pop_size=NP, generations=G, seed=SEED + rank, de=de, gwo=gwo, sch=sch,
-                   stream=stream)
-    eng.init()
+
+    def make_engine():
+        uid = broadcast_unique_id() if world > 1 else None
+        eng = ShardedEngine.create(obj, "hybrid", pop_size=np_total, generations=G, seed=SEED, de=de, gwo=gwo,
+                                   sch=sch, rank=rank, world=world, nccl_id=uid, stream=stream)
+        eng.init()
+        return eng
+
+    eng = make_engine()
     eng.step(args.warmup)
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -272,8 +280,7 @@ def run_ours(args):
 
     # per-stage breakdown of the same workload, CUDA events on the engine stream
     prof_gens = 20
-    eng2 = q.Engine(obj, "hybrid", pop_size=NP, generations=G, seed=SEED, de=de, gwo=gwo, sch=sch, stream=stream)
-    eng2.init()
+    eng2 = make_engine()
     eng2.step(args.warmup)
     stages = eng2.profile(prof_gens)
     torch.cuda.synchronize()
@@ -288,30 +295,41 @@ def run_ours(args):
 
     # end to end through the public API (host buffers, everything inside the clock)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
-    res = q.run_hybrid(obj, dimension=D, pop_size=NP, generations=args.steps, seed=SEED)
+    if world > 1:
+        res = run_sharded("hybrid", obj, dimension=D, pop_size=np_total, generations=args.steps, seed=SEED)
+    else:
+        res = q.run_hybrid(obj, dimension=D, pop_size=NP, generations=args.steps, seed=SEED)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
     h2d = (args.steps + 1) * 8 * 8 + 256
     d2h = (args.steps + 1) * 5 * 8 + D * 9 + 8 + 64
-    e2e = {"value": evals_per_generation() * args.steps * world / e2e_s, "unit": UNIT,
+    e2e = {"value": evals_gen * args.steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-           "what": "public run_hybrid(objective, generations=K) call: engine allocation, schedule upload, init, "
-                   "K generations, trace + best individual read back", "seconds": e2e_s,
+           "what": "public run_hybrid(objective, generations=K) call (run_sharded for N > 1): engine allocation, "
+                   "schedule upload, init, K generations, trace + best individual read back", "seconds": e2e_s,
            "best_fitness": res.best.fitness}
 
     if rank == 0:
         cpu = cpu_baseline() if (world == 1 and not args.no_cpu_baseline) else None
-        value = evals_per_generation() * args.steps * world / (ms * 1e-3)
+        value = evals_gen * args.steps / (ms * 1e-3)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_gen, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded init_population, C2 shape)",
-                "config": {"workload": "C2 run_hybrid NP=1024 D=10000 THG 1404nm t=1um, 1000 generations",
-                           "NP": NP, "D": D, "generations": G, "fitness_mode": "fast",
+                "config": {"workload": f"C2 run_hybrid D=10000 THG 1404nm t=1um, NP=1024 per GPU "
+                                       f"(NP={np_total}), {G} generations",
+                           "NP": np_total, "D": D, "generations": G, "fitness_mode": "fast",
                            "timed_generations": [args.warmup + 1, args.warmup + args.steps],
-                           "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                           "l2": "genome pool 164 MB > 126 MB L2; no flush"},
-                "generations_per_s": 1e3 / ms_gen * world, "best_after_timed": best_after,
+                           "parallelism": (f"row-sharded x{world}: NCCL all-gather of candidate fitness and "
+                                           f"wolf rows, replicated genome") if world > 1 else "1 GPU",
+                           "l2": "genome pool 2 x NP x D f64 (164 MB per 1,024 rows) > 126 MB L2; no flush"},
+                "generations_per_s": 1e3 / ms_gen, "best_after_timed": best_after,
                 "roofline": roof, "stages": [{"name": n, "ms": m} for n, m in stages],
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
                 "peaks": peaks_kind}

@@ -160,6 +160,28 @@ int qpm_engine_generation(const qpm_engine *e, int64_t *g_done);
 int qpm_engine_read_trace(qpm_engine *e, int64_t first_row, int64_t n_rows, double *host_rows);
 int qpm_engine_read_best(qpm_engine *e, double *genome, int8_t *proj, double *fitness);
 int qpm_engine_read_population(qpm_engine *e, double *genome, double *fitness);
+/* ------------------------------------------------------------ multi-GPU
+ * One process per GPU, rows sharded in equal contiguous slices
+ * [rank NP/world, (rank+1) NP/world) (set row_lo/row_hi in qpm_run_params).
+ * Every rank keeps the whole population; after each fitness phase the
+ * candidate fitness vector is all-gathered over NCCL and foreign accepted
+ * trials / wolf candidates are recomputed locally from the same counter
+ * streams (bit-identical to one GPU).  Replaces the reference's in-process
+ * thread pool (parexec.py:73-120). */
+/* rank 0 creates the NCCL id (128 bytes) and broadcasts it to the others */
+int qpm_nccl_unique_id(uint8_t *id_out);
+int qpm_engine_set_comm(qpm_engine *e, int rank, int world, const uint8_t *id);
+/* shard without a communicator: the caller exchanges qpm_engine_cand_ptr()
+ * slices between phases (single-GPU emulation of several ranks in tests) */
+int qpm_engine_set_shard(qpm_engine *e, int rank, int world);
+int qpm_engine_phases(const qpm_engine *e);
+int qpm_engine_run_phase(qpm_engine *e, int phase);
+/* emulated exchange before `phase`: copy src's own slices (candidate
+ * fitness; staged wolf candidates before phase 2) into dst (synchronous) */
+int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase);
+int qpm_engine_cand_ptr(qpm_engine *e, double **cand_dev);
+int qpm_engine_stream(qpm_engine *e, void **stream);
+
 /* run n generations eagerly with CUDA events between the stages of each
  * generation (advances the run); stage_ms[k] = mean ms of stage k, names
  * are written as n_stages fixed-width strings of name_len bytes */

@@ -25,7 +25,9 @@ EXPORTS = (
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
     "qpm_engine_step", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
     "qpm_engine_read_best", "qpm_engine_read_population", "qpm_engine_profile", "qpm_engine_launches_per_generation",
-    "qpm_engine_fitness_ptr",
+    "qpm_engine_fitness_ptr", "qpm_nccl_unique_id", "qpm_engine_set_comm", "qpm_engine_set_shard",
+    "qpm_engine_phases", "qpm_engine_run_phase", "qpm_engine_exchange_from", "qpm_engine_cand_ptr",
+    "qpm_engine_stream",
 )
 
 
@@ -106,6 +108,14 @@ def lib():
         "qpm_engine_profile": (I32, [P, I64, P, P, P, I32]),
         "qpm_engine_launches_per_generation": (I32, [P]),
         "qpm_engine_fitness_ptr": (I32, [P, P]),
+        "qpm_nccl_unique_id": (I32, [P]),
+        "qpm_engine_set_comm": (I32, [P, I32, I32, P]),
+        "qpm_engine_set_shard": (I32, [P, I32, I32]),
+        "qpm_engine_phases": (I32, [P]),
+        "qpm_engine_run_phase": (I32, [P, I32]),
+        "qpm_engine_exchange_from": (I32, [P, P, I32]),
+        "qpm_engine_cand_ptr": (I32, [P, P]),
+        "qpm_engine_stream": (I32, [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -34,6 +34,8 @@
 //   - DE arithmetic x_r1 + F (x_r2 - x_r3) is unfused (-fmad=false);
 //   - u < p comparisons are exact integer compares on the 53-bit mantissa;
 //   - np.mean / np.std use a replica of numpy's pairwise summation.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -51,6 +53,11 @@ constexpr int kGenesPerThread = 4;  // genes per thread (strided by kRowThreads)
 constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
 constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
 constexpr int64_t kStatsSmemMaxNP = 12288;  // 2 x NP doubles of dynamic smem (<= 192 KB)
+
+// ncclUniqueId layout (NCCL_UNIQUE_ID_BYTES = 128, nccl.h)
+struct ncclUniqueIdPod {
+    char internal[128];
+};
 
 struct EngineState {
     int64_t g;       // generation computed next (0 before init)
@@ -264,6 +271,7 @@ __device__ __forceinline__ uint32_t wolf_lane_bits(const RunConsts &c, const Gen
 struct PlanArgs {
     EngineState *st;
     const GenThr *gthr;
+    int64_t row_lo, n_rows;  // rows whose mask / planes this rank draws
     uint64_t *keys;    // [2][NP]
     int4 *picks;       // [2][NP]  r1, r2, r3, m
     int32_t *jrand;    // [2][NP]
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(kRowThreads) k_plan_draws(RunConsts c, PlanArg
     const int64_t g = a.st->g_plan;
     if (g > c.G) return;
     const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
-    const int64_t i = blockIdx.x / nchunk;
+    const int64_t i = a.row_lo + blockIdx.x / nchunk;
     const int jc = (int)(blockIdx.x % nchunk) * kGenesPerBlock;
     const GenThr t = a.gthr[g];
     const bool full = jc + kGenesPerBlock <= (int)c.D;
@@ -456,15 +464,18 @@ struct TrialArgs {
     int64_t own_lo, own_hi;
     const double *cand, *fit;
     const int4 *picks;       // [2][NP]
-    const uint32_t *mask;    // [2][NP][W]
-    const uint32_t *planes;  // [2][NP][W][8]
+    const uint64_t *keys;    // [2][NP]
+    const int32_t *jrand;    // [2][NP]
+    const uint32_t *mask;    // [2][NP][W]   (own rows)
+    const uint32_t *planes;  // [2][NP][W][8] (own rows)
     const int32_t *slot_of, *spare_of;
     uint8_t *slot_bin;
     double *genome;
     uint32_t *bits;
+    uint32_t *cbits;  // [NP][W] wolf candidates staged for the all-gather (multi-GPU), else null
 };
 
-template <bool BIN, bool FULL>
+template <bool BIN, bool FULL, bool DRAW>
 __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
                                                double F) {
     // Each lane owns an adjacent gene pair (16-byte loads and stores); a warp
@@ -489,7 +500,24 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     for (int st = 0; st < kSteps; ++st) {
         const int j64 = jc + (st * (kRowThreads / 32) + warp) * 64;
         mb[st] = 0u;
-        if (FULL || j64 < (int)c.Dp) mb[st] = (mrow[(j64 >> 5) + (lane >> 4)] >> ((2 * lane) & 31)) & 3u;
+        if (!FULL && j64 >= (int)c.Dp) continue;
+        if (DRAW) {
+            // a foreign row the planner did not draw: crossover mask inline
+            const uint64_t key = a.keys[b * c.NP + i];
+            const int jr = a.jrand[b * c.NP + i];
+            const uint32_t p_mask = (uint32_t)pk.w + 2;
+            const int j = j64 + 2 * lane;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int jj = j + q;
+                if (jj < D) {
+                    const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
+                    if (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == jr) mb[st] |= 1u << q;
+                }
+            }
+        } else {
+            mb[st] = (mrow[(j64 >> 5) + (lane >> 4)] >> ((2 * lane) & 31)) & 3u;
+        }
     }
     double2 y[kSteps], p1[kSteps], p2[kSteps], p3[kSteps];
 #pragma unroll
@@ -558,16 +586,39 @@ __global__ void __launch_bounds__(kRowThreads) k_de_trial(RunConsts c, TrialArgs
     const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
                      a.slot_bin[a.slot_of[pk.z]];
     const bool full = jc + kGenesPerBlock <= (int)c.D;
-    if (bin) {
-        if (full)
-            de_trial_chunk<true, true>(c, a, b, i, jc, F);
+    if (a.filter) {  // foreign rows: masks drawn inline
+        if (bin)
+            de_trial_chunk<true, false, true>(c, a, b, i, jc, F);
         else
-            de_trial_chunk<true, false>(c, a, b, i, jc, F);
+            de_trial_chunk<false, false, true>(c, a, b, i, jc, F);
+    } else if (bin) {
+        if (full)
+            de_trial_chunk<true, true, false>(c, a, b, i, jc, F);
+        else
+            de_trial_chunk<true, false, false>(c, a, b, i, jc, F);
     } else {
         if (full)
-            de_trial_chunk<false, true>(c, a, b, i, jc, F);
+            de_trial_chunk<false, true, false>(c, a, b, i, jc, F);
         else
-            de_trial_chunk<false, false>(c, a, b, i, jc, F);
+            de_trial_chunk<false, false, false>(c, a, b, i, jc, F);
+    }
+}
+
+// multi-GPU: all-gathered wolf candidates of accepted (non-leader) rows into
+// their spare slots, ahead of the selection
+__global__ void k_commit_cand_bits(RunConsts c, TrialArgs a) {
+    const int64_t total = c.NP * c.W;
+    int32_t lead[kMaxLeaders];
+#pragma unroll
+    for (int t = 0; t < kMaxLeaders; ++t) lead[t] = t < c.k ? a.st->leaders[t] : -1;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx / c.W;
+        bool skip = !(a.cand[i] > a.fit[i]);
+#pragma unroll
+        for (int t = 0; t < kMaxLeaders; ++t) skip |= lead[t] == i;
+        if (skip) continue;
+        a.bits[(int64_t)a.spare_of[i] * c.W + idx % c.W] = a.cbits[idx];
     }
 }
 
@@ -605,7 +656,9 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_apply(RunConsts c, TrialArg
         const uint32_t pl[kPlanes] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         const int rem = (int)c.D - w * 32;
         const uint32_t valid = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        a.bits[(int64_t)a.spare_of[i] * c.W + w] = wolf_word<K>(ld, pl, early) & valid;
+        const uint32_t word = wolf_word<K>(ld, pl, early) & valid;
+        a.bits[(int64_t)a.spare_of[i] * c.W + w] = word;  // scored from the spare slot
+        if (a.cbits) a.cbits[i * c.W + w] = word;          // staged for the all-gather
     }
 }
 
@@ -1011,8 +1064,12 @@ struct Engine {
     uint32_t *bits = nullptr;
     uint8_t *slot_bin = nullptr;
     uint32_t *planes = nullptr, *mask = nullptr;  // [2][...] by generation parity
+    uint32_t *cbits = nullptr;                    // [NP][W] wolf candidates staged for exchange
     GenThr *gthr = nullptr;
     cudaStream_t side = nullptr;  // low-priority planner stream
+    int rank = 0, world = 1;       // row shard of this engine (multi-GPU)
+    int64_t own_lo = 0, own_hi = 0;
+    void *comm = nullptr;          // ncclComm_t
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int32_t *slot_of = nullptr, *spare_of = nullptr, *jrand = nullptr;
     double *fit = nullptr, *cand = nullptr, *scratch = nullptr;
@@ -1145,8 +1202,11 @@ static TrialArgs trial_args(const Engine *e, int64_t row_lo, int64_t n_rows) {
     a.cand = e->cand;
     a.fit = e->fit;
     a.picks = e->picks;
+    a.keys = e->keys;
+    a.jrand = e->jrand;
     a.mask = e->mask;
     a.planes = e->planes;
+    a.cbits = e->world > 1 ? e->cbits : nullptr;
     a.slot_of = e->slot_of;
     a.spare_of = e->spare_of;
     a.slot_bin = e->slot_bin;
@@ -1159,6 +1219,8 @@ static PlanArgs plan_args(const Engine *e) {
     PlanArgs a;
     a.st = e->st;
     a.gthr = e->gthr;
+    a.row_lo = e->own_lo;
+    a.n_rows = e->own_hi - e->own_lo;
     a.keys = e->keys;
     a.picks = e->picks;
     a.jrand = e->jrand;
@@ -1172,7 +1234,7 @@ static int enqueue_planner(Engine *e, cudaStream_t s) {
     const RunConsts &c = e->c;
     const PlanArgs pa = plan_args(e);
     k_plan_rows<<<(unsigned)((c.NP + 127) / 128), 128, 0, s>>>(c, pa);
-    const unsigned items = (unsigned)(c.NP * ((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock));
+    const unsigned items = (unsigned)(pa.n_rows * ((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock));
     if (c.algorithm == QPM_ALGO_HYBRID && c.k == 4)
         k_plan_draws<4><<<items, kRowThreads, 0, s>>>(c, pa);
     else if (c.algorithm == QPM_ALGO_HYBRID)
@@ -1184,72 +1246,171 @@ static int enqueue_planner(Engine *e, cudaStream_t s) {
     return QPM_OK;
 }
 
-// one generation's launch sequence
-static int enqueue_generation(Engine *e, int *launches, StageMarks *pm = nullptr) {
+// ---------------------------------------------------------------- NCCL
+// Loaded at run time from the process's libnccl.so.2 (the one torch already
+// mapped), so the library has no link-time NCCL dependency.
+typedef int (*nccl_get_id_fn)(void *);
+typedef int (*nccl_init_rank_fn)(void **, int, ncclUniqueIdPod, int);
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef int (*nccl_destroy_fn)(void *);
+typedef const char *(*nccl_err_fn)(int);
+struct NcclApi {
+    bool loaded = false;
+    nccl_get_id_fn get_id = nullptr;
+    nccl_init_rank_fn init_rank = nullptr;
+    nccl_allgather_fn allgather = nullptr;
+    nccl_destroy_fn destroy = nullptr;
+    nccl_err_fn err = nullptr;
+};
+static NcclApi g_nccl;
+constexpr int kNcclFloat64 = 8;  // ncclFloat64 in nccl.h
+constexpr int kNcclUint8 = 1;    // ncclUint8
+
+static int nccl_load() {
+    if (g_nccl.loaded) return QPM_OK;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        set_error("dlopen(libnccl.so.2) failed: %s", dlerror());
+        return QPM_ERR_NCCL;
+    }
+    g_nccl.get_id = (nccl_get_id_fn)dlsym(h, "ncclGetUniqueId");
+    g_nccl.init_rank = (nccl_init_rank_fn)dlsym(h, "ncclCommInitRank");
+    g_nccl.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
+    g_nccl.destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
+    g_nccl.err = (nccl_err_fn)dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.get_id || !g_nccl.init_rank || !g_nccl.allgather || !g_nccl.destroy || !g_nccl.err) {
+        set_error("libnccl.so.2 lacks a required symbol");
+        return QPM_ERR_NCCL;
+    }
+    g_nccl.loaded = true;
+    return QPM_OK;
+}
+
+// exchange before phase `phase`: every rank's own slice of the candidate
+// fitness (and, before the wolf selection, of the staged wolf candidates)
+static int enqueue_exchange(Engine *e, int phase) {
+    if (!e->comm) return QPM_OK;  // one rank (a 1-rank communicator still runs the collective)
+    const int64_t n_own = e->own_hi - e->own_lo;
+    int r = g_nccl.allgather(e->cand + e->own_lo, e->cand, (size_t)n_own, kNcclFloat64, e->comm, e->stream);
+    if (r == 0 && phase == 2)
+        r = g_nccl.allgather(e->cbits + e->own_lo * e->c.W, e->cbits, (size_t)(n_own * e->c.W * 4), kNcclUint8,
+                             e->comm, e->stream);
+    if (r != 0) {
+        set_error("ncclAllGather: %s", g_nccl.err(r));
+        return QPM_ERR_NCCL;
+    }
+    return QPM_OK;
+}
+
+static int phase_count(const Engine *e) { return e->c.algorithm == QPM_ALGO_HYBRID ? 3 : 2; }
+
+// One generation = phases separated by candidate-fitness exchanges:
+//   hybrid  P0 trial(own) fit(own) | X | P1 trial(foreign accepted) select+top-k
+//           wolf(own) fit(own) | X | P2 wolf(foreign accepted) select+stats
+//   de      P0 trial(own) fit(own) | X | P1 trial(foreign accepted) select+stats
+//   gwo     P0 top-k, wolf move (all rows) fit(own) | X | P1 replace+stats
+// With one rank own = all rows and the foreign kernels are skipped.
+static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
-    int n = 0;
     int rc;
     auto mark = [&](const char *next) {
         if (pm) pm->mark(s, next);
     };
-    const int64_t NP = c.NP;
+    const int64_t NP = c.NP, lo = e->own_lo, n_own = e->own_hi - e->own_lo;
+    const bool sharded = e->world > 1;
+    const int64_t nchunk = (c.Dp + kGenesPerBlock - 1) / kGenesPerBlock;
     if (c.algorithm == QPM_ALGO_GWO) {
-        mark("topk");
-        k_topk_leaders<<<1, kCtaThreads, 0, s>>>(c, e->st, e->fit, 3);  // rank_leaders(pop, 3)
-        mark("gwo_continuous");
-        k_gwo_continuous<<<row_grid(e, NP), kRowThreads, 0, s>>>(c, e->st, e->sched, 0, e->slot_of, e->spare_of,
-                                                                 e->slot_bin, e->genome, e->bits);
-        QPM_LAUNCH_CHECK();
-        n += 2;
-        mark("fitness");
-        rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, NP, e->cand, e->P.fitness_mode, s, &n);
-        if (rc) return rc;
-        mark("replace_stats");
-        if ((rc = launch_select_stats(e, 2, s))) return rc;
-        k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,
-                                       e->best_bits);
-        QPM_LAUNCH_CHECK();
-        n += 2;
-    } else {
-        const bool hybrid = c.algorithm == QPM_ALGO_HYBRID;
-        const TrialArgs ta = trial_args(e, 0, NP);
+        if (phase == 0) {
+            mark("topk");
+            k_topk_leaders<<<1, kCtaThreads, 0, s>>>(c, e->st, e->fit, 3);  // rank_leaders(pop, 3)
+            mark("gwo_continuous");
+            k_gwo_continuous<<<row_grid(e, NP), kRowThreads, 0, s>>>(c, e->st, e->sched, 0, e->slot_of, e->spare_of,
+                                                                     e->slot_bin, e->genome, e->bits);
+            QPM_LAUNCH_CHECK();
+            *n += 2;
+            mark("fitness");
+            rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+            if (rc) return rc;
+        } else {
+            mark("replace_stats");
+            if ((rc = launch_select_stats(e, 2, s))) return rc;
+            k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,
+                                           e->best_bits);
+            QPM_LAUNCH_CHECK();
+            *n += 2;
+        }
+        return QPM_OK;
+    }
+    const bool hybrid = c.algorithm == QPM_ALGO_HYBRID;
+    TrialArgs own = trial_args(e, lo, n_own);
+    TrialArgs foreign = trial_args(e, 0, NP);
+    foreign.filter = 1;
+    foreign.own_lo = e->own_lo;
+    foreign.own_hi = e->own_hi;
+    if (phase == 0) {
         // fork: the planner draws generation g+1 on the side stream
         QPM_CUDA_TRY(cudaEventRecord(e->ev_fork, s));
         QPM_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
         if ((rc = enqueue_planner(e, e->side))) return rc;
         QPM_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
-        n += 3;
+        *n += 3;
         mark("de_trial");
-        k_de_trial<<<(unsigned)(NP * ((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock)), kRowThreads, 0, s>>>(c, ta);
+        k_de_trial<<<(unsigned)(n_own * nchunk), kRowThreads, 0, s>>>(c, own);
         QPM_LAUNCH_CHECK();
-        n += 1;
+        *n += 1;
         mark("fitness_de");
-        rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, NP, e->cand, e->P.fitness_mode, s, &n);
-        if (rc) return rc;
-        if (hybrid) {
-            mark("select_topk");
-            k_select_topk<<<1, kCtaThreads, 0, s>>>(c, e->st, e->cand, e->fit, e->slot_of, e->spare_of);
-            mark("gwo_apply");
-            if (c.k == 4)
-                k_gwo_apply<4><<<e->apply_grid, kRowThreads, 0, s>>>(c, ta);
-            else
-                k_gwo_apply<3><<<e->apply_grid, kRowThreads, 0, s>>>(c, ta);
+        return launch_fitness(e->prob, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+    }
+    if (phase == 1) {
+        if (sharded) {
+            mark("de_trial_foreign");
+            k_de_trial<<<(unsigned)(NP * nchunk), kRowThreads, 0, s>>>(c, foreign);
             QPM_LAUNCH_CHECK();
-            n += 2;
-            mark("fitness_gwo");
-            rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of, NP, e->cand, e->P.fitness_mode, s, &n);
-            if (rc) return rc;
-            mark("select_stats");
-            if ((rc = launch_select_stats(e, 1, s))) return rc;
-        } else {
+            *n += 1;
+        }
+        if (!hybrid) {
             mark("select_stats");
             if ((rc = launch_select_stats(e, 0, s))) return rc;
+            *n += 1;
+            QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
+            return QPM_OK;
         }
-        n += 1;
-        QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
+        mark("select_topk");
+        k_select_topk<<<1, kCtaThreads, 0, s>>>(c, e->st, e->cand, e->fit, e->slot_of, e->spare_of);
+        mark("gwo_apply");
+        if (c.k == 4)
+            k_gwo_apply<4><<<e->apply_grid, kRowThreads, 0, s>>>(c, own);
+        else
+            k_gwo_apply<3><<<e->apply_grid, kRowThreads, 0, s>>>(c, own);
+        QPM_LAUNCH_CHECK();
+        *n += 2;
+        mark("fitness_gwo");
+        return launch_fitness(e->prob, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
     }
-    mark(nullptr);
+    // phase 2 (hybrid)
+    if (sharded) {
+        mark("commit_wolves");
+        k_commit_cand_bits<<<e->apply_grid, kRowThreads, 0, s>>>(c, foreign);
+        QPM_LAUNCH_CHECK();
+        *n += 1;
+    }
+    mark("select_stats");
+    if ((rc = launch_select_stats(e, 1, s))) return rc;
+    *n += 1;
+    QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
+    return QPM_OK;
+}
+
+// one generation's launch sequence
+static int enqueue_generation(Engine *e, int *launches, StageMarks *pm = nullptr) {
+    int n = 0, rc;
+    const int np = phase_count(e);
+    for (int ph = 0; ph < np; ++ph) {
+        if (ph > 0 && (rc = enqueue_exchange(e, ph))) return rc;
+        if ((rc = enqueue_phase(e, ph, &n, pm))) return rc;
+    }
+    if (pm) pm->mark(e->stream, nullptr);
     if (launches) *launches = n;
     return QPM_OK;
 }
@@ -1263,6 +1424,7 @@ static void engine_free(Engine *e) {
         cudaStreamSynchronize(e->side);
         cudaStreamDestroy(e->side);
     }
+    if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->exec) cudaGraphExecDestroy(e->exec);
@@ -1291,11 +1453,13 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ARG_CHECK(P->algorithm == QPM_ALGO_GWO || P->leader_count == 3 || P->leader_count == 4,
                   "leader_count must be 3 or 4");
     QPM_ARG_CHECK(P->conv_window >= 1 && P->conv_window <= kMaxWindow, "conv_window in [1, 256]");
-    QPM_ARG_CHECK(P->row_lo == 0 && P->row_hi == P->NP, "sharded rows need the multi-GPU engine");
+    QPM_ARG_CHECK(P->row_lo >= 0 && P->row_lo < P->row_hi && P->row_hi <= P->NP, "row shard [row_lo, row_hi)");
     QPM_ARG_CHECK(P->NP < (1LL << 30), "NP < 2^30");
     Engine *e = new Engine();
     e->prob = &prob->p;
     e->P = *P;
+    e->own_lo = P->row_lo;
+    e->own_hi = P->row_hi;
     e->stream = (cudaStream_t)stream;
     if (!e->stream) {
         // graphs cannot be captured on the legacy default stream: own a stream
@@ -1389,6 +1553,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->slot_bin, (size_t)2 * NP);
     QPM_ALLOC(e->planes, P->algorithm == QPM_ALGO_HYBRID ? (size_t)2 * NP * c.W * kPlanes : 16);
     QPM_ALLOC(e->mask, P->algorithm != QPM_ALGO_GWO ? (size_t)2 * NP * c.W : 16);
+    QPM_ALLOC(e->cbits, P->algorithm == QPM_ALGO_HYBRID ? (size_t)NP * c.W : 16);
     QPM_ALLOC(e->gthr, (size_t)(P->G + 1));
     QPM_ALLOC(e->slot_of, NP);
     QPM_ALLOC(e->spare_of, NP);
@@ -1504,6 +1669,10 @@ int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
         return QPM_ERR_STATE;
     }
     QPM_ARG_CHECK(n >= 0 && e->g_done + n <= e->c.G, "generation count exceeds G");
+    if (e->world > 1 && !e->comm) {
+        set_error("sharded engine without a communicator: drive it with qpm_engine_run_phase");
+        return QPM_ERR_STATE;
+    }
     if (n == 0) return QPM_OK;
     if (use_graph) {
         if (!e->exec) {
@@ -1664,6 +1833,100 @@ int qpm_engine_profile(qpm_engine *h, int64_t n, double *stage_ms, int *n_stages
             names[k * name_len + name_len - 1] = 0;
         }
     }
+    return QPM_OK;
+}
+
+int qpm_nccl_unique_id(uint8_t *id_out) {
+    QPM_ARG_CHECK(id_out, "id_out");
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclUniqueIdPod id;
+    const int r = g_nccl.get_id(&id);
+    if (r != 0) {
+        set_error("ncclGetUniqueId: %s", g_nccl.err(r));
+        return QPM_ERR_NCCL;
+    }
+    memcpy(id_out, id.internal, sizeof(id.internal));
+    return QPM_OK;
+}
+
+static int check_shard(Engine *e, int rank, int world) {
+    QPM_ARG_CHECK(world >= 1 && rank >= 0 && rank < world, "rank in [0, world)");
+    QPM_ARG_CHECK(e->c.NP % world == 0, "NP must be a multiple of the rank count (equal all-gather slices)");
+    const int64_t per = e->c.NP / world;
+    QPM_ARG_CHECK(e->own_lo == rank * per && e->own_hi == (rank + 1) * per,
+                  "row_lo/row_hi must be this rank's equal slice [rank NP/world, (rank+1) NP/world)");
+    QPM_ARG_CHECK(!e->exec, "the shard must be set before the first graph step");
+    e->rank = rank;
+    e->world = world;
+    return QPM_OK;
+}
+
+int qpm_engine_set_comm(qpm_engine *h, int rank, int world, const uint8_t *id) {
+    QPM_ARG_CHECK(h && id, "engine, id");
+    Engine *e = h->e;
+    int rc = check_shard(e, rank, world);
+    if (rc) return rc;
+    if ((rc = nccl_load())) return rc;
+    ncclUniqueIdPod uid;
+    memcpy(uid.internal, id, sizeof(uid.internal));
+    const int r = g_nccl.init_rank(&e->comm, world, uid, rank);
+    if (r != 0) {
+        e->comm = nullptr;
+        set_error("ncclCommInitRank: %s", g_nccl.err(r));
+        return QPM_ERR_NCCL;
+    }
+    return QPM_OK;
+}
+
+int qpm_engine_set_shard(qpm_engine *h, int rank, int world) {
+    QPM_ARG_CHECK(h, "engine");
+    return check_shard(h->e, rank, world);
+}
+
+int qpm_engine_phases(const qpm_engine *h) { return h ? phase_count(h->e) : -1; }
+
+int qpm_engine_run_phase(qpm_engine *h, int phase) {
+    QPM_ARG_CHECK(h, "engine");
+    Engine *e = h->e;
+    if (!e->initialized) {
+        set_error("qpm_engine_run_phase before qpm_engine_init");
+        return QPM_ERR_STATE;
+    }
+    const int np = phase_count(e);
+    QPM_ARG_CHECK(phase >= 0 && phase < np, "phase index");
+    QPM_ARG_CHECK(e->g_done < e->c.G, "generation count exceeds G");
+    int n = 0;
+    int rc = enqueue_phase(e, phase, &n, nullptr);
+    if (rc) return rc;
+    if (phase == np - 1) e->g_done += 1;
+    return QPM_OK;
+}
+
+int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase) {
+    QPM_ARG_CHECK(dst && src, "engines");
+    Engine *d = dst->e, *s = src->e;
+    QPM_ARG_CHECK(d->c.NP == s->c.NP && d->c.W == s->c.W, "engines of one sharded run");
+    const int64_t n_own = s->own_hi - s->own_lo;
+    QPM_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    QPM_CUDA_TRY(cudaMemcpyAsync(d->cand + s->own_lo, s->cand + s->own_lo, sizeof(double) * n_own,
+                                 cudaMemcpyDeviceToDevice, d->stream));
+    if (phase == 2 && d->c.algorithm == QPM_ALGO_HYBRID)
+        QPM_CUDA_TRY(cudaMemcpyAsync(d->cbits + s->own_lo * s->c.W, s->cbits + s->own_lo * s->c.W,
+                                     sizeof(uint32_t) * n_own * s->c.W, cudaMemcpyDeviceToDevice, d->stream));
+    QPM_CUDA_TRY(cudaStreamSynchronize(d->stream));
+    return QPM_OK;
+}
+
+int qpm_engine_cand_ptr(qpm_engine *h, double **cand_dev) {
+    QPM_ARG_CHECK(h && cand_dev, "engine, out");
+    *cand_dev = h->e->cand;
+    return QPM_OK;
+}
+
+int qpm_engine_stream(qpm_engine *h, void **stream) {
+    QPM_ARG_CHECK(h && stream, "engine, out");
+    *stream = (void *)h->e->stream;
     return QPM_OK;
 }
 

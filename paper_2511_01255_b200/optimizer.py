@@ -216,7 +216,7 @@ class Engine:
 
     def __init__(self, objective: GpuPatternObjective, algorithm: str, *, pop_size: int, generations: int,
                  seed: int, de: DEParams, gwo: GWOParams, sch: Schedules, fitness_mode: str | None = None,
-                 bounds: tuple[float, float] = (-1.0, 1.0), stream=None):
+                 bounds: tuple[float, float] = (-1.0, 1.0), stream=None, row_range: tuple[int, int] | None = None):
         import torch
 
         if not isinstance(objective, GpuPatternObjective):
@@ -251,7 +251,7 @@ class Engine:
         p.conv_window = max(1, int(sch.conv_window))
         p.adaptive_branches = int(bool(sch.adaptive_branches))
         p.gwo_lo, p.gwo_hi, p.gwo_a0 = float(bounds[0]), float(bounds[1]), gwo.a
-        p.row_lo, p.row_hi = 0, self.NP
+        p.row_lo, p.row_hi = row_range if row_range is not None else (0, self.NP)
         self.params = p
         self.sched = np.ascontiguousarray(schedule_table(self.G, de, gwo, sch))
         h = ctypes.c_void_p()
