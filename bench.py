@@ -41,7 +41,12 @@ UNIT = "domain-evals/s"
 NP, D, G_RUN, SEED = 1024, 10_000, 1000, 0
 THICKNESS_UM, PUMP_NM = 1.0, 1404.0
 FLOP_PER_EVAL = 10  # complex add + complex mul + complex add per domain
-DE_BYTES_PER_GENE = 40  # x_i, x_r1, x_r2, x_r3 read + trial written, f64
+CR = 0.9
+# DE trial bytes per gene that the algorithm must move: the three donor genes
+# when the crossover takes the mutant (probability CR), the target gene
+# otherwise, the trial gene written, plus its sign bit (SURVEY 8(d) counts the
+# unconditional 40 B upper bound)
+DE_BYTES_PER_GENE = CR * 24 + (1 - CR) * 8 + 8 + 0.125
 
 
 def env_rank():
@@ -208,7 +213,7 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
         peak = peaks.get("hbm_gbs", 6650.0)
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
-                "algorithmic_unit": f"{DE_BYTES_PER_GENE} B per gene x NP*D"}
+                "algorithmic_unit": f"{DE_BYTES_PER_GENE:.3f} B per gene (CR={CR}) x NP*D"}
     else:
         nbytes = NP * D * 8
         achieved = nbytes / (ms * 1e-3) / 1e9
