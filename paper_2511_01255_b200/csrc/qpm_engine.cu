@@ -52,6 +52,7 @@ constexpr int kRowThreads = 256;    // threads per row-block in the elementwise 
 constexpr int kGenesPerThread = 4;  // genes per thread (strided by kRowThreads)
 constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
 constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
+constexpr int kDeChunk = 4096;      // genes per DE-trial CTA (amortizes the per-row setup)
 constexpr int64_t kStatsSmemMaxNP = 12288;  // 2 x NP doubles of dynamic smem (<= 192 KB)
 
 // ncclUniqueId layout (NCCL_UNIQUE_ID_BYTES = 128, nccl.h)
@@ -478,8 +479,9 @@ struct TrialArgs {
 template <bool BIN, bool FULL, bool DRAW>
 __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
                                                double F) {
-    // Each lane owns an adjacent gene pair (16-byte loads and stores); a warp
-    // covers 64 genes = 2 mask words and 2 sign words per step.
+    // A warp covers 64 genes per step: lane l owns genes l and l+32, so every
+    // load/store is one coalesced 256-byte warp access and the two sign words
+    // are plain ballots.
     const int4 pk = a.picks[b * c.NP + i];
     const RowRef xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
     const RowRef x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
@@ -492,100 +494,97 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const int D = (int)c.D;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    constexpr int kSteps = kGenesPerBlock / (kRowThreads * 2);  // 2 pair-steps per 1024-gene chunk
-    // all mask words, then all genome loads of the chunk, then the math:
-    // the kernel is bound by memory latency, so keep every load in flight
-    uint32_t mb[kSteps];
+    constexpr int kSteps = 2;  // 64-gene warp steps per batch (registers)
+    constexpr int kSpan = kRowThreads * 2;  // genes per CTA step
+    constexpr int kBatches = kDeChunk / (kSpan * kSteps);
+#pragma unroll 1
+    for (int bt = 0; bt < kBatches; ++bt) {
+        const int jb = jc + bt * kSpan * kSteps + warp * 64;
+        // all mask bits, then all genome loads of the batch, then the math:
+        // the kernel is bound by memory latency, so keep every load in flight
+        uint32_t mb[kSteps];
 #pragma unroll
-    for (int st = 0; st < kSteps; ++st) {
-        const int j64 = jc + (st * (kRowThreads / 32) + warp) * 64;
-        mb[st] = 0u;
-        if (!FULL && j64 >= (int)c.Dp) continue;
-        if (DRAW) {
-            // a foreign row the planner did not draw: crossover mask inline
-            const uint64_t key = a.keys[b * c.NP + i];
-            const int jr = a.jrand[b * c.NP + i];
-            const uint32_t p_mask = (uint32_t)pk.w + 2;
-            const int j = j64 + 2 * lane;
+        for (int st = 0; st < kSteps; ++st) {
+            const int j64 = jb + st * kSpan;
+            mb[st] = 0u;
+            if (!FULL && j64 >= (int)c.Dp) continue;
+            if (DRAW) {
+                // a foreign row the planner did not draw: crossover mask inline
+                const uint64_t key = a.keys[b * c.NP + i];
+                const int jr = a.jrand[b * c.NP + i];
+                const uint32_t p_mask = (uint32_t)pk.w + 2;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int jj = j64 + lane + 32 * q;
+                    if (jj < D) {
+                        const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
+                        if (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == jr) mb[st] |= 1u << q;
+                    }
+                }
+            } else {
+                const uint2 w = *reinterpret_cast<const uint2 *>(mrow + (j64 >> 5));
+                mb[st] = ((w.x >> lane) & 1u) | (((w.y >> lane) & 1u) << 1);
+            }
+        }
+        double y[kSteps][2], p1[kSteps][2], p2[kSteps][2], p3[kSteps][2];
+#pragma unroll
+        for (int st = 0; st < kSteps; ++st) {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                const int jj = j + q;
-                if (jj < D) {
-                    const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
-                    if (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == jr) mb[st] |= 1u << q;
+                const int j = jb + st * kSpan + lane + 32 * q;
+                y[st][q] = p1[st][q] = p2[st][q] = p3[st][q] = 0.0;
+                if (!FULL && j >= D) continue;
+                if (BIN) {
+                    y[st][q] = xi.at(j);
+                    p1[st][q] = x1.at(j);
+                    p2[st][q] = x2.at(j);
+                    p3[st][q] = x3.at(j);
+                } else if ((mb[st] >> q) & 1u) {
+                    p1[st][q] = x1.f[j];
+                    p2[st][q] = x2.f[j];
+                    p3[st][q] = x3.f[j];
+                } else {
+                    y[st][q] = xi.f[j];
                 }
             }
-        } else {
-            mb[st] = (mrow[(j64 >> 5) + (lane >> 4)] >> ((2 * lane) & 31)) & 3u;
         }
-    }
-    double2 y[kSteps], p1[kSteps], p2[kSteps], p3[kSteps];
 #pragma unroll
-    for (int st = 0; st < kSteps; ++st) {
-        const int j = jc + (st * (kRowThreads / 32) + warp) * 64 + 2 * lane;
-        y[st] = p1[st] = p2[st] = p3[st] = make_double2(0.0, 0.0);
-        if (!FULL && j >= D) continue;
-        if (BIN) {
-            y[st] = make_double2(xi.at(j), xi.at(j + 1));
-            p1[st] = make_double2(x1.at(j), x1.at(j + 1));
-            p2[st] = make_double2(x2.at(j), x2.at(j + 1));
-            p3[st] = make_double2(x3.at(j), x3.at(j + 1));
-        } else {
-            if (mb[st] != 3u) y[st] = *reinterpret_cast<const double2 *>(xi.f + j);
-            if (mb[st] != 0u) {
-                p1[st] = *reinterpret_cast<const double2 *>(x1.f + j);
-                p2[st] = *reinterpret_cast<const double2 *>(x2.f + j);
-                p3[st] = *reinterpret_cast<const double2 *>(x3.f + j);
+        for (int st = 0; st < kSteps; ++st) {
+            const int j64 = jb + st * kSpan;  // this warp's 64-gene span
+            if (!FULL && j64 >= (int)c.Dp) break;
+            bool neg[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int j = j64 + lane + 32 * q;
+                neg[q] = false;
+                if (FULL || j < D) {
+                    const double v = ((mb[st] >> q) & 1u) ? p1[st][q] + F * (p2[st][q] - p3[st][q]) : y[st][q];
+                    out[j] = v;
+                    neg[q] = !(v >= 0.0);
+                } else if (j < (int)c.Dp) {
+                    out[j] = 0.0;
+                }
             }
-        }
-    }
-#pragma unroll
-    for (int st = 0; st < kSteps; ++st) {
-        const int j64 = jc + (st * (kRowThreads / 32) + warp) * 64;  // this warp's 64-gene span
-        if (!FULL && j64 >= (int)c.Dp) break;
-        const int j = j64 + 2 * lane;
-        bool n0 = false, n1 = false;
-        if (FULL || j < D) {
-            const double v0 = (mb[st] & 1u) ? p1[st].x + F * (p2[st].x - p3[st].x) : y[st].x;
-            double v1 = (mb[st] & 2u) ? p1[st].y + F * (p2[st].y - p3[st].y) : y[st].y;
-            const bool in1 = FULL || j + 1 < D;
-            if (!in1) v1 = 0.0;
-            *reinterpret_cast<double2 *>(out + j) = make_double2(v0, v1);
-            n0 = !(v0 >= 0.0);
-            n1 = in1 && !(v1 >= 0.0);
-        }
-        // sign bits: lane l holds genes 2l, 2l+1 -> interleave two ballots
-        const uint32_t be = __ballot_sync(0xffffffffu, n0);
-        const uint32_t bo = __ballot_sync(0xffffffffu, n1);
-        if (lane < 2) {
-            uint32_t e = lane ? (be >> 16) : (be & 0xffffu);
-            uint32_t o = lane ? (bo >> 16) : (bo & 0xffffu);
-            e = (e | (e << 8)) & 0x00ff00ffu;
-            e = (e | (e << 4)) & 0x0f0f0f0fu;
-            e = (e | (e << 2)) & 0x33333333u;
-            e = (e | (e << 1)) & 0x55555555u;
-            o = (o | (o << 8)) & 0x00ff00ffu;
-            o = (o | (o << 4)) & 0x0f0f0f0fu;
-            o = (o | (o << 2)) & 0x33333333u;
-            o = (o | (o << 1)) & 0x55555555u;
-            bout[(j64 >> 5) + lane] = e | (o << 1);
+            const uint32_t w0 = __ballot_sync(0xffffffffu, neg[0]);
+            const uint32_t w1 = __ballot_sync(0xffffffffu, neg[1]);
+            if (lane < 2) bout[(j64 >> 5) + lane] = lane ? w1 : w0;
         }
     }
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[out_slot] = 0;
 }
 
-__global__ void __launch_bounds__(kRowThreads) k_de_trial(RunConsts c, TrialArgs a) {
+__global__ void __launch_bounds__(kRowThreads, 4) k_de_trial(RunConsts c, TrialArgs a) {
     const int64_t g = a.st->g;
     const int64_t b = g & 1;
     const double F = a.st->F;
-    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
+    const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
-    const int jc = (int)(blockIdx.x % nchunk) * kGenesPerBlock;
+    const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
     if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
     const int4 pk = a.picks[b * c.NP + i];
     const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
                      a.slot_bin[a.slot_of[pk.z]];
-    const bool full = jc + kGenesPerBlock <= (int)c.D;
+    const bool full = jc + kDeChunk <= (int)c.D;
     if (a.filter) {  // foreign rows: masks drawn inline
         if (bin)
             de_trial_chunk<true, false, true>(c, a, b, i, jc, F);
@@ -1057,6 +1056,7 @@ __global__ void k_reset_flag(EngineState *st) { st->best_flag = 0; }
 // ---------------------------------------------------------------- engine
 struct Engine {
     Problem *prob = nullptr;
+    FitScratch fs;  // this engine's fitness scratch (engines may share a problem)
     qpm_run_params P{};
     RunConsts c{};
     cudaStream_t stream = nullptr;
@@ -1319,7 +1319,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     };
     const int64_t NP = c.NP, lo = e->own_lo, n_own = e->own_hi - e->own_lo;
     const bool sharded = e->world > 1;
-    const int64_t nchunk = (c.Dp + kGenesPerBlock - 1) / kGenesPerBlock;
+    const int64_t de_chunks = (c.Dp + kDeChunk - 1) / kDeChunk;
     if (c.algorithm == QPM_ALGO_GWO) {
         if (phase == 0) {
             mark("topk");
@@ -1330,7 +1330,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             QPM_LAUNCH_CHECK();
             *n += 2;
             mark("fitness");
-            rc = launch_fitness(e->prob, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+            rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
             if (rc) return rc;
         } else {
             mark("replace_stats");
@@ -1356,16 +1356,16 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         QPM_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
         *n += 3;
         mark("de_trial");
-        k_de_trial<<<(unsigned)(n_own * nchunk), kRowThreads, 0, s>>>(c, own);
+        k_de_trial<<<(unsigned)(n_own * de_chunks), kRowThreads, 0, s>>>(c, own);
         QPM_LAUNCH_CHECK();
         *n += 1;
         mark("fitness_de");
-        return launch_fitness(e->prob, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
     }
     if (phase == 1) {
         if (sharded) {
             mark("de_trial_foreign");
-            k_de_trial<<<(unsigned)(NP * nchunk), kRowThreads, 0, s>>>(c, foreign);
+            k_de_trial<<<(unsigned)(NP * de_chunks), kRowThreads, 0, s>>>(c, foreign);
             QPM_LAUNCH_CHECK();
             *n += 1;
         }
@@ -1386,7 +1386,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         QPM_LAUNCH_CHECK();
         *n += 2;
         mark("fitness_gwo");
-        return launch_fitness(e->prob, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
     }
     // phase 2 (hybrid)
     if (sharded) {
@@ -1430,6 +1430,7 @@ static void engine_free(Engine *e) {
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
     for (void *p : e->allocs) cudaFree(p);
+    scratch_free(&e->fs);
     delete e;
 }
 
@@ -1571,10 +1572,11 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->best_genome, c.Dp);
     QPM_ALLOC(e->best_bits, c.W);
 #undef QPM_ALLOC
-    if ((rc = problem_reserve(e->prob, NP)) != 0) {
+    if ((rc = scratch_reserve(e->prob, &e->fs, NP)) != 0) {
         engine_free(e);
         return rc;
     }
+    e->device_bytes += e->fs.bytes;
     std::vector<int32_t> tree_host;
     tree_host.insert(tree_host.end(), ht.leaf_off.begin(), ht.leaf_off.end());
     tree_host.insert(tree_host.end(), ht.kid.begin(), ht.kid.end());
@@ -1649,7 +1651,7 @@ int qpm_engine_init(qpm_engine *h) {
     cudaStream_t s = e->stream;
     k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of);
     QPM_LAUNCH_CHECK();
-    int rc = launch_fitness(e->prob, e->bits, c.W, e->slot_of, c.NP, e->fit, e->P.fitness_mode, s, nullptr);
+    int rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->slot_of, c.NP, e->fit, e->P.fitness_mode, s, nullptr);
     if (rc) return rc;
     if ((rc = launch_select_stats(e, 3, s))) return rc;
     k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,

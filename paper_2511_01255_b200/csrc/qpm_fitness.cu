@@ -416,46 +416,57 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const double *__restrict_
 }
 
 // ------------------------------------------------------------ launchers
-int problem_reserve(Problem *p, int64_t rows) {
-    if (rows <= p->part_rows) return QPM_OK;
-    if (p->part) cudaFree(p->part);
-    if (p->gains) cudaFree(p->gains);
-    p->part = nullptr;
-    p->gains = nullptr;
-    int64_t S = std::max<int64_t>(p->S, 1);
-    size_t bytes = (size_t)p->n_wl * rows * S * kPartDoubles * sizeof(double);
-    QPM_CUDA_TRY(cudaMalloc(&p->part, bytes));
-    QPM_CUDA_TRY(cudaMalloc(&p->gains, (size_t)rows * p->n_wl * sizeof(double)));
-    p->part_rows = rows;
-    p->device_bytes += (int64_t)bytes + rows * p->n_wl * 8;
+int scratch_reserve(const Problem *p, FitScratch *fs, int64_t rows) {
+    if (rows <= fs->rows) return QPM_OK;
+    scratch_free(fs);
+    const int64_t S = std::max<int64_t>(p->S, 1);
+    const size_t bytes = (size_t)p->n_wl * rows * S * kPartDoubles * sizeof(double);
+    QPM_CUDA_TRY(cudaMalloc(&fs->part, bytes));
+    QPM_CUDA_TRY(cudaMalloc(&fs->gains, (size_t)rows * p->n_wl * sizeof(double)));
+    fs->rows = rows;
+    fs->bytes = (int64_t)bytes + rows * p->n_wl * 8;
     return QPM_OK;
 }
 
-int launch_fitness(Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index, int64_t rows,
-                   double *out, int mode, cudaStream_t stream, int *launches) {
+void scratch_free(FitScratch *fs) {
+    cudaFree(fs->part);
+    cudaFree(fs->gains);
+    *fs = FitScratch{};
+}
+
+static int problem_reserve(Problem *p, int64_t rows) {
+    if (!p->own) p->own = new FitScratch;
+    const int64_t before = p->own->bytes;
+    const int rc = scratch_reserve(p, p->own, rows);
+    p->device_bytes += p->own->bytes - before;
+    return rc;
+}
+
+int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
+                   const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches) {
     QPM_ARG_CHECK(row_words == p->W, "row_words must equal qpm_problem_row_words()");
     QPM_ARG_CHECK(rows >= 0, "rows >= 0");
     if (rows == 0) return QPM_OK;
-    QPM_ARG_CHECK(rows <= p->part_rows, "rows exceed the reserved fitness scratch");
+    QPM_ARG_CHECK(rows <= fs->rows, "rows exceed the reserved fitness scratch");
     const int thg = p->process == QPM_PROCESS_THG;
     int S;
     if (mode == QPM_MODE_EXACT) {
         S = 1;
         dim3 grid((unsigned)((rows + 127) / 128), (unsigned)p->n_wl);
-        k_fit_exact<<<grid, 128, 0, stream>>>(p->e1, p->b, p->D, thg, bits, p->W, row_index, rows, p->part);
+        k_fit_exact<<<grid, 128, 0, stream>>>(p->e1, p->b, p->D, thg, bits, p->W, row_index, rows, fs->part);
     } else {
         S = p->S;
         dim3 grid((unsigned)S, (unsigned)((rows + kFitThreads - 1) / kFitThreads), (unsigned)p->n_wl);
         if (thg)
             k_fit_fast<true><<<grid, kFitThreads, 0, stream>>>(p->qt, p->nquads, p->nchunks, p->seg_chunks, S,
-                                                               bits, p->W, row_index, rows, p->part);
+                                                               bits, p->W, row_index, rows, fs->part);
         else
             k_fit_fast<false><<<grid, kFitThreads, 0, stream>>>(p->qt, p->nquads, p->nchunks, p->seg_chunks, S,
-                                                                bits, p->W, row_index, rows, p->part);
+                                                                bits, p->W, row_index, rows, fs->part);
     }
     QPM_LAUNCH_CHECK();
     k_fit_finish<<<(unsigned)((rows + kFinishWarps - 1) / kFinishWarps), 32 * kFinishWarps, 0, stream>>>(
-        p->part, S, rows, p->n_wl, p->w, p->h, thg, p->scale, p->multi, p->g0, p->beta, p->gains, out);
+        fs->part, S, rows, p->n_wl, p->w, p->h, thg, p->scale, p->multi, p->g0, p->beta, fs->gains, out);
     QPM_LAUNCH_CHECK();
     if (launches) *launches += 2;
     return QPM_OK;
@@ -606,8 +617,10 @@ int qpm_problem_destroy(qpm_problem *h) {
     cudaFree(p.qt);
     cudaFree(p.w);
     cudaFree(p.h);
-    cudaFree(p.part);
-    cudaFree(p.gains);
+    if (p.own) {
+        scratch_free(p.own);
+        delete p.own;
+    }
     cudaFree(p.hp_signs);
     cudaFree(p.hp_bits);
     cudaFree(p.hp_out);
@@ -629,8 +642,8 @@ int qpm_fitness_bits(qpm_problem *h, const uint32_t *bits_dev, int64_t row_words
     QPM_ARG_CHECK(h, "problem");
     int rc = problem_reserve(&h->p, rows);
     if (rc) return rc;
-    return launch_fitness(&h->p, bits_dev, row_words, row_index_dev, rows, out_dev, mode, (cudaStream_t)stream,
-                          nullptr);
+    return launch_fitness(&h->p, h->p.own, bits_dev, row_words, row_index_dev, rows, out_dev, mode,
+                          (cudaStream_t)stream, nullptr);
 }
 
 int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, double *out, int mode) {
@@ -642,7 +655,7 @@ int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, d
     QPM_CUDA_TRY(cudaMemcpyAsync(p.hp_signs, signs, (size_t)rows * p.D, cudaMemcpyHostToDevice, p.hp_stream));
     rc = launch_pack(p.hp_signs, rows, p.D, p.hp_bits, p.W, p.hp_stream);
     if (rc) return rc;
-    rc = launch_fitness(&p, p.hp_bits, p.W, nullptr, rows, p.hp_out, mode, p.hp_stream, nullptr);
+    rc = launch_fitness(&p, p.own, p.hp_bits, p.W, nullptr, rows, p.hp_out, mode, p.hp_stream, nullptr);
     if (rc) return rc;
     QPM_CUDA_TRY(cudaMemcpyAsync(out, p.hp_out, (size_t)rows * sizeof(double), cudaMemcpyDeviceToHost, p.hp_stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
@@ -662,10 +675,10 @@ int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows
     const int thg = p.process == QPM_PROCESS_THG;
     k_fit_exact<<<(unsigned)((rows + 127) / 128), 128, 0, p.hp_stream>>>(
         p.e1 + (int64_t)wl * p.D, thg ? p.b + (int64_t)wl * p.D : nullptr, p.D, thg, p.hp_bits, p.W, nullptr, rows,
-        p.part);
+        p.own->part);
     QPM_LAUNCH_CHECK();
     // part rows are [acc.r, acc.i, 0, 0, 0, 0]; gather the first two doubles
-    QPM_CUDA_TRY(cudaMemcpy2DAsync(out, 2 * sizeof(double), p.part, kPartDoubles * sizeof(double),
+    QPM_CUDA_TRY(cudaMemcpy2DAsync(out, 2 * sizeof(double), p.own->part, kPartDoubles * sizeof(double),
                                    2 * sizeof(double), (size_t)rows, cudaMemcpyDeviceToHost, p.hp_stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
     return QPM_OK;

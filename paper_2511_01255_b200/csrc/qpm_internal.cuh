@@ -62,10 +62,9 @@ struct Problem {
     double2 *qt = nullptr;  // [n_wl][nquads][24]
     double2 *w = nullptr;   // [n_wl]
     double2 *h = nullptr;   // [n_wl]
-    // scratch for fitness launches, sized by reserve()
-    double *part = nullptr;
-    int64_t part_rows = 0;
-    double *gains = nullptr;
+    // scratch of the problem's own entry points (qpm_fitness_bits, host path);
+    // every engine owns its scratch, so engines sharing a problem never race
+    struct FitScratch *own = nullptr;
     // host plugin path buffers
     int8_t *hp_signs = nullptr;
     uint32_t *hp_bits = nullptr;
@@ -75,10 +74,18 @@ struct Problem {
     int64_t device_bytes = 0;
 };
 
-int problem_reserve(Problem *p, int64_t rows);
+// per-row segment partials and per-wavelength gains of one fitness launch
+struct FitScratch {
+    double *part = nullptr;
+    double *gains = nullptr;
+    int64_t rows = 0;
+    int64_t bytes = 0;
+};
+int scratch_reserve(const Problem *p, FitScratch *fs, int64_t rows);
+void scratch_free(FitScratch *fs);
 // launch the fitness of `rows` bit rows (row_index may be null) into out
-int launch_fitness(Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index, int64_t rows,
-                   double *out, int mode, cudaStream_t stream, int *launches);
+int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
+                   const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches);
 int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out, cudaStream_t stream);
 
 }  // namespace qpm

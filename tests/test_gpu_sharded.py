@@ -76,3 +76,26 @@ def test_one_rank_nccl_communicator_in_graph(q):
     eng.init()
     eng.step(12, use_graph=True)
     assert np.array_equal(eng.trace(), ref.trace())
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_engines_sharing_a_problem_run_concurrently(q, mode):
+    """Engines built on one objective own their fitness scratch: stepped
+    concurrently on their own streams they reproduce their solo traces."""
+    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, 900, mode=mode)
+    kws = [dict(pop_size=64, generations=30, seed=s, de=q.DEParams(), gwo=q.GWOParams(), sch=q.Schedules())
+           for s in (1, 2, 3)]
+    solo = []
+    for kw in kws:
+        e = q.Engine(obj, "hybrid", **kw)
+        e.init()
+        e.step(30)
+        solo.append(e.trace())
+    engines = [q.Engine(obj, "hybrid", **kw) for kw in kws]
+    for e in engines:
+        e.init()
+    for _ in range(30):
+        for e in engines:
+            e.step(1)
+    for e, want in zip(engines, solo):
+        assert np.array_equal(e.trace(), want)
