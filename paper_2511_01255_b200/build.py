@@ -42,7 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + ARCH + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    extra = os.environ.get("QPM_NVCC_EXTRA", "").split()  # tuning builds, e.g. -DQPM_DE_MINB=3
+    cmd = [nvcc()] + NVCC_FLAGS + extra + ARCH + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")

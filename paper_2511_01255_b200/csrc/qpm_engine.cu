@@ -18,11 +18,11 @@
 //
 // One hybrid generation is 8 launches, all reading g and F from device
 // memory so a single CUDA graph replays every generation:
-//   k_de_trial      DE index draws (thread 0 of each block), crossover mask,
-//                   trial genome + bits, AND the wolf phase's three random
-//                   draws per gene folded into a 1-byte decision code.  The
-//                   kernel is HBM-bound; the splitmix64 integer work of the
-//                   wolf phase rides in its shadow.
+//   k_plan_rows     (side stream, one generation ahead) keys + DE indices
+//   k_de_trial      crossover mask, trial genome + bits, AND the wolf
+//                   phase's three random draws per gene folded into 8
+//                   bit-planes.  The kernel is HBM-bound; the splitmix64
+//                   integer work rides in its shadow.
 //   fitness x2      segmented quad-table scan + warp-parallel stitch
 //   k_select_topk   greedy selection + top-k leaders (one CTA)
 //   k_gwo_apply     leader vote per gene from the codes -> candidate bits
@@ -52,7 +52,10 @@ constexpr int kRowThreads = 256;    // threads per row-block in the elementwise 
 constexpr int kGenesPerThread = 4;  // genes per thread (strided by kRowThreads)
 constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
 constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
-constexpr int kDeChunk = 4096;      // genes per DE-trial CTA (amortizes the per-row setup)
+constexpr int kDeChunk = 4096;
+#ifndef QPM_DE_MINB
+#define QPM_DE_MINB 3  // k_de_trial CTAs per SM the register budget is sized for
+#endif      // genes per DE-trial CTA (amortizes the per-row setup)
 constexpr int64_t kStatsSmemMaxNP = 12288;  // 2 x NP doubles of dynamic smem (<= 192 KB)
 
 // ncclUniqueId layout (NCCL_UNIQUE_ID_BYTES = 128, nccl.h)
@@ -183,15 +186,20 @@ __device__ void de_row_draws(const RunConsts &c, uint64_t key, int64_t i, int4 &
 // at most three draws of the 6 x D block:
 //   row 0 social;  row 1 pick (social) | 2 disturb (early) | 5 flip (late);
 //   row 3 state | 4 plus (early, not disturbed).
-// They are recorded as 8 bit-planes per 32-gene word (one ballot each):
-//   0 social   1-2 pick   3 disturbed|flipped   4 state (+1)
-//   5-7 plus level L = #{c <= K : u_plus >= p_plus(c)}  (p_plus is
-//   nondecreasing in c, so u_plus < p_plus(count) <=> count >= L).
-// The leader vote is then evaluated 32 genes at a time with bit-sliced logic.
-constexpr int kPlanes = 8;
+// Since social and non-social genes use disjoint outcomes, they share
+// bit-planes (one ballot each per 32-gene word):
+//   P0 social
+//   P1 social ? pick bit 0 : disturbed (early) | flipped (late)
+//   P2 social ? pick bit 1 : state (+1)       -- early & !disturbed: L bit 0
+//   P3, P4 (early, !social, !disturbed) L bits 1, 2, with the plus level
+//      L = #{c <= K : u_plus >= p_plus(c)}  (p_plus is nondecreasing in c, so
+//      u_plus < p_plus(count) <=> count >= L)
+// so a late generation writes 3 planes and an early one 5.  The leader vote
+// is then evaluated 32 genes at a time with bit-sliced logic.
+constexpr int kPlanes = 8;  // plane slots per word (P0..P4 used)
 
 // bit-sliced leader vote of one 32-gene word.  ld[t]: leader t's sign bits
-// (1 = -1); pl: the word's 8 planes.  Returns the candidate's sign bits.
+// (1 = -1); pl: the word's planes.  Returns the candidate's sign bits.
 template <int K>
 __device__ __forceinline__ uint32_t wolf_word(const uint32_t *ld, const uint32_t *pl, bool early) {
     // count of +1 leaders per gene, as bits s2 s1 s0
@@ -206,63 +214,35 @@ __device__ __forceinline__ uint32_t wolf_word(const uint32_t *ld, const uint32_t
         s2 = s1 & cy;
         s1 ^= cy;
     }
-    const uint32_t soc = pl[0], p0 = pl[1], p1 = pl[2], f2 = pl[3], st = pl[4];
+    const uint32_t soc = pl[0], a = pl[1], bb = pl[2];
     uint32_t plus;
     if (early) {
-        // count >= L, three-bit unsigned compare
-        const uint32_t l0 = pl[5], l1 = pl[6], l2 = pl[7];
+        // count >= L (three-bit unsigned compare), L = (P4 P3 P2)
+        const uint32_t l0 = bb, l1 = pl[3], l2 = pl[4];
         const uint32_t ge0 = s0 | ~l0;
         const uint32_t ge1 = (s1 & ~l1) | (~(s1 ^ l1) & ge0);
         const uint32_t ge2 = (s2 & ~l2) | (~(s2 ^ l2) & ge1);
-        plus = (f2 & st) | (~f2 & ge2);
+        plus = (a & bb) | (~a & ge2);  // disturbed: state, else sampled
     } else {
         uint32_t maj;
         if (K == 4)
-            maj = s2 | (s1 & s0) | (s1 & ~s0 & ~s2 & st);  // >= 3 of 4, or a 2-2 tie broken by state
+            maj = s2 | (s1 & s0) | (s1 & ~s0 & ~s2 & bb);  // >= 3 of 4, or a 2-2 tie broken by state
         else
             maj = s1;  // >= 2 of 3
-        plus = maj ^ f2;
+        plus = maj ^ a;
     }
     const uint32_t l3 = K == 4 ? ld[3] : ld[0];
-    const uint32_t lp = (p1 & ((p0 & l3) | (~p0 & ld[2]))) | (~p1 & ((p0 & ld[1]) | (~p0 & ld[0])));
+    const uint32_t lp = (bb & ((a & l3) | (~a & ld[2]))) | (~bb & ((a & ld[1]) | (~a & ld[0])));
     return (soc & lp) | (~soc & ~plus);
-}
-
-template <int K, bool EARLY>
-__device__ __forceinline__ uint32_t wolf_lane_bits(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p1,
-                                                   uint32_t D) {
-    // returns the gene's 8 plane bits packed low to high
-    const uint64_t u1 = mix_at(key, p1);
-    const bool soc = passes(t.sl, u1);
-    const uint64_t u2 = mix_at(key, p1 + (soc ? D : (EARLY ? 2 * D : 5 * D)));
-    uint32_t pick;
-    if (K == 4) {
-        pick = (uint32_t)(u2 >> 62);  // int(u * 4) = m53 >> 51, exact
-    } else {
-        const int pv = (int)((double)(u2 >> 11) * kTwoM53 * (double)K);
-        pick = (uint32_t)(pv < K - 1 ? pv : K - 1);
-    }
-    const bool flag2 = passes(EARLY ? t.dist : t.flip, u2);
-    const uint64_t u3 = mix_at(key, p1 + ((EARLY && !flag2) ? 4 * D : 3 * D));
-    uint32_t L = 0;
-    if (EARLY) {
-        if (K == 4 && c.plus_dyadic) {
-            L = 1u + (uint32_t)(u3 >> 62);  // thresholds c/4: L = 1 + floor(4u)
-        } else {
-#pragma unroll
-            for (int cc = 0; cc <= K; ++cc) L += passes(c.thr_plus[cc], u3) ? 0u : 1u;
-        }
-    }
-    const uint32_t st = (int64_t)u3 >= 0 ? 1u : 0u;  // u < 0.5 <=> top bit clear
-    return (soc ? 1u : 0u) | (pick << 1) | ((flag2 ? 1u : 0u) << 3) | (st << 4) | (L << 5);
 }
 
 // ---------------------------------------------------------------- planner
 // Everything random in generation g depends only on (seed, g, i, position):
-// the planner draws generation g+1's DE indices, crossover mask (1 bit per
-// gene) and wolf planes (8 bits per gene) on a low-priority side stream while
-// generation g's dependent chain (trial -> fitness -> select -> wolf ->
-// fitness -> stats) runs on the main stream.  Buffers alternate by g & 1.
+// the planner draws generation g+1's per-row keys and DE indices (rejection
+// sampling) on a low-priority side stream while generation g's dependent
+// chain runs on the main stream (buffers alternate by g & 1).  The per-gene
+// draws (crossover mask, wolf planes) are made inside k_de_trial, whose HBM
+// stream leaves most issue slots free.
 //
 // Draw arithmetic is trimmed to what each decision needs: splitmix64's last
 // step z ^= z >> 31 leaves bits 63..33 untouched, so top-bit decisions (state,
@@ -272,11 +252,10 @@ __device__ __forceinline__ uint32_t wolf_lane_bits(const RunConsts &c, const Gen
 struct PlanArgs {
     EngineState *st;
     const GenThr *gthr;
-    int64_t row_lo, n_rows;  // rows whose mask / planes this rank draws
+    int64_t row_lo, n_rows;  // this rank's rows
     uint64_t *keys;    // [2][NP]
     int4 *picks;       // [2][NP]  r1, r2, r3, m
     int32_t *jrand;    // [2][NP]
-    uint32_t *mask;    // [2][NP][W]
     uint32_t *planes;  // [2][NP][W][8]
 };
 
@@ -310,6 +289,16 @@ __device__ __forceinline__ bool passes_hi(const Thr &t, uint64_t x, uint32_t h) 
     return !t.never && r;
 }
 
+// branch-free variant: decides on the high word and flags a tie (probability
+// 2^-32 per compare) for the caller's warp-level exact fallback, so two
+// independent draws interleave without per-compare branches
+__device__ __forceinline__ bool lt_hi(const Thr &t, uint32_t h, bool &tie) {
+    const uint32_t ho = h ^ (h >> 31);
+    const uint32_t hl = (uint32_t)(t.le >> 32);
+    tie |= !t.never && ho == hl;
+    return !t.never && ho < hl;
+}
+
 __global__ void k_plan_rows(RunConsts c, PlanArgs a) {
     const int64_t g = a.st->g_plan;
     if (g > c.G) return;
@@ -325,100 +314,123 @@ __global__ void k_plan_rows(RunConsts c, PlanArgs a) {
     }
 }
 
-template <int K, bool EARLY, bool FULL>
-__device__ __forceinline__ void plan_chunk(const RunConsts &c, const PlanArgs &a, const GenThr &t, int64_t b,
-                                           int64_t i, int jc) {
-    const uint64_t key = a.keys[b * c.NP + i];
-    const int4 pk = a.picks[b * c.NP + i];
-    const int jr = a.jrand[b * c.NP + i];
-    const uint32_t p_mask = (uint32_t)pk.w + 2;                  // m + 1 + j, plus one
-    const uint32_t p_wolf = (uint32_t)pk.w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
-    const uint32_t D = (uint32_t)c.D;
-    uint32_t *mrow = a.mask + (b * c.NP + i) * c.W;
-    uint32_t *prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
-    const int lane = threadIdx.x & 31;
+template <bool EXACT>
+__device__ __forceinline__ bool draw_lt(const Thr &t, uint64_t x, uint32_t h, bool &tie) {
+    return EXACT ? passes_hi(t, x, h) : lt_hi(t, h, tie);
+}
+
+// Phase of the wolf draws: late (flip), early (disturb + plus level), or
+// early with dyadic plus thresholds c/4 (K = 4, discreteness 1: the level is
+// the top two bits of the draw).
+enum WolfPhase { kLate = 0, kEarly = 1, kEarlyDyadic = 2 };
+
+// the wolf draws of one gene (stream position p0 = m + 1 + D + j, plus one)
+// as its plane bits (P0..P4 above).  Straight-line code (selects only), so
+// the draws of several genes interleave.  EXACT = false decides every compare
+// on the high word and sets `tie` when one tied; the caller then redoes the
+// gene with EXACT = true.
+template <int K, int PH, bool EXACT>
+__device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p0,
+                                              uint32_t D, bool &tie) {
+    constexpr bool EARLY = PH != kLate;
+    const uint64_t x1 = mix_pre2(key, p0, c.m4);
+    const bool soc = draw_lt<EXACT>(t.sl, x1, mix_hi2(x1), tie);
+    const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)), c.m4);
+    const uint32_t h2 = mix_hi2(x2);
+    uint32_t pick;
+    if (K == 4) {
+        pick = h2 >> 30;  // int(u * 4) = top two bits
+    } else {
+        const uint64_t z = x2 * kMix2;
+        const int pv = (int)((double)((z ^ (z >> 31)) >> 11) * kTwoM53 * (double)K);
+        pick = (uint32_t)min(pv, K - 1);
+    }
+    const uint32_t soc_code = 1u | (pick << 1);
+    const bool f2 = draw_lt<EXACT>(EARLY ? t.dist : t.flip, x2, h2, tie);
+    if (!EARLY && K == 3) return soc ? soc_code : (f2 ? 2u : 0u);  // majority of 3 never ties: no state draw
+    const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c.m4);
+    const uint32_t h3 = mix_hi2(x3);
+    const uint32_t st = (h3 >> 31) ^ 1u;  // u < 0.5
+    uint32_t L = 0;
+    if (PH == kEarlyDyadic) {
+        L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
+    } else if (PH == kEarly) {
 #pragma unroll
-    for (int it = 0; it < kGenesPerThread; ++it) {
-        const int j = jc + it * kRowThreads + threadIdx.x;
-        if (!FULL && j - lane >= (int)c.Dp) break;
-        const bool in = FULL || j < (int)c.D;
-        bool take = false;
-        if (in) {
-            const uint64_t x = mix_pre2(key, p_mask + (uint32_t)j, c.m4);
-            take = passes_hi(c.thr_cr, x, mix_hi2(x)) || j == jr;
-        }
-        const uint32_t mword = __ballot_sync(0xffffffffu, take);
-        const int w = (j - lane) >> 5;
-        if (K > 0) {
-            bool soc = false, f2 = false, st = false;
-            uint32_t pick = 0, L = 0;
-            if (in) {
-                const uint32_t p0 = p_wolf + (uint32_t)j;
-                const uint64_t x1 = mix_pre2(key, p0, c.m4);
-                soc = passes_hi(t.sl, x1, mix_hi2(x1));
-                const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)), c.m4);
-                const uint32_t h2 = mix_hi2(x2);
-                if (K == 4) {
-                    pick = h2 >> 30;  // int(u * 4) = top two bits
-                } else {
-                    const uint64_t z = x2 * kMix2;
-                    const int pv = (int)((double)((z ^ (z >> 31)) >> 11) * kTwoM53 * (double)K);
-                    pick = (uint32_t)(pv < K - 1 ? pv : K - 1);
-                }
-                f2 = passes_hi(EARLY ? t.dist : t.flip, x2, h2);
-                const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c.m4);
-                const uint32_t h3 = mix_hi2(x3);
-                st = (h3 >> 31) == 0u;  // u < 0.5
-                if (EARLY) {
-                    if (K == 4 && c.plus_dyadic) {
-                        L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
-                    } else {
-#pragma unroll
-                        for (int cc = 0; cc <= K; ++cc) L += passes_hi(c.thr_plus[cc], x3, h3) ? 0u : 1u;
-                    }
-                }
-            }
-            const uint32_t w0 = __ballot_sync(0xffffffffu, soc);
-            const uint32_t w1 = __ballot_sync(0xffffffffu, (pick & 1u) != 0u);
-            const uint32_t w2 = __ballot_sync(0xffffffffu, (pick & 2u) != 0u);
-            const uint32_t w3 = __ballot_sync(0xffffffffu, f2);
-            const uint32_t w4 = __ballot_sync(0xffffffffu, st);
-            const uint32_t w5 = __ballot_sync(0xffffffffu, (L & 1u) != 0u);
-            const uint32_t w6 = __ballot_sync(0xffffffffu, (L & 2u) != 0u);
-            const uint32_t w7 = __ballot_sync(0xffffffffu, (L & 4u) != 0u);
-            if (lane == 0) {
-                uint4 *dst = reinterpret_cast<uint4 *>(prow + w * kPlanes);
-                dst[0] = make_uint4(w0, w1, w2, w3);
-                dst[1] = make_uint4(w4, w5, w6, w7);
-            }
-        }
-        if (lane == 0) mrow[w] = mword;
+        for (int cc = 0; cc <= K; ++cc) L += draw_lt<EXACT>(c.thr_plus[cc], x3, h3, tie) ? 0u : 1u;
+    }
+    const uint32_t rest = (EARLY && !f2) ? (L << 2) : ((f2 ? 2u : 0u) | (st << 2));
+    return soc ? soc_code : rest;
+}
+
+// the wolf planes of one 32-gene word from each lane's code: P0..P2, and
+// P3, P4 in early generations; lane `writer` stores them
+template <bool EARLY>
+__device__ __forceinline__ void store_planes(uint32_t *dst_word, uint32_t code, int lane, int writer) {
+    const uint32_t p0 = __ballot_sync(0xffffffffu, code & 1u);
+    const uint32_t p1 = __ballot_sync(0xffffffffu, code & 2u);
+    const uint32_t p2 = __ballot_sync(0xffffffffu, code & 4u);
+    uint32_t p3 = 0, p4 = 0;
+    if (EARLY) {
+        p3 = __ballot_sync(0xffffffffu, code & 8u);
+        p4 = __ballot_sync(0xffffffffu, code & 16u);
+    }
+    if (lane == writer) {
+        uint4 *dst = reinterpret_cast<uint4 *>(dst_word);
+        dst[0] = make_uint4(p0, p1, p2, p3);
+        if (EARLY) dst_word[4] = p4;
     }
 }
 
-// one CTA per (row, 1024-gene chunk) so the block scheduler can interleave
-// these low-priority CTAs with the main stream's kernels
+// the wolf planes of generation g_plan for this rank's rows on the side
+// stream (QPM_WOLF=planner; the default draws them inside k_de_trial)
+template <int K, int PH>
+__device__ __forceinline__ void plan_wolf_items(const RunConsts &c, const PlanArgs &a, const GenThr &t, int64_t b) {
+    const uint32_t D = (uint32_t)c.D;
+    const int lane = threadIdx.x & 31;
+    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
+    const int64_t items = a.n_rows * nchunk;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int64_t i = a.row_lo + item / nchunk;
+        const int jc = (int)(item % nchunk) * kGenesPerBlock;
+        const uint64_t key = a.keys[b * c.NP + i];
+        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + D;  // m + 1 + D + j, plus one
+        uint32_t *prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
+#pragma unroll
+        for (int it = 0; it < kGenesPerThread; it += 2) {
+            int j[2];
+            uint32_t code[2];
+            bool tie[2] = {false, false};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                j[h] = jc + (it + h) * kRowThreads + (int)threadIdx.x;
+                code[h] = wolf_code<K, PH, false>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
+                if (j[h] >= (int)D) code[h] = 0u, tie[h] = false;
+            }
+            if (__any_sync(0xffffffffu, tie[0] || tie[1])) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (tie[h]) code[h] = wolf_code<K, PH, true>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (j[h] - lane >= (int)c.Dp) break;  // warp-uniform
+                store_planes<PH != kLate>(prow + ((j[h] - lane) >> 5) * kPlanes, code[h], lane, 0);
+            }
+        }
+    }
+}
+
 template <int K>
-__global__ void __launch_bounds__(kRowThreads) k_plan_draws(RunConsts c, PlanArgs a) {
+__global__ void __launch_bounds__(kRowThreads) k_plan_wolf(RunConsts c, PlanArgs a) {
     const int64_t g = a.st->g_plan;
     if (g > c.G) return;
-    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
-    const int64_t i = a.row_lo + blockIdx.x / nchunk;
-    const int jc = (int)(blockIdx.x % nchunk) * kGenesPerBlock;
     const GenThr t = a.gthr[g];
-    const bool full = jc + kGenesPerBlock <= (int)c.D;
-    const int64_t b = g & 1;
-    if (K > 0 && t.early) {
-        if (full)
-            plan_chunk<K, true, true>(c, a, t, b, i, jc);
-        else
-            plan_chunk<K, true, false>(c, a, t, b, i, jc);
-    } else {
-        if (full)
-            plan_chunk<K, false, true>(c, a, t, b, i, jc);
-        else
-            plan_chunk<K, false, false>(c, a, t, b, i, jc);
-    }
+    if (!t.early)
+        plan_wolf_items<K, kLate>(c, a, t, g & 1);
+    else if (K == 4 && c.plus_dyadic)
+        plan_wolf_items<K, kEarlyDyadic>(c, a, t, g & 1);
+    else
+        plan_wolf_items<K, kEarly>(c, a, t, g & 1);
 }
 
 __global__ void k_plan_bump(EngineState *st) { st->g_plan += 1; }
@@ -467,8 +479,7 @@ struct TrialArgs {
     const int4 *picks;       // [2][NP]
     const uint64_t *keys;    // [2][NP]
     const int32_t *jrand;    // [2][NP]
-    const uint32_t *mask;    // [2][NP][W]   (own rows)
-    const uint32_t *planes;  // [2][NP][W][8] (own rows)
+    uint32_t *planes;        // [2][NP][W][8] wolf planes (own rows)
     const int32_t *slot_of, *spare_of;
     uint8_t *slot_bin;
     double *genome;
@@ -476,13 +487,20 @@ struct TrialArgs {
     uint32_t *cbits;  // [NP][W] wolf candidates staged for the all-gather (multi-GPU), else null
 };
 
-template <bool BIN, bool FULL, bool DRAW>
+// The trial of row i over genes [jc, jc + kDeChunk) with the crossover mask
+// drawn inline (one splitmix64 per gene).  For K > 0 (run_hybrid, own rows)
+// the same pass draws the row's wolf planes for this generation (three
+// draws per gene): the trial is HBM-bound (~30 B per gene) and the integer
+// work of the draws runs while the genome loads are in flight.
+template <bool BIN, bool FULL, int K, int PH>
 __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
-                                               double F) {
+                                               double F, const GenThr &t) {
     // A warp covers 64 genes per step: lane l owns genes l and l+32, so every
     // load/store is one coalesced 256-byte warp access and the two sign words
     // are plain ballots.
     const int4 pk = a.picks[b * c.NP + i];
+    const uint64_t key = a.keys[b * c.NP + i];
+    const int jr = a.jrand[b * c.NP + i];
     const RowRef xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
     const RowRef x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
     const RowRef x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
@@ -490,55 +508,66 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const int64_t out_slot = a.spare_of[i];
     double *out = a.genome + out_slot * c.Dp;
     uint32_t *bout = a.bits + out_slot * c.W;
-    const uint32_t *mrow = a.mask + (b * c.NP + i) * c.W;
+    uint32_t *prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
+    const uint32_t p_mask = (uint32_t)pk.w + 2;      // m + 1 + j, plus one
+    const uint32_t p_wolf = p_mask + (uint32_t)c.D;  // m + 1 + D + j, plus one
     const int D = (int)c.D;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    constexpr int kSteps = 2;  // 64-gene warp steps per batch (registers)
+    constexpr int kSteps = 2;               // 64-gene warp steps per batch (registers)
     constexpr int kSpan = kRowThreads * 2;  // genes per CTA step
     constexpr int kBatches = kDeChunk / (kSpan * kSteps);
 #pragma unroll 1
     for (int bt = 0; bt < kBatches; ++bt) {
         const int jb = jc + bt * kSpan * kSteps + warp * 64;
-        // all mask bits, then all genome loads of the batch, then the math:
-        // the kernel is bound by memory latency, so keep every load in flight
+        if (!FULL && jb >= (int)c.Dp) break;
+        // mask bits first, then every genome load of the batch, then the wolf
+        // draws while the loads are in flight, then the math
         uint32_t mb[kSteps];
+        bool tie = false;
 #pragma unroll
         for (int st = 0; st < kSteps; ++st) {
-            const int j64 = jb + st * kSpan;
             mb[st] = 0u;
-            if (!FULL && j64 >= (int)c.Dp) continue;
-            if (DRAW) {
-                // a foreign row the planner did not draw: crossover mask inline
-                const uint64_t key = a.keys[b * c.NP + i];
-                const int jr = a.jrand[b * c.NP + i];
-                const uint32_t p_mask = (uint32_t)pk.w + 2;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int jj = jb + st * kSpan + lane + 32 * q;
+                bool ti = false;
+                const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
+                const bool take = lt_hi(c.thr_cr, mix_hi2(x), ti) || jj == jr;
+                if (FULL || jj < D) {
+                    mb[st] |= take ? 1u << q : 0u;
+                    tie |= ti;
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, tie) && tie) {  // a high-word tie (p = 2^-32): exact compares
+#pragma unroll
+            for (int st = 0; st < kSteps; ++st) {
+                mb[st] = 0u;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const int jj = j64 + lane + 32 * q;
-                    if (jj < D) {
-                        const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
-                        if (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == jr) mb[st] |= 1u << q;
-                    }
+                    const int jj = jb + st * kSpan + lane + 32 * q;
+                    const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
+                    if ((FULL || jj < D) && (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == jr)) mb[st] |= 1u << q;
                 }
-            } else {
-                const uint2 w = *reinterpret_cast<const uint2 *>(mrow + (j64 >> 5));
-                mb[st] = ((w.x >> lane) & 1u) | (((w.y >> lane) & 1u) << 1);
             }
         }
         double y[kSteps][2], p1[kSteps][2], p2[kSteps][2], p3[kSteps][2];
 #pragma unroll
         for (int st = 0; st < kSteps; ++st) {
+            const int j64 = jb + st * kSpan;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                const int j = jb + st * kSpan + lane + 32 * q;
+                const int j = j64 + lane + 32 * q;
                 y[st][q] = p1[st][q] = p2[st][q] = p3[st][q] = 0.0;
                 if (!FULL && j >= D) continue;
                 if (BIN) {
-                    y[st][q] = xi.at(j);
-                    p1[st][q] = x1.at(j);
-                    p2[st][q] = x2.at(j);
-                    p3[st][q] = x3.at(j);
+                    // +/-1 rows: one broadcast word load per 32 genes
+                    const int w = (j64 >> 5) + q;
+                    y[st][q] = xi.f ? xi.f[j] : (((xi.b[w] >> lane) & 1u) ? -1.0 : 1.0);
+                    p1[st][q] = x1.f ? x1.f[j] : (((x1.b[w] >> lane) & 1u) ? -1.0 : 1.0);
+                    p2[st][q] = x2.f ? x2.f[j] : (((x2.b[w] >> lane) & 1u) ? -1.0 : 1.0);
+                    p3[st][q] = x3.f ? x3.f[j] : (((x3.b[w] >> lane) & 1u) ? -1.0 : 1.0);
                 } else if ((mb[st] >> q) & 1u) {
                     p1[st][q] = x1.f[j];
                     p2[st][q] = x2.f[j];
@@ -546,6 +575,41 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 } else {
                     y[st][q] = xi.f[j];
                 }
+            }
+        }
+        if (K > 0) {
+            uint32_t code[kSteps][2];
+            bool wtie = false;
+#pragma unroll
+            for (int st = 0; st < kSteps; ++st) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int jj = jb + st * kSpan + lane + 32 * q;
+                    bool ti = false;
+                    code[st][q] = wolf_code<K, PH, false>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, ti);
+                    if (!FULL && jj >= D) code[st][q] = 0u, ti = false;
+                    wtie |= ti;
+                }
+            }
+            if (__any_sync(0xffffffffu, wtie) && wtie) {
+#pragma unroll
+                for (int st = 0; st < kSteps; ++st) {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int jj = jb + st * kSpan + lane + 32 * q;
+                        bool ti = false;
+                        if (FULL || jj < D)
+                            code[st][q] = wolf_code<K, PH, true>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, ti);
+                    }
+                }
+            }
+#pragma unroll
+            for (int st = 0; st < kSteps; ++st) {
+                const int j64 = jb + st * kSpan;
+                if (!FULL && j64 >= (int)c.Dp) break;
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    store_planes<PH != kLate>(prow + ((j64 >> 5) + q) * kPlanes, code[st][q], lane, q);
             }
         }
 #pragma unroll
@@ -573,7 +637,29 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[out_slot] = 0;
 }
 
-__global__ void __launch_bounds__(kRowThreads, 4) k_de_trial(RunConsts c, TrialArgs a) {
+template <int K, int PH>
+__device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
+                                                  double F, const GenThr &t, bool bin) {
+    const bool full = jc + kDeChunk <= (int)c.D;
+    if (bin) {
+        if (full)
+            de_trial_chunk<true, true, K, PH>(c, a, b, i, jc, F, t);
+        else
+            de_trial_chunk<true, false, K, PH>(c, a, b, i, jc, F, t);
+    } else {
+        if (full)
+            de_trial_chunk<false, true, K, PH>(c, a, b, i, jc, F, t);
+        else
+            de_trial_chunk<false, false, K, PH>(c, a, b, i, jc, F, t);
+    }
+}
+
+// one CTA per (row, kDeChunk genes).  K = leader count when the CTA also
+// draws the wolf planes (run_hybrid own rows), 0 otherwise; filter mode
+// recomputes the trials of foreign rows that won (multi-GPU)
+template <int K>
+__global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts c, TrialArgs a) {
+    pdl_wait();
     const int64_t g = a.st->g;
     const int64_t b = g & 1;
     const double F = a.st->F;
@@ -581,31 +667,22 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_de_trial(RunConsts c, TrialA
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
     const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
     if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
+    const GenThr t = a.gthr[g];
     const int4 pk = a.picks[b * c.NP + i];
     const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
                      a.slot_bin[a.slot_of[pk.z]];
-    const bool full = jc + kDeChunk <= (int)c.D;
-    if (a.filter) {  // foreign rows: masks drawn inline
-        if (bin)
-            de_trial_chunk<true, false, true>(c, a, b, i, jc, F);
-        else
-            de_trial_chunk<false, false, true>(c, a, b, i, jc, F);
-    } else if (bin) {
-        if (full)
-            de_trial_chunk<true, true, false>(c, a, b, i, jc, F);
-        else
-            de_trial_chunk<true, false, false>(c, a, b, i, jc, F);
-    } else {
-        if (full)
-            de_trial_chunk<false, true, false>(c, a, b, i, jc, F);
-        else
-            de_trial_chunk<false, false, false>(c, a, b, i, jc, F);
-    }
+    if (K == 0 || !t.early)
+        de_trial_dispatch<K, kLate>(c, a, b, i, jc, F, t, bin);
+    else if (K == 4 && c.plus_dyadic)
+        de_trial_dispatch<K, kEarlyDyadic>(c, a, b, i, jc, F, t, bin);
+    else
+        de_trial_dispatch<K, kEarly>(c, a, b, i, jc, F, t, bin);
 }
 
 // multi-GPU: all-gathered wolf candidates of accepted (non-leader) rows into
 // their spare slots, ahead of the selection
 __global__ void k_commit_cand_bits(RunConsts c, TrialArgs a) {
+    pdl_wait();
     const int64_t total = c.NP * c.W;
     int32_t lead[kMaxLeaders];
 #pragma unroll
@@ -627,6 +704,7 @@ __global__ void k_commit_cand_bits(RunConsts c, TrialArgs a) {
 // genes).  Leaders do not move (optimizer.py:454).
 template <int K>
 __global__ void __launch_bounds__(kRowThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
+    pdl_wait();
     const int64_t g = a.st->g;
     const bool early = a.gthr[g].early != 0;
     const uint32_t *planes = a.planes + (g & 1) * c.NP * c.W * kPlanes;
@@ -650,9 +728,9 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_apply(RunConsts c, TrialArg
         uint32_t ld[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) ld[t] = t < K ? lrow[t][w] : 0u;
-        const uint4 *pp = reinterpret_cast<const uint4 *>(planes + (i * c.W + w) * kPlanes);
-        const uint4 q0 = pp[0], q1 = pp[1];
-        const uint32_t pl[kPlanes] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const uint32_t *pw = planes + (i * c.W + w) * kPlanes;
+        const uint4 q0 = *reinterpret_cast<const uint4 *>(pw);
+        const uint32_t pl[5] = {q0.x, q0.y, q0.z, q0.w, early ? pw[4] : 0u};
         const int rem = (int)c.D - w * 32;
         const uint32_t valid = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
         const uint32_t word = wolf_word<K>(ld, pl, early) & valid;
@@ -663,13 +741,13 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_apply(RunConsts c, TrialArg
 
 // ---------------------------------------------------------------- run_gwo
 // gwo_reference_update (optimizer.py:302-332) with the three ranked leaders
-__global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, const EngineState *__restrict__ st,
+__global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, const EngineState *st,
                                                                 const double *__restrict__ sched, int64_t row_lo,
-                                                                const int32_t *__restrict__ slot_of,
-                                                                const int32_t *__restrict__ spare_of,
+                                                                const int32_t *slot_of, const int32_t *spare_of,
                                                                 uint8_t *__restrict__ slot_bin,
                                                                 double *__restrict__ genome,
                                                                 uint32_t *__restrict__ bits) {
+    pdl_wait();
     const int64_t i = row_lo + blockIdx.y;
     for (int t = 0; t < 3; ++t)
         if (st->leaders[t] == i) return;
@@ -832,9 +910,10 @@ __device__ double block_pairwise(const double *v, int64_t n, const RunConsts &c,
 // de_select over all individuals (strict >, ties keep the target), then
 // rank_leaders (optimizer.py:437-444).  One CTA.
 __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, EngineState *__restrict__ st,
-                                                             const double *__restrict__ cand,
+                                                             const double *cand,
                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                              int32_t *__restrict__ spare_of) {
+    pdl_wait();
     for (int64_t i = threadIdx.x; i < c.NP; i += blockDim.x) {
         const double f = cand[i];
         if (f > fit[i]) {
@@ -849,7 +928,8 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, Engine
 }
 
 __global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, EngineState *__restrict__ st,
-                                                              const double *__restrict__ fit, int k) {
+                                                              const double *fit, int k) {
+    pdl_wait();
     block_topk_k(fit, c.NP, k, st->leaders);
 }
 
@@ -862,12 +942,13 @@ __global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, Engin
 // (optimizer.py:586-589), and the trace row.  One CTA.
 __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int mode, EngineState *__restrict__ st,
                                                               const double *__restrict__ sched,
-                                                              const double *__restrict__ cand,
+                                                              const double *cand,
                                                               double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                               int32_t *__restrict__ spare_of,
                                                               uint8_t *__restrict__ slot_bin,
                                                               double *__restrict__ scratch, SumTree tr,
                                                               double *__restrict__ trace) {
+    pdl_wait();
     const int64_t n = c.NP;
     __shared__ EngineState s_state;
     {
@@ -1063,8 +1144,8 @@ struct Engine {
     double *genome = nullptr;
     uint32_t *bits = nullptr;
     uint8_t *slot_bin = nullptr;
-    uint32_t *planes = nullptr, *mask = nullptr;  // [2][...] by generation parity
-    uint32_t *cbits = nullptr;                    // [NP][W] wolf candidates staged for exchange
+    uint32_t *planes = nullptr;  // [2][NP][W][8] by generation parity
+    uint32_t *cbits = nullptr;   // [NP][W] wolf candidates staged for exchange
     GenThr *gthr = nullptr;
     cudaStream_t side = nullptr;  // low-priority planner stream
     int rank = 0, world = 1;       // row shard of this engine (multi-GPU)
@@ -1085,7 +1166,11 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
-    int trial_grid = 148, apply_grid = 148, plan_grid = 148;
+    int apply_grid = 148;
+    int plan_grid = 148;       // k_plan_wolf CTAs (QPM_PLAN_CTAS)
+    bool plan_after_trial = false;  // fork the planner after k_de_trial (QPM_PLAN_FORK=trial)
+    bool wolf_in_planner = false;   // wolf planes on the side stream (QPM_WOLF=planner)
+    bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
     int64_t g_done = 0;
     bool initialized = false;
     bool owns_stream = false;
@@ -1183,10 +1268,9 @@ static size_t stats_smem_bytes(const RunConsts &c) {
 }
 
 static int launch_select_stats(Engine *e, int mode, cudaStream_t s) {
-    k_select_stats<<<1, kCtaThreads, stats_smem_bytes(e->c), s>>>(e->c, mode, e->st, e->sched, e->cand, e->fit,
-                                                                  e->slot_of, e->spare_of, e->slot_bin, e->scratch,
-                                                                  e->tree, e->trace);
-    QPM_LAUNCH_CHECK();
+    QPM_CUDA_TRY(launch_k(e->pdl, k_select_stats, dim3(1), dim3(kCtaThreads), stats_smem_bytes(e->c), s, e->c, mode,
+                          e->st, (const double *)e->sched, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
+                          e->slot_bin, e->scratch, e->tree, e->trace));
     return QPM_OK;
 }
 
@@ -1204,7 +1288,6 @@ static TrialArgs trial_args(const Engine *e, int64_t row_lo, int64_t n_rows) {
     a.picks = e->picks;
     a.keys = e->keys;
     a.jrand = e->jrand;
-    a.mask = e->mask;
     a.planes = e->planes;
     a.cbits = e->world > 1 ? e->cbits : nullptr;
     a.slot_of = e->slot_of;
@@ -1224,7 +1307,6 @@ static PlanArgs plan_args(const Engine *e) {
     a.keys = e->keys;
     a.picks = e->picks;
     a.jrand = e->jrand;
-    a.mask = e->mask;
     a.planes = e->planes;
     return a;
 }
@@ -1234,13 +1316,12 @@ static int enqueue_planner(Engine *e, cudaStream_t s) {
     const RunConsts &c = e->c;
     const PlanArgs pa = plan_args(e);
     k_plan_rows<<<(unsigned)((c.NP + 127) / 128), 128, 0, s>>>(c, pa);
-    const unsigned items = (unsigned)(pa.n_rows * ((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock));
-    if (c.algorithm == QPM_ALGO_HYBRID && c.k == 4)
-        k_plan_draws<4><<<items, kRowThreads, 0, s>>>(c, pa);
-    else if (c.algorithm == QPM_ALGO_HYBRID)
-        k_plan_draws<3><<<items, kRowThreads, 0, s>>>(c, pa);
-    else
-        k_plan_draws<0><<<items, kRowThreads, 0, s>>>(c, pa);
+    if (c.algorithm == QPM_ALGO_HYBRID && e->wolf_in_planner) {
+        if (c.k == 4)
+            k_plan_wolf<4><<<e->plan_grid, kRowThreads, 0, s>>>(c, pa);
+        else
+            k_plan_wolf<3><<<e->plan_grid, kRowThreads, 0, s>>>(c, pa);
+    }
     k_plan_bump<<<1, 1, 0, s>>>(e->st);
     QPM_LAUNCH_CHECK();
     return QPM_OK;
@@ -1323,14 +1404,17 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     if (c.algorithm == QPM_ALGO_GWO) {
         if (phase == 0) {
             mark("topk");
-            k_topk_leaders<<<1, kCtaThreads, 0, s>>>(c, e->st, e->fit, 3);  // rank_leaders(pop, 3)
+            QPM_CUDA_TRY(launch_k(false, k_topk_leaders, dim3(1), dim3(kCtaThreads), 0, s, c, e->st,
+                                  (const double *)e->fit, 3));  // rank_leaders(pop, 3); first kernel: no PDL
             mark("gwo_continuous");
-            k_gwo_continuous<<<row_grid(e, NP), kRowThreads, 0, s>>>(c, e->st, e->sched, 0, e->slot_of, e->spare_of,
-                                                                     e->slot_bin, e->genome, e->bits);
+            QPM_CUDA_TRY(launch_k(e->pdl, k_gwo_continuous, row_grid(e, NP), dim3(kRowThreads), 0, s, c,
+                                  (const EngineState *)e->st, (const double *)e->sched, (int64_t)0,
+                                  (const int32_t *)e->slot_of, (const int32_t *)e->spare_of, e->slot_bin, e->genome,
+                                  e->bits));
             QPM_LAUNCH_CHECK();
             *n += 2;
             mark("fitness");
-            rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+            rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n, e->pdl);
             if (rc) return rc;
         } else {
             mark("replace_stats");
@@ -1350,22 +1434,33 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     foreign.own_hi = e->own_hi;
     if (phase == 0) {
         // fork: the planner draws generation g+1 on the side stream
-        QPM_CUDA_TRY(cudaEventRecord(e->ev_fork, s));
-        QPM_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
-        if ((rc = enqueue_planner(e, e->side))) return rc;
-        QPM_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
-        *n += 3;
+        auto fork = [&]() -> int {
+            QPM_CUDA_TRY(cudaEventRecord(e->ev_fork, s));
+            QPM_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+            int r = enqueue_planner(e, e->side);
+            if (r) return r;
+            QPM_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
+            *n += (hybrid && e->wolf_in_planner) ? 3 : 2;
+            return QPM_OK;
+        };
+        if (!e->plan_after_trial && (rc = fork())) return rc;
         mark("de_trial");
-        k_de_trial<<<(unsigned)(n_own * de_chunks), kRowThreads, 0, s>>>(c, own);
+        auto kern = (!hybrid || e->wolf_in_planner) ? k_de_trial<0> : (c.k == 4 ? k_de_trial<4> : k_de_trial<3>);
+        // the generation's first kernel is never launched programmatically: a
+        // graph's root node would otherwise overlap the previous replay's
+        // tail, including its planner branch
+        QPM_CUDA_TRY(launch_k(false, kern, dim3((unsigned)(n_own * de_chunks)), dim3(kRowThreads), 0, s, c, own));
         QPM_LAUNCH_CHECK();
         *n += 1;
+        if (e->plan_after_trial && (rc = fork())) return rc;
         mark("fitness_de");
-        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n, e->pdl);
     }
     if (phase == 1) {
         if (sharded) {
             mark("de_trial_foreign");
-            k_de_trial<<<(unsigned)(NP * de_chunks), kRowThreads, 0, s>>>(c, foreign);
+            QPM_CUDA_TRY(launch_k(e->pdl, k_de_trial<0>, dim3((unsigned)(NP * de_chunks)), dim3(kRowThreads), 0, s, c,
+                                  foreign));
             QPM_LAUNCH_CHECK();
             *n += 1;
         }
@@ -1377,21 +1472,20 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             return QPM_OK;
         }
         mark("select_topk");
-        k_select_topk<<<1, kCtaThreads, 0, s>>>(c, e->st, e->cand, e->fit, e->slot_of, e->spare_of);
+        QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3(1), dim3(kCtaThreads), 0, s, c, e->st,
+                              (const double *)e->cand, e->fit, e->slot_of, e->spare_of));
         mark("gwo_apply");
-        if (c.k == 4)
-            k_gwo_apply<4><<<e->apply_grid, kRowThreads, 0, s>>>(c, own);
-        else
-            k_gwo_apply<3><<<e->apply_grid, kRowThreads, 0, s>>>(c, own);
+        QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>, dim3(e->apply_grid),
+                              dim3(kRowThreads), 0, s, c, own));
         QPM_LAUNCH_CHECK();
         *n += 2;
         mark("fitness_gwo");
-        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n);
+        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n, e->pdl);
     }
     // phase 2 (hybrid)
     if (sharded) {
         mark("commit_wolves");
-        k_commit_cand_bits<<<e->apply_grid, kRowThreads, 0, s>>>(c, foreign);
+        QPM_CUDA_TRY(launch_k(e->pdl, k_commit_cand_bits, dim3(e->apply_grid), dim3(kRowThreads), 0, s, c, foreign));
         QPM_LAUNCH_CHECK();
         *n += 1;
     }
@@ -1522,21 +1616,19 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         return QPM_ERR_CUDA;
     }
     {
-        int dev = 0, sms = 148, occ_t = 1, occ_a = 1;
+        int dev = 0, sms = 148, occ_a = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        int occ_p = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_de_trial, kRowThreads, 0);
-        if (c.k == 4) {
+        if (c.k == 4)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_gwo_apply<4>, kRowThreads, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_plan_draws<4>, kRowThreads, 0);
-        } else {
+        else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_gwo_apply<3>, kRowThreads, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_plan_draws<3>, kRowThreads, 0);
-        }
-        e->plan_grid = sms * std::max(occ_p, 1);
-        e->trial_grid = sms * std::max(occ_t, 1);
         e->apply_grid = sms * std::max(occ_a, 1);
+        e->plan_grid = sms * 2;
+        if (const char *v = getenv("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
+        if (const char *v = getenv("QPM_PLAN_FORK")) e->plan_after_trial = strcmp(v, "trial") == 0;
+        if (const char *v = getenv("QPM_WOLF")) e->wolf_in_planner = strcmp(v, "planner") == 0;
+        if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
     }
     HostTree ht = build_tree(c.NP);
     c.n_leaf = (int32_t)ht.leaf_off.size() - 1;
@@ -1553,7 +1645,6 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->bits, (size_t)2 * NP * c.W);
     QPM_ALLOC(e->slot_bin, (size_t)2 * NP);
     QPM_ALLOC(e->planes, P->algorithm == QPM_ALGO_HYBRID ? (size_t)2 * NP * c.W * kPlanes : 16);
-    QPM_ALLOC(e->mask, P->algorithm != QPM_ALGO_GWO ? (size_t)2 * NP * c.W : 16);
     QPM_ALLOC(e->cbits, P->algorithm == QPM_ALGO_HYBRID ? (size_t)NP * c.W : 16);
     QPM_ALLOC(e->gthr, (size_t)(P->G + 1));
     QPM_ALLOC(e->slot_of, NP);
@@ -1936,7 +2027,7 @@ int qpm_engine_launches_per_generation(const qpm_engine *h) {
     if (!h) return -1;
     if (h->e->launches) return h->e->launches;
     const int a = h->e->c.algorithm;
-    return a == QPM_ALGO_HYBRID ? 8 : (a == QPM_ALGO_DE ? 4 : 6);
+    return a == QPM_ALGO_HYBRID ? 10 : 6;  // single-rank counts (enqueue_phase)
 }
 
 int qpm_engine_fitness_ptr(qpm_engine *h, double **fit_dev) {

@@ -24,12 +24,14 @@
 //   T += sB (2 DADD): 10 FP64 instructions per 4 domain-evals instead of the
 //   direct form's 8 per domain.  The sign flip is an integer XOR on the high
 //   word.  A quad's 8 entries are one 128-byte shared-memory row, so any
-//   lane pattern is bank-conflict free.  Rows map to lanes (256 rows per CTA),
-//   the table chunk for 32 quads (12 KB) is staged in shared memory and
-//   shared by all 256 rows.  Segments of the domain axis run in parallel and
-//   are stitched by k_fit_finish:  acc = sum_s (acc_s + C_s T_s),
-//   C_s = sum_{s'<s} P_s', in a fixed order, so fitness is a pure function of
-//   the row bits (required: 18% of selections compare identical projections).
+//   lane pattern is bank-conflict free.  Rows map to lanes (128 rows per
+//   CTA); the table chunk for 32 quads (12 KB) is staged in shared memory by
+//   TMA and shared by the CTA's rows.  Within a chunk, the 4 bit words are
+//   scanned as 4 interleaved sub-chains (ILP).  Segments of the domain axis
+//   run in parallel and are stitched by k_fit_finish:
+//   acc = sum_s (acc_s + C_s T_s), C_s = sum_{s'<s} P_s', in a fixed order,
+//   so fitness is a pure function of the row bits (required: 18% of
+//   selections compare identical projections).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -75,6 +77,7 @@ __global__ void k_pack_signs(const int8_t *__restrict__ signs, int64_t rows, int
 }
 
 // quad tables: entry rel (bit k-1 set <=> s_k != s_0) of B, E, I for quad q
+// (the s_0 = +1 values; the scan flips B and E by s_0)
 __global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__restrict__ b, int64_t D,
                               int64_t nquads, int n_wl, int thg, double2 *__restrict__ qt) {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -118,18 +121,19 @@ __global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__r
 // ------------------------------------------------------------ exact path
 // one thread per (row, wavelength); numba's _thg_sum_nb / _shg_sum_nb order
 __global__ void k_fit_exact(const double2 *__restrict__ e1, const double2 *__restrict__ b, int64_t D, int thg,
-                            const uint32_t *__restrict__ bits, int64_t W, const int32_t *__restrict__ row_index,
-                            int64_t rows, double *__restrict__ part) {
+                            const uint32_t *bits, int64_t W, const int32_t *row_index, int64_t rows,
+                            double *__restrict__ part) {
+    pdl_wait();
     int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int lam = blockIdx.y;
     if (r >= rows) return;
-    const uint32_t *rb = bits + (int64_t)(row_index ? row_index[r] : r) * W;
+    const uint32_t *rb = bits + (int64_t)(row_index ? __ldcg(row_index + r) : r) * W;
     const double2 *el = e1 + (int64_t)lam * D;
     const double2 *bl = thg ? b + (int64_t)lam * D : nullptr;
     double ar = 0.0, ai = 0.0, pr = 0.0, pi = 0.0;
     uint32_t word = 0;
     for (int64_t j = 0; j < D; ++j) {
-        if ((j & 31) == 0) word = rb[j >> 5];
+        if ((j & 31) == 0) word = __ldcg(rb + (j >> 5));
         double sd = ((word >> (j & 31)) & 1u) ? -1.0 : 1.0;
         double2 e = el[j];
         if (thg) {
@@ -176,36 +180,53 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+// spin on test_wait (non-suspending): the chunks arrive within ~1 us, and a
+// suspended try_wait can oversleep that by several microseconds
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
 }
 
+// Segment concatenation: (a1, P1, T1) . (a2, P2, T2) = (a1 + a2 + P1 T2, P1 + P2, T1 + T2).
+struct Seg {
+    double ar, ai, pr, pi, tr, ti;
+};
+
+__device__ __forceinline__ Seg seg_cat(const Seg &x, const Seg &y) {
+    Seg z;
+    z.ar = (x.ar + y.ar) + fma(x.pr, y.tr, -x.pi * y.ti);
+    z.ai = (x.ai + y.ai) + fma(x.pr, y.ti, x.pi * y.tr);
+    z.pr = x.pr + y.pr;
+    z.pi = x.pi + y.pi;
+    z.tr = x.tr + y.tr;
+    z.ti = x.ti + y.ti;
+    return z;
+}
+
 constexpr int kChunkEntries = kQuadsPerChunk * kQuadEntries;  // 768 double2 = 12 KB
 constexpr uint32_t kChunkBytes = kChunkEntries * sizeof(double2);
+constexpr int kFitSmem = 2 * kChunkBytes;  // double-buffered chunks (dynamic shared memory)
 
 template <bool THG>
 __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,
                                                           int64_t nchunks, int seg_chunks, int S,
-                                                          const uint32_t *__restrict__ bits, int64_t W,
-                                                          const int32_t *__restrict__ row_index, int64_t rows,
+                                                          const uint32_t *bits, int64_t W,
+                                                          const int32_t *row_index, int64_t rows,
                                                           double *__restrict__ part) {
-    __shared__ __align__(128) double2 tab[2][kChunkEntries];  // 2 x 12 KB
+    extern __shared__ __align__(128) double2 tab[];  // 2 x 12 KB
     __shared__ __align__(8) uint64_t bar[2];
     const int s = blockIdx.x;
     const int lam = blockIdx.z;
     const int tid = threadIdx.x;
     const int64_t r = (int64_t)blockIdx.y * kFitThreads + tid;
     const bool active = r < rows;
-    const uint4 *rb =
-        reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? row_index[r] : r) : 0) * W);
     const double2 *qtl = qt + (int64_t)lam * nquads * kQuadEntries;
     const int64_t c0 = (int64_t)s * seg_chunks;
     const int n = (int)((c0 + seg_chunks < nchunks ? c0 + seg_chunks : nchunks) - c0);
@@ -215,45 +236,62 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
-        bulk_load(tab[0], qtl + c0 * kChunkEntries, kChunkBytes, &bar[0]);
-        if (n > 1) bulk_load(tab[1], qtl + (c0 + 1) * kChunkEntries, kChunkBytes, &bar[1]);
+    if (tid == 0) {  // the tables are the problem's own: staged before waiting on the predecessor
+        bulk_load(tab, qtl + c0 * kChunkEntries, kChunkBytes, &bar[0]);
+        if (n > 1) bulk_load(tab + kChunkEntries, qtl + (c0 + 1) * kChunkEntries, kChunkBytes, &bar[1]);
     }
-    double ar = 0.0, ai = 0.0, pr = 0.0, pi = 0.0, tr = 0.0, ti = 0.0;
+    pdl_wait();
+    const uint4 *rb =
+        reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? __ldcg(row_index + r) : r) : 0) * W);
+    // The 32 quads of a chunk are scanned as 4 independent sub-chains (one
+    // per bit word, 8 quads each) interleaved for instruction-level
+    // parallelism, then stitched in a fixed order: (c0 . c1) . (c2 . c3).
+    Seg run = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    uint4 w4 = active ? __ldcg(rb + c0) : make_uint4(0, 0, 0, 0);
     for (int k = 0; k < n; ++k) {
         const int buf = k & 1;
-        const uint4 w4 = active ? rb[c0 + k] : make_uint4(0, 0, 0, 0);
-        mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
-        const double2 *tb = tab[buf];
         const uint32_t words[4] = {w4.x, w4.y, w4.z, w4.w};
+        if (k + 1 < n) w4 = active ? __ldcg(rb + c0 + k + 1) : make_uint4(0, 0, 0, 0);  // next chunk's bits
+        mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
+        const double2 *tb = tab + buf * kChunkEntries;
+        Seg ch[4];
 #pragma unroll
-        for (int q = 0; q < kQuadsPerChunk; ++q) {
-            const uint32_t nib = (words[q >> 3] >> (4 * (q & 7))) & 0xFu;
-            const uint32_t s0 = nib & 1u;
-            const uint32_t rel = ((nib ^ (0u - s0)) >> 1) & 7u;
-            const uint64_t m = sign_mask64(s0);
-            const double2 *tq = tb + q * kQuadEntries;
-            const double2 E = tq[8 + rel];
-            const double ser = flip_if(E.x, m), sei = flip_if(E.y, m);
-            if (THG) {
-                const double2 B = tq[rel];
-                const double2 I = tq[16 + rel];
-                const double sbr = flip_if(B.x, m), sbi = flip_if(B.y, m);
-                ar = fma(pr, sbr, ar);
-                ar = fma(-pi, sbi, ar);
-                ar += I.x;
-                ai = fma(pr, sbi, ai);
-                ai = fma(pi, sbr, ai);
-                ai += I.y;
-                tr += sbr;
-                ti += sbi;
+        for (int h = 0; h < 4; ++h) ch[h] = Seg{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int q = 8 * h + u;
+                const uint32_t nib = (words[h] >> (4 * u)) & 0xFu;
+                const uint32_t s0 = nib & 1u;
+                const uint32_t rel = ((nib ^ (0u - s0)) >> 1) & 7u;
+                const uint64_t m = sign_mask64(s0);
+                const double2 *tq = tb + q * kQuadEntries + rel;
+                const double2 Et = tq[8];
+                const double2 E = make_double2(flip_if(Et.x, m), flip_if(Et.y, m));
+                Seg &z = ch[h];
+                if (THG) {
+                    const double2 Bt = tq[0];
+                    const double2 I = tq[16];
+                    const double2 B = make_double2(flip_if(Bt.x, m), flip_if(Bt.y, m));
+                    z.ar = fma(z.pr, B.x, z.ar);
+                    z.ar = fma(-z.pi, B.y, z.ar);
+                    z.ar += I.x;
+                    z.ai = fma(z.pr, B.y, z.ai);
+                    z.ai = fma(z.pi, B.x, z.ai);
+                    z.ai += I.y;
+                    z.tr += B.x;
+                    z.ti += B.y;
+                }
+                z.pr += E.x;
+                z.pi += E.y;
             }
-            pr += ser;
-            pi += sei;
         }
         __syncthreads();  // every lane is done with tab[buf]
-        if (tid == 0 && k + 2 < n) bulk_load(tab[buf], qtl + (c0 + k + 2) * kChunkEntries, kChunkBytes, &bar[buf]);
+        if (tid == 0 && k + 2 < n) bulk_load(tab + buf * kChunkEntries, qtl + (c0 + k + 2) * kChunkEntries, kChunkBytes, &bar[buf]);
+        run = seg_cat(run, seg_cat(seg_cat(ch[0], ch[1]), seg_cat(ch[2], ch[3])));
     }
+    const double ar = run.ar, ai = run.ai, pr = run.pr, pi = run.pi, tr = run.tr, ti = run.ti;
     if (!active) return;
     double *o = part + (((int64_t)lam * rows + r) * S + s) * kPartDoubles;
     if (THG) {
@@ -275,29 +313,14 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
 
 // stitch segments, apply w/hconst, |.| (glibc hypot), scale, objective.
 // One warp per row: lane l stitches a contiguous run of segments, then the
-// 32 runs are stitched by a fixed shuffle tree (deterministic).  Segment
-// concatenation: (a1, P1, T1) . (a2, P2, T2) = (a1 + a2 + P1 T2, P1 + P2, T1 + T2).
-struct Seg {
-    double ar, ai, pr, pi, tr, ti;
-};
-
-__device__ __forceinline__ Seg seg_cat(const Seg &x, const Seg &y) {
-    Seg z;
-    z.ar = (x.ar + y.ar) + fma(x.pr, y.tr, -x.pi * y.ti);
-    z.ai = (x.ai + y.ai) + fma(x.pr, y.ti, x.pi * y.tr);
-    z.pr = x.pr + y.pr;
-    z.pi = x.pi + y.pi;
-    z.tr = x.tr + y.tr;
-    z.ti = x.ti + y.ti;
-    return z;
-}
-
+// 32 runs are stitched by a fixed shuffle tree (deterministic).
 constexpr int kFinishWarps = 4;
 
 __global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
-    const double *__restrict__ part, int S, int64_t rows, int n_wl, const double2 *__restrict__ w,
+    const double *part, int S, int64_t rows, int n_wl, const double2 *__restrict__ w,
     const double2 *__restrict__ h, int thg, double scale, int multi, double g0, double beta,
     double *__restrict__ gains, double *__restrict__ out) {
+    pdl_wait();
     const int64_t r = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
@@ -309,13 +332,13 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
         const double *p = part + ((int64_t)lam * rows + r) * S * kPartDoubles;
         double ar, ai;
         if (S == 1) {
-            ar = p[0];  // exact mode: the row's sum, untouched
-            ai = p[1];
+            ar = __ldcg(p);  // exact mode: the row's sum, untouched
+            ai = __ldcg(p + 1);
         } else {
             Seg acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             for (int s = s0; s < s1; ++s) {
                 const double *q = p + (int64_t)s * kPartDoubles;
-                const Seg y = {q[0], q[1], q[2], q[3], q[4], q[5]};
+                const Seg y = {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5)};
                 acc = s == s0 ? y : seg_cat(acc, y);
             }
             for (int off = 1; off < 32; off <<= 1) {
@@ -442,8 +465,12 @@ static int problem_reserve(Problem *p, int64_t rows) {
     return rc;
 }
 
+// With pdl the kernels may become resident while their predecessor still
+// writes: everything a predecessor produces (bits, row ids, partials) is read
+// with ld.global.cg (__ldcg), never through the non-coherent read-only path.
 int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
-                   const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches) {
+                   const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches,
+                   bool pdl) {
     QPM_ARG_CHECK(row_words == p->W, "row_words must equal qpm_problem_row_words()");
     QPM_ARG_CHECK(rows >= 0, "rows >= 0");
     if (rows == 0) return QPM_OK;
@@ -452,22 +479,20 @@ int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64
     int S;
     if (mode == QPM_MODE_EXACT) {
         S = 1;
-        dim3 grid((unsigned)((rows + 127) / 128), (unsigned)p->n_wl);
-        k_fit_exact<<<grid, 128, 0, stream>>>(p->e1, p->b, p->D, thg, bits, p->W, row_index, rows, fs->part);
+        const dim3 grid((unsigned)((rows + 127) / 128), (unsigned)p->n_wl);
+        QPM_CUDA_TRY(launch_k(pdl, k_fit_exact, grid, dim3(128), 0, stream, (const double2 *)p->e1, (const double2 *)p->b,
+                              p->D, thg, bits, p->W, row_index, rows, fs->part));
     } else {
         S = p->S;
-        dim3 grid((unsigned)S, (unsigned)((rows + kFitThreads - 1) / kFitThreads), (unsigned)p->n_wl);
-        if (thg)
-            k_fit_fast<true><<<grid, kFitThreads, 0, stream>>>(p->qt, p->nquads, p->nchunks, p->seg_chunks, S,
-                                                               bits, p->W, row_index, rows, fs->part);
-        else
-            k_fit_fast<false><<<grid, kFitThreads, 0, stream>>>(p->qt, p->nquads, p->nchunks, p->seg_chunks, S,
-                                                                bits, p->W, row_index, rows, fs->part);
+        const dim3 grid((unsigned)S, (unsigned)((rows + kFitThreads - 1) / kFitThreads), (unsigned)p->n_wl);
+        QPM_CUDA_TRY(launch_k(pdl, thg ? k_fit_fast<true> : k_fit_fast<false>, grid, dim3(kFitThreads), kFitSmem,
+                              stream, (const double2 *)p->qt, p->nquads, p->nchunks, p->seg_chunks, S, bits, p->W,
+                              row_index, rows, fs->part));
     }
-    QPM_LAUNCH_CHECK();
-    k_fit_finish<<<(unsigned)((rows + kFinishWarps - 1) / kFinishWarps), 32 * kFinishWarps, 0, stream>>>(
-        fs->part, S, rows, p->n_wl, p->w, p->h, thg, p->scale, p->multi, p->g0, p->beta, fs->gains, out);
-    QPM_LAUNCH_CHECK();
+    QPM_CUDA_TRY(launch_k(pdl, k_fit_finish, dim3((unsigned)((rows + kFinishWarps - 1) / kFinishWarps)),
+                          dim3(32 * kFinishWarps), 0, stream, (const double *)fs->part, S, rows, p->n_wl,
+                          (const double2 *)p->w, (const double2 *)p->h, thg, p->scale, p->multi, p->g0, p->beta,
+                          fs->gains, out));
     if (launches) *launches += 2;
     return QPM_OK;
 }
@@ -600,6 +625,9 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
     } else if (cudaMemset(p.h, 0, n_wl * sizeof(double2)) != cudaSuccess) {
         return fail((set_error("memset h"), QPM_ERR_CUDA));
     }
+    if (cudaFuncSetAttribute(k_fit_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_fit_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitSmem) != cudaSuccess)
+        return fail((set_error("cudaFuncSetAttribute(k_fit_fast)"), QPM_ERR_CUDA));
     int64_t nt = p.nquads * n_wl;
     k_build_quads<<<(unsigned)((nt + 127) / 128), 128>>>(p.e1, p.b, D, p.nquads, n_wl,
                                                           process == QPM_PROCESS_THG, p.qt);

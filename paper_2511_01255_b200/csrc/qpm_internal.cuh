@@ -8,6 +8,8 @@
 
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "../../include/qpm_b200.h"
 
 namespace qpm {
@@ -42,7 +44,7 @@ void set_error(const char *fmt, ...);
 
 constexpr int kFitThreads = 128;      // rows per fast-fitness CTA (one lane per row)
 constexpr int kQuadsPerChunk = 32;    // 128 domains = 4 u32 words per chunk
-constexpr int kQuadEntries = 24;      // B[8], E[8], I[8] complex entries per quad
+constexpr int kQuadEntries = 24;      // B[8], E[8], I[8] complex entries per quad (by relative signs)
 constexpr int kPartDoubles = 6;       // acc, P, T (complex) per (row, wavelength, segment)
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -85,7 +87,34 @@ int scratch_reserve(const Problem *p, FitScratch *fs, int64_t rows);
 void scratch_free(FitScratch *fs);
 // launch the fitness of `rows` bit rows (row_index may be null) into out
 int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
-                   const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches);
+                   const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches,
+                   bool pdl = false);
+// Programmatic dependent launch: a kernel launched with pdl = true is staged
+// while its stream predecessor runs and starts when the predecessor exits, so
+// the launch latency overlaps the predecessor's tail.  It must call pdl_wait()
+// before touching anything the predecessor wrote (a no-op when launched
+// without the attribute).  No kernel triggers its dependents early
+// (griddepcontrol.launch_dependents): measured on B200, an early trigger let
+// dependents observe stale data in about one C2 run in eight, and the early
+// residents slowed the primary down.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out, cudaStream_t stream);
 
 }  // namespace qpm

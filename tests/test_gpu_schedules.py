@@ -1,0 +1,80 @@
+"""GPU: the engine's scheduling knobs change where and when work runs, never
+the result.  Every combination of wolf-plane placement (inside k_de_trial or
+on the planner stream), planner fork point, planner CTA count and
+programmatic dependent launch must reproduce the default trace bit for bit.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL")
+
+
+@pytest.fixture(scope="module")
+def q():
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_2511_01255_b200 as pkg
+
+    return pkg
+
+
+def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders=4, mode="fast"):
+    for k in KNOBS:
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, D, mode=mode)
+    eng = q.Engine(obj, algorithm, pop_size=NP, generations=G, seed=3, de=q.DEParams(),
+                   gwo=q.GWOParams(leader_count=leaders), sch=q.Schedules(phase_split=0.5))
+    eng.init()
+    eng.step(G)
+    eng.finalize()
+    return eng.trace(), eng.population()[0]
+
+
+VARIANTS = [
+    {"QPM_PDL": "0"},
+    {"QPM_WOLF": "planner"},
+    {"QPM_WOLF": "planner", "QPM_PDL": "0"},
+    {"QPM_WOLF": "planner", "QPM_PLAN_FORK": "trial"},
+    {"QPM_WOLF": "planner", "QPM_PLAN_CTAS": "7"},
+    {"QPM_WOLF": "planner", "QPM_PLAN_CTAS": "1000", "QPM_PLAN_FORK": "trial"},
+]
+
+
+@pytest.mark.parametrize("leaders", [3, 4])
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_schedule_knobs_do_not_change_the_trace(q, monkeypatch, env, leaders):
+    want_t, want_p = _trace(q, monkeypatch, {}, leaders=leaders)
+    got_t, got_p = _trace(q, monkeypatch, env, leaders=leaders)
+    assert np.array_equal(got_t, want_t)
+    assert np.array_equal(got_p, want_p)
+
+
+def test_schedule_knobs_exact_mode_de(q, monkeypatch):
+    want_t, _ = _trace(q, monkeypatch, {}, algorithm="de", mode="exact")
+    got_t, _ = _trace(q, monkeypatch, {"QPM_PDL": "0", "QPM_PLAN_FORK": "trial"}, algorithm="de", mode="exact")
+    assert np.array_equal(got_t, want_t)
+
+
+def test_repeated_runs_are_identical(q, monkeypatch):
+    """Graph replays with the default schedule (planner stream, programmatic
+    launches) are deterministic: repeated runs give the same trace.  Guards
+    against ordering races between the engine's kernels and streams."""
+    for k in KNOBS:
+        monkeypatch.delenv(k, raising=False)
+    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, 6000)
+    traces = []
+    for _ in range(4):
+        eng = q.Engine(obj, "hybrid", pop_size=512, generations=200, seed=9, de=q.DEParams(), gwo=q.GWOParams(),
+                       sch=q.Schedules())
+        eng.init()
+        eng.step(200)
+        traces.append(eng.trace())
+        del eng
+    for t in traces[1:]:
+        assert np.array_equal(t, traces[0])
