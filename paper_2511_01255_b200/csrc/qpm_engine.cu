@@ -114,7 +114,7 @@ struct RunConsts {
     int32_t n_leaf, n_levels;
     Thr thr_cr;      // u <= CR (de_crossover)
     int plus_dyadic; // K = 4 and p_plus(c) = c/4 exactly: plus level = 1 + floor(4u)
-    uint32_t m4;     // = 4, a runtime constant (see xs30_fma)
+    uint32_t m4, m32, m2;  // = 4, 32, 2: runtime constants (see xs_fma)
     Thr thr_plus[5]; // u_plus < p_plus(count), count = 0..K (hybrid K <= 4)
 };
 
@@ -259,19 +259,20 @@ struct PlanArgs {
     uint32_t *planes;  // [2][NP][W][8]
 };
 
-// z ^= z >> 30 with the shifts done as multiplies on the FMA pipe (the ALU
-// pipe is the binding one in this kernel); m4 = 4 is a runtime value so
-// ptxas cannot turn the multiplies back into shifts.
-__device__ __forceinline__ uint64_t xs30_fma(uint64_t z, uint32_t m4) {
+// z ^= z >> s with the shifts done as multiplies on the FMA pipe (the ALU
+// pipe is the binding one in the draw-heavy kernels): m = 2^(32-s) is a
+// runtime value so ptxas cannot turn the multiplies back into shifts.
+__device__ __forceinline__ uint64_t xs_fma(uint64_t z, uint32_t m) {
     const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
-    const uint32_t nlo = lo ^ __umulhi(lo, m4) ^ (hi * m4);
-    const uint32_t nhi = hi ^ __umulhi(hi, m4);
+    const uint32_t nlo = lo ^ __umulhi(lo, m) ^ (hi * m);
+    const uint32_t nhi = hi ^ __umulhi(hi, m);
     return ((uint64_t)nhi << 32) | nlo;
 }
-__device__ __forceinline__ uint64_t mix_pre2(uint64_t key, uint32_t p1, uint32_t m4) {
+// splitmix64 up to (excluding) the last multiply: position p1 = pos + 1
+__device__ __forceinline__ uint64_t mix_pre2(uint64_t key, uint32_t p1, const RunConsts &c) {
     uint64_t z = key + (uint64_t)p1 * kGold;
-    z = xs30_fma(z, m4) * kMix1;
-    return z ^ (z >> 27);
+    z = xs_fma(z, c.m4) * kMix1;  // z ^= z >> 30
+    return xs_fma(z, c.m32);      // z ^= z >> 27
 }
 __device__ __forceinline__ uint32_t mix_hi2(uint64_t x) {  // high word of x * kMix2
     const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
@@ -292,11 +293,13 @@ __device__ __forceinline__ bool passes_hi(const Thr &t, uint64_t x, uint32_t h) 
 // branch-free variant: decides on the high word and flags a tie (probability
 // 2^-32 per compare) for the caller's warp-level exact fallback, so two
 // independent draws interleave without per-compare branches
-__device__ __forceinline__ bool lt_hi(const Thr &t, uint32_t h, bool &tie) {
-    const uint32_t ho = h ^ (h >> 31);
+// (a never-passing threshold has le = 0, so its high word decides "no"; a
+// tie there is resolved by the exact path like any other)
+__device__ __forceinline__ bool lt_hi(const Thr &t, uint32_t h, bool &tie, uint32_t m2) {
+    const uint32_t ho = h ^ __umulhi(h, m2);  // h ^ (h >> 31)
     const uint32_t hl = (uint32_t)(t.le >> 32);
-    tie |= !t.never && ho == hl;
-    return !t.never && ho < hl;
+    tie |= ho == hl;
+    return ho < hl;
 }
 
 __global__ void k_plan_rows(RunConsts c, PlanArgs a) {
@@ -315,8 +318,8 @@ __global__ void k_plan_rows(RunConsts c, PlanArgs a) {
 }
 
 template <bool EXACT>
-__device__ __forceinline__ bool draw_lt(const Thr &t, uint64_t x, uint32_t h, bool &tie) {
-    return EXACT ? passes_hi(t, x, h) : lt_hi(t, h, tie);
+__device__ __forceinline__ bool draw_lt(const RunConsts &c, const Thr &t, uint64_t x, uint32_t h, bool &tie) {
+    return EXACT ? passes_hi(t, x, h) : lt_hi(t, h, tie, c.m2);
 }
 
 // Phase of the wolf draws: late (flip), early (disturb + plus level), or
@@ -333,9 +336,9 @@ template <int K, int PH, bool EXACT>
 __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p0,
                                               uint32_t D, bool &tie) {
     constexpr bool EARLY = PH != kLate;
-    const uint64_t x1 = mix_pre2(key, p0, c.m4);
-    const bool soc = draw_lt<EXACT>(t.sl, x1, mix_hi2(x1), tie);
-    const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)), c.m4);
+    const uint64_t x1 = mix_pre2(key, p0, c);
+    const bool soc = draw_lt<EXACT>(c, t.sl, x1, mix_hi2(x1), tie);
+    const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)), c);
     const uint32_t h2 = mix_hi2(x2);
     uint32_t pick;
     if (K == 4) {
@@ -346,9 +349,9 @@ __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &
         pick = (uint32_t)min(pv, K - 1);
     }
     const uint32_t soc_code = 1u | (pick << 1);
-    const bool f2 = draw_lt<EXACT>(EARLY ? t.dist : t.flip, x2, h2, tie);
+    const bool f2 = draw_lt<EXACT>(c, EARLY ? t.dist : t.flip, x2, h2, tie);
     if (!EARLY && K == 3) return soc ? soc_code : (f2 ? 2u : 0u);  // majority of 3 never ties: no state draw
-    const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c.m4);
+    const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c);
     const uint32_t h3 = mix_hi2(x3);
     const uint32_t st = (h3 >> 31) ^ 1u;  // u < 0.5
     uint32_t L = 0;
@@ -356,7 +359,7 @@ __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &
         L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
     } else if (PH == kEarly) {
 #pragma unroll
-        for (int cc = 0; cc <= K; ++cc) L += draw_lt<EXACT>(c.thr_plus[cc], x3, h3, tie) ? 0u : 1u;
+        for (int cc = 0; cc <= K; ++cc) L += draw_lt<EXACT>(c, c.thr_plus[cc], x3, h3, tie) ? 0u : 1u;
     }
     const uint32_t rest = (EARLY && !f2) ? (L << 2) : ((f2 ? 2u : 0u) | (st << 2));
     return soc ? soc_code : rest;
@@ -532,8 +535,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             for (int q = 0; q < 2; ++q) {
                 const int jj = jb + st * kSpan + lane + 32 * q;
                 bool ti = false;
-                const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
-                const bool take = lt_hi(c.thr_cr, mix_hi2(x), ti) || jj == jr;
+                const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c);
+                const bool take = lt_hi(c.thr_cr, mix_hi2(x), ti, c.m2) || jj == jr;
                 if (FULL || jj < D) {
                     mb[st] |= take ? 1u << q : 0u;
                     tie |= ti;
@@ -547,7 +550,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const int jj = jb + st * kSpan + lane + 32 * q;
-                    const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c.m4);
+                    const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c);
                     if ((FULL || jj < D) && (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == jr)) mb[st] |= 1u << q;
                 }
             }
@@ -811,58 +814,63 @@ __device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
     return a.v > b.v || (a.v == b.v && a.i < b.i);
 }
 
-// top-K of vals[0..n) by (-value, index) (parexec.reduce_best), whole CTA.
-// Every thread keeps a sorted K-list of its strided elements; lists are
-// merged by a fixed shuffle tree inside each warp, then across warps by warp
-// 0.  Insertion is a static bubble (compare-swap down the list), so the lists
-// stay in registers.  Deterministic: (-value, index) is a total order.
-template <int K>
-__device__ __forceinline__ void topk_insert(Cand (&L)[K], Cand e) {
-#pragma unroll
-    for (int t = 0; t < K; ++t) {
-        if (better(e, L[t])) {
-            const Cand tmp = L[t];
-            L[t] = e;
-            e = tmp;
-        }
+// top-K by (-value, index) (parexec.reduce_best), whole CTA.  (-value,
+// index) is a strict total order on the elements, so the top-K set and its
+// order are unique: any merge structure gives the same, exact answer.  Each
+// thread keeps a sorted 4-slot list (unused slots are sentinels, index -1);
+// two sorted lists merge by a bitonic network (4 compare-selects, then a
+// 4-element bitonic sort), lanes merge by an xor butterfly, and warp 0
+// merges the per-warp lists.
+constexpr int kTopSlots = 4;
+
+__device__ __forceinline__ void cswap(Cand &a, Cand &b) {  // a := better of the two
+    if (better(b, a)) {
+        const Cand t = a;
+        a = b;
+        b = t;
     }
 }
 
-template <int K>
-__device__ __forceinline__ void topk_warp_merge(Cand (&L)[K]) {
+__device__ __forceinline__ void topk_insert(Cand (&L)[kTopSlots], Cand e) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        Cand o[K];
-#pragma unroll
-        for (int t = 0; t < K; ++t) {
-            o[t].v = __shfl_down_sync(0xffffffffu, L[t].v, off);
-            o[t].i = __shfl_down_sync(0xffffffffu, L[t].i, off);
-        }
-        if ((threadIdx.x & 31) + off < 32) {
-#pragma unroll
-            for (int t = 0; t < K; ++t) topk_insert<K>(L, o[t]);
-        }
-    }
+    for (int t = 0; t < kTopSlots; ++t) cswap(L[t], e);
 }
 
-template <int K>
-__device__ void block_topk(const double *vals, int64_t n, int32_t *out) {
-    __shared__ double s_v[32][K];
-    __shared__ int32_t s_i[32][K];
+// L := top-4 of L and the list in lane (lane ^ off)
+__device__ __forceinline__ void topk_merge_xor(Cand (&L)[kTopSlots], int off) {
+    Cand o[kTopSlots];
+#pragma unroll
+    for (int t = 0; t < kTopSlots; ++t) {
+        o[t].v = __shfl_xor_sync(0xffffffffu, L[t].v, off);
+        o[t].i = __shfl_xor_sync(0xffffffffu, L[t].i, off);
+    }
+    // the better of L[t] and o[3-t] for every t is the top-4 of the union,
+    // as a bitonic sequence; two compare-swap stages sort it
+#pragma unroll
+    for (int t = 0; t < kTopSlots; ++t)
+        if (better(o[kTopSlots - 1 - t], L[t])) L[t] = o[kTopSlots - 1 - t];
+    cswap(L[0], L[2]);
+    cswap(L[1], L[3]);
+    cswap(L[0], L[1]);
+    cswap(L[2], L[3]);
+}
+
+__device__ __forceinline__ void topk_warp(Cand (&L)[kTopSlots]) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) topk_merge_xor(L, off);
+}
+
+// the CTA's top-k (k <= 4) of the per-thread lists into out[0..k); every
+// thread must call it
+__device__ void block_topk_lists(Cand (&L)[kTopSlots], int k, int32_t *out) {
+    __shared__ double s_v[32][kTopSlots];
+    __shared__ int32_t s_i[32][kTopSlots];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // few warps while n is small: the merge tree costs the same per warp
-    const int nwarps = min((int)(blockDim.x >> 5), max(1, (int)((n + 127) / 128)));
-    const int nthr = nwarps * 32;
-    Cand L[K];
+    const int nwarps = (int)(blockDim.x >> 5);
+    topk_warp(L);
+    if (lane == 0) {
 #pragma unroll
-    for (int t = 0; t < K; ++t) L[t] = {0.0, -1};
-    if (warp < nwarps) {
-        for (int64_t i = threadIdx.x; i < n; i += nthr) topk_insert<K>(L, Cand{vals[i], (int32_t)i});
-        topk_warp_merge<K>(L);
-    }
-    if (lane == 0 && warp < nwarps) {
-#pragma unroll
-        for (int t = 0; t < K; ++t) {
+        for (int t = 0; t < kTopSlots; ++t) {
             s_v[warp][t] = L[t].v;
             s_i[warp][t] = L[t].i;
         }
@@ -870,38 +878,78 @@ __device__ void block_topk(const double *vals, int64_t n, int32_t *out) {
     __syncthreads();
     if (warp == 0) {
 #pragma unroll
-        for (int t = 0; t < K; ++t) L[t] = lane < nwarps ? Cand{s_v[lane][t], s_i[lane][t]} : Cand{0.0, -1};
-        topk_warp_merge<K>(L);
-        if (lane == 0) {
+        for (int t = 0; t < kTopSlots; ++t) L[t] = lane < nwarps ? Cand{s_v[lane][t], s_i[lane][t]} : Cand{0.0, -1};
+        topk_warp(L);
+        if (lane < k) {
 #pragma unroll
-            for (int t = 0; t < K; ++t) out[t] = L[t].i;
+            for (int t = 0; t < kTopSlots; ++t)
+                if (t == lane) out[t] = L[t].i;
         }
     }
     __syncthreads();
 }
 
 __device__ void block_topk_k(const double *vals, int64_t n, int k, int32_t *out) {
-    if (k == 4)
-        block_topk<4>(vals, n, out);
-    else if (k == 3)
-        block_topk<3>(vals, n, out);
-    else
-        block_topk<1>(vals, n, out);
+    Cand L[kTopSlots];
+#pragma unroll
+    for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) topk_insert(L, Cand{vals[i], (int32_t)i});
+    block_topk_lists(L, k, out);
 }
 
-// numpy pairwise sum of v[0..n) over the host-built split tree
-__device__ double block_pairwise(const double *v, int64_t n, const RunConsts &c, const SumTree &tr) {
-    for (int l = threadIdx.x; l < c.n_leaf; l += blockDim.x) {
-        const int64_t off = tr.leaf_off[l];
-        tr.val[l] = pairwise_leaf(v + off, tr.leaf_off[l + 1] - off);
+// numpy pairwise sum (np.add.reduce, pairwise.c) of v[0..n) over the
+// host-built split tree.  Tree structure and node values live in shared
+// memory (ts).  A leaf (<= 128 elements) is summed by 8 lanes: lane k owns
+// numpy's accumulator r_k (elements k, k+8, ... in order), the eight are
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by xor shuffles, and the
+// tail (n % 8 elements) is added in order; internal nodes follow by height.
+struct TreeSmem {
+    int32_t *leaf_off, *kid, *lvl;
+    double *val;
+};
+
+__device__ double block_pairwise(const double *v, const RunConsts &c, const TreeSmem &ts) {
+    const int lane = threadIdx.x & 31, sub = lane & 7;
+    const int groups = (int)(blockDim.x >> 3);
+    for (int base = (int)(threadIdx.x >> 3) - (lane >> 3); base < c.n_leaf; base += groups) {
+        const int l = base + (lane >> 3);  // warp-uniform trip count: shuffles see all lanes
+        const bool ok = l < c.n_leaf;
+        const int off = ok ? ts.leaf_off[l] : 0;
+        const int len = ok ? ts.leaf_off[l + 1] - off : 0;
+        const double *a = v + off;
+        const int m = len - len % 8;
+        double r = 0.0;
+        if (len >= 8) {
+            r = a[sub];
+            for (int i = 8 + sub; i < m; i += 8) r += a[i];
+        }
+        r += __shfl_xor_sync(0xffffffffu, r, 1);
+        r += __shfl_xor_sync(0xffffffffu, r, 2);
+        r += __shfl_xor_sync(0xffffffffu, r, 4);
+        if (ok && sub == 0) {
+            double res = len >= 8 ? r : 0.0;
+            for (int i = m; i < len; ++i) res += a[i];
+            ts.val[l] = res;
+        }
     }
     __syncthreads();
-    for (int h = 0; h < c.n_levels; ++h) {
-        for (int t = tr.lvl[h] + threadIdx.x; t < tr.lvl[h + 1]; t += blockDim.x)
-            tr.val[c.n_leaf + t] = tr.val[tr.kid[2 * t]] + tr.val[tr.kid[2 * t + 1]];
-        __syncthreads();
+    if (c.n_leaf <= 64) {  // few internal nodes: one warp, warp-level barriers
+        if (threadIdx.x < 32) {
+            for (int h = 0; h < c.n_levels; ++h) {
+                for (int t = ts.lvl[h] + (int)threadIdx.x; t < ts.lvl[h + 1]; t += 32)
+                    ts.val[c.n_leaf + t] = ts.val[ts.kid[2 * t]] + ts.val[ts.kid[2 * t + 1]];
+                __syncwarp();
+            }
+        }
+    } else {
+        for (int h = 0; h < c.n_levels; ++h) {
+            for (int t = ts.lvl[h] + (int)threadIdx.x; t < ts.lvl[h + 1]; t += blockDim.x)
+                ts.val[c.n_leaf + t] = ts.val[ts.kid[2 * t]] + ts.val[ts.kid[2 * t + 1]];
+            __syncthreads();
+        }
     }
-    const double r = tr.val[c.n_leaf > 1 ? 2 * c.n_leaf - 2 : 0];
+    __syncthreads();
+    const double r = ts.val[c.n_leaf > 1 ? 2 * c.n_leaf - 2 : 0];
     __syncthreads();
     return r;
 }
@@ -914,17 +962,22 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, Engine
                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                              int32_t *__restrict__ spare_of) {
     pdl_wait();
+    Cand L[kTopSlots];
+#pragma unroll
+    for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
     for (int64_t i = threadIdx.x; i < c.NP; i += blockDim.x) {
         const double f = cand[i];
-        if (f > fit[i]) {
+        double v = fit[i];
+        if (f > v) {
             const int32_t a = slot_of[i];
             slot_of[i] = spare_of[i];
             spare_of[i] = a;
             fit[i] = f;
+            v = f;
         }
+        topk_insert(L, Cand{v, (int32_t)i});  // the selected value, straight from registers
     }
-    __syncthreads();
-    block_topk_k(fit, c.NP, c.k, st->leaders);
+    block_topk_lists(L, c.k, st->leaders);
 }
 
 __global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, EngineState *__restrict__ st,
@@ -948,53 +1001,54 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
                                                               uint8_t *__restrict__ slot_bin,
                                                               double *__restrict__ scratch, SumTree tr,
                                                               double *__restrict__ trace) {
-    pdl_wait();
     const int64_t n = c.NP;
+    // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
+    // then the pairwise-sum tree (values, leaf offsets, children, levels)
+    extern __shared__ double s_dyn[];
+    const bool on_chip = n <= kStatsSmemMaxNP;
+    double *fv = on_chip ? s_dyn : fit;
+    double *sq = on_chip ? s_dyn + n : scratch;
+    TreeSmem ts;
+    ts.val = s_dyn + (on_chip ? 2 * n : 0);
+    ts.leaf_off = reinterpret_cast<int32_t *>(ts.val + 2 * c.n_leaf);
+    ts.kid = ts.leaf_off + c.n_leaf + 1;
+    ts.lvl = ts.kid + 2 * c.n_leaf;
+    // the tree is the engine's constant: staged before waiting on the predecessor
+    for (int t = threadIdx.x; t <= c.n_leaf; t += blockDim.x) ts.leaf_off[t] = tr.leaf_off[t];
+    for (int t = threadIdx.x; t < 2 * (c.n_leaf - 1); t += blockDim.x) ts.kid[t] = tr.kid[t];
+    for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
+    pdl_wait();
     __shared__ EngineState s_state;
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(st);
         uint32_t *dst = reinterpret_cast<uint32_t *>(&s_state);
         for (int t = threadIdx.x; t < (int)(sizeof(EngineState) / 4); t += blockDim.x) dst[t] = src[t];
     }
-    if (mode != 3) {
-        int32_t lead[kMaxLeaders];
+    int32_t lead[kMaxLeaders];
 #pragma unroll
-        for (int t = 0; t < kMaxLeaders; ++t) lead[t] = (mode != 0 && t < c.k) ? st->leaders[t] : -1;
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int t = 0; t < kMaxLeaders; ++t) lead[t] = (mode == 1 || mode == 2) && t < c.k ? st->leaders[t] : -1;
+    // selection; every thread keeps its elements' final values for the max/min
+    double mx = -INFINITY, mn = INFINITY;
+    int64_t amx = n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double v = fit[i];
+        if (mode != 3) {
             bool is_leader = false;
 #pragma unroll
             for (int t = 0; t < kMaxLeaders; ++t) is_leader |= lead[t] == i;
-            if (is_leader) continue;
             const double f = cand[i];
-            if (mode == 2 || f > fit[i]) {
+            if (!is_leader && (mode == 2 || f > v)) {
                 const int32_t a = slot_of[i];
                 const int32_t b = spare_of[i];
                 slot_of[i] = b;
                 spare_of[i] = a;
                 fit[i] = f;
                 if (mode == 1) slot_bin[b] = 1;
+                v = f;
             }
         }
-        __syncthreads();
-    }
-    // stage the fitness vector (and the squared deviations) in shared memory
-    // when it fits; the pairwise-sum leaves then read on-chip
-    extern __shared__ double s_dyn[];
-    const bool on_chip = n <= kStatsSmemMaxNP;
-    const double *fv = fit;
-    double *sq = scratch;
-    if (on_chip) {
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s_dyn[i] = fit[i];
-        fv = s_dyn;
-        sq = s_dyn + n;
-        __syncthreads();
-    }
-    // max (lowest index on ties) and min
-    double mx = -INFINITY, mn = INFINITY;
-    int64_t amx = n;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double v = fv[i];
-        if (v > mx || (v == mx && i < amx)) {
+        if (on_chip) fv[i] = v;
+        if (v > mx || (v == mx && i < amx)) {  // max, lowest index on ties
             mx = v;
             amx = i;
         }
@@ -1012,35 +1066,36 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     }
     __shared__ double s_mx[kCtaThreads / 32], s_mn[kCtaThreads / 32];
     __shared__ int64_t s_am[kCtaThreads / 32];
-    if ((threadIdx.x & 31) == 0) {
+    const int lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+    if (lane == 0) {
         s_mx[threadIdx.x >> 5] = mx;
         s_mn[threadIdx.x >> 5] = mn;
         s_am[threadIdx.x >> 5] = amx;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-            if (s_mx[w] > mx || (s_mx[w] == mx && s_am[w] < amx)) {
-                mx = s_mx[w];
-                amx = s_am[w];
-            }
-            mn = s_mn[w] < mn ? s_mn[w] : mn;
+    __syncthreads();  // also publishes fv (and, without on-chip staging, fit)
+    mx = lane < nw ? s_mx[lane] : -INFINITY;
+    mn = lane < nw ? s_mn[lane] : INFINITY;
+    amx = lane < nw ? s_am[lane] : n;
+    for (int off = 16; off > 0; off >>= 1) {  // every warp reduces the 32 partials itself
+        const double omx = __shfl_down_sync(0xffffffffu, mx, off);
+        const int64_t oam = __shfl_down_sync(0xffffffffu, amx, off);
+        const double omn = __shfl_down_sync(0xffffffffu, mn, off);
+        if (omx > mx || (omx == mx && oam < amx)) {
+            mx = omx;
+            amx = oam;
         }
-        s_mx[0] = mx;
-        s_mn[0] = mn;
-        s_am[0] = amx;
+        mn = omn < mn ? omn : mn;
     }
-    __syncthreads();
-    mx = s_mx[0];
-    mn = s_mn[0];
-    amx = s_am[0];
-    const double mean = block_pairwise(fv, n, c, tr) / (double)n;
+    mx = __shfl_sync(0xffffffffu, mx, 0);
+    mn = __shfl_sync(0xffffffffu, mn, 0);
+    amx = __shfl_sync(0xffffffffu, amx, 0);
+    const double mean = block_pairwise(fv, c, ts) / (double)n;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = fv[i] - mean;
         sq[i] = d * d;
     }
     __syncthreads();
-    const double var = block_pairwise(sq, n, c, tr) / (double)n;
+    const double var = block_pairwise(sq, c, ts) / (double)n;
     if (threadIdx.x != 0) return;
     // serial tail on the shared-memory copy of the state (fetched at entry);
     // only the fields this kernel owns are written back (g_plan belongs to
@@ -1125,7 +1180,7 @@ __global__ void k_copy_best(RunConsts c, const EngineState *__restrict__ st, con
 __global__ void k_finalize_best(RunConsts c, EngineState *st, const double *fit) {
     // rank_leaders(pop, 1): highest fitness, lowest index on ties
     __shared__ int32_t top[kMaxLeaders];
-    block_topk<1>(fit, c.NP, top);
+    block_topk_k(fit, c.NP, 1, top);
     if (threadIdx.x == 0) {
         st->best_idx = top[0];
         st->best_flag = 1;
@@ -1264,7 +1319,10 @@ struct StageMarks {
 };
 
 static size_t stats_smem_bytes(const RunConsts &c) {
-    return c.NP <= kStatsSmemMaxNP ? (size_t)2 * c.NP * sizeof(double) : 0;
+    const size_t fitv = c.NP <= kStatsSmemMaxNP ? (size_t)2 * c.NP * sizeof(double) : 0;
+    const size_t tree = (size_t)2 * c.n_leaf * sizeof(double) +
+                        (size_t)((c.n_leaf + 1) + 2 * c.n_leaf + (c.n_levels + 1)) * sizeof(int32_t);
+    return fitv + ((tree + 15) & ~(size_t)15);
 }
 
 static int launch_select_stats(Engine *e, int mode, cudaStream_t s) {
@@ -1609,12 +1667,6 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     c.conv_window = P->conv_window;
     c.adaptive = P->adaptive_branches;
     c.gwo_a0 = P->gwo_a0;
-    if (cudaFuncSetAttribute(k_select_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)std::max<size_t>(stats_smem_bytes(c), 1)) != cudaSuccess) {
-        set_error("cudaFuncSetAttribute(k_select_stats) failed");
-        engine_free(e);
-        return QPM_ERR_CUDA;
-    }
     {
         int dev = 0, sms = 148, occ_a = 1;
         cudaGetDevice(&dev);
@@ -1633,6 +1685,23 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     HostTree ht = build_tree(c.NP);
     c.n_leaf = (int32_t)ht.leaf_off.size() - 1;
     c.n_levels = (int32_t)ht.lvl.size() - 1;
+    {
+        // the attribute is per function and process-wide: raise it to the
+        // device's opt-in maximum once, whatever the engine's size
+        int dev = 0, max_optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k_select_stats);
+        const size_t need = stats_smem_bytes(c) + fa.sharedSizeBytes;
+        if ((size_t)max_optin < need ||
+            cudaFuncSetAttribute(k_select_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
+            set_error("k_select_stats needs %zu bytes of shared memory (device: %d)", need, max_optin);
+            engine_free(e);
+            return QPM_ERR_CUDA;
+        }
+    }
 
     const int64_t NP = c.NP;
     int rc = QPM_OK;
@@ -1687,6 +1756,8 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     }
     c.plus_dyadic = (c.k == 4 && P->discreteness_factor == 1.0) ? 1 : 0;
     c.m4 = 4;
+    c.m32 = 32;
+    c.m2 = 2;
     hs.g = 0;
     hs.g_plan = 1;
     hs.F = P->f_max;
