@@ -54,7 +54,7 @@ constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
 constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
 constexpr int kDeChunk = 4096;
 #ifndef QPM_DE_MINB
-#define QPM_DE_MINB 3  // k_de_trial CTAs per SM the register budget is sized for
+#define QPM_DE_MINB 4  // k_de_trial CTAs per SM the register budget is sized for
 #endif      // genes per DE-trial CTA (amortizes the per-row setup)
 constexpr int64_t kStatsSmemMaxNP = 12288;  // 2 x NP doubles of dynamic smem (<= 192 KB)
 
@@ -384,56 +384,66 @@ __device__ __forceinline__ void store_planes(uint32_t *dst_word, uint32_t code, 
     }
 }
 
-// the wolf planes of generation g_plan for this rank's rows on the side
-// stream (QPM_WOLF=planner; the default draws them inside k_de_trial)
+// The wolf planes of row genes [jc, jc + len) (len a multiple of
+// 2 * kRowThreads) by one CTA: each thread draws two genes at a time
+// (independent chains), warps ballot the plane words.
 template <int K, int PH>
-__device__ __forceinline__ void plan_wolf_items(const RunConsts &c, const PlanArgs &a, const GenThr &t, int64_t b) {
+__device__ __forceinline__ void wolf_chunk(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p_wolf,
+                                           uint32_t *prow, int jc, int len) {
     const uint32_t D = (uint32_t)c.D;
     const int lane = threadIdx.x & 31;
-    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
-    const int64_t items = a.n_rows * nchunk;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        const int64_t i = a.row_lo + item / nchunk;
-        const int jc = (int)(item % nchunk) * kGenesPerBlock;
-        const uint64_t key = a.keys[b * c.NP + i];
-        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + D;  // m + 1 + D + j, plus one
-        uint32_t *prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
+#pragma unroll 1
+    for (int it = 0; it < len; it += 2 * kRowThreads) {
+        int j[2];
+        uint32_t code[2];
+        bool tie[2] = {false, false};
 #pragma unroll
-        for (int it = 0; it < kGenesPerThread; it += 2) {
-            int j[2];
-            uint32_t code[2];
-            bool tie[2] = {false, false};
+        for (int h = 0; h < 2; ++h) {
+            j[h] = jc + it + h * kRowThreads + (int)threadIdx.x;
+            code[h] = wolf_code<K, PH, false>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
+            if (j[h] >= (int)D) code[h] = 0u, tie[h] = false;
+        }
+        if (__any_sync(0xffffffffu, tie[0] || tie[1])) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                j[h] = jc + (it + h) * kRowThreads + (int)threadIdx.x;
-                code[h] = wolf_code<K, PH, false>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
-                if (j[h] >= (int)D) code[h] = 0u, tie[h] = false;
-            }
-            if (__any_sync(0xffffffffu, tie[0] || tie[1])) {
+            for (int h = 0; h < 2; ++h)
+                if (tie[h]) code[h] = wolf_code<K, PH, true>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
+        }
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
-                    if (tie[h]) code[h] = wolf_code<K, PH, true>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (j[h] - lane >= (int)c.Dp) break;  // warp-uniform
-                store_planes<PH != kLate>(prow + ((j[h] - lane) >> 5) * kPlanes, code[h], lane, 0);
-            }
+        for (int h = 0; h < 2; ++h) {
+            if (j[h] - lane >= (int)c.Dp) break;  // warp-uniform
+            store_planes<PH != kLate>(prow + ((j[h] - lane) >> 5) * kPlanes, code[h], lane, 0);
         }
     }
 }
 
 template <int K>
+__device__ __forceinline__ void wolf_chunk_phase(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p_wolf,
+                                                 uint32_t *prow, int jc, int len) {
+    if (!t.early)
+        wolf_chunk<K, kLate>(c, t, key, p_wolf, prow, jc, len);
+    else if (K == 4 && c.plus_dyadic)
+        wolf_chunk<K, kEarlyDyadic>(c, t, key, p_wolf, prow, jc, len);
+    else
+        wolf_chunk<K, kEarly>(c, t, key, p_wolf, prow, jc, len);
+}
+
+// the wolf planes of generation g_plan for this rank's rows on the side
+// stream (QPM_WOLF=planner)
+template <int K>
 __global__ void __launch_bounds__(kRowThreads) k_plan_wolf(RunConsts c, PlanArgs a) {
     const int64_t g = a.st->g_plan;
     if (g > c.G) return;
+    const int64_t b = g & 1;
     const GenThr t = a.gthr[g];
-    if (!t.early)
-        plan_wolf_items<K, kLate>(c, a, t, g & 1);
-    else if (K == 4 && c.plus_dyadic)
-        plan_wolf_items<K, kEarlyDyadic>(c, a, t, g & 1);
-    else
-        plan_wolf_items<K, kEarly>(c, a, t, g & 1);
+    const int nchunk = (int)((c.Dp + kGenesPerBlock - 1) / kGenesPerBlock);
+    const int64_t items = a.n_rows * nchunk;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int64_t i = a.row_lo + item / nchunk;
+        const int jc = (int)(item % nchunk) * kGenesPerBlock;
+        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
+        wolf_chunk_phase<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
+                            kGenesPerBlock);
+    }
 }
 
 __global__ void k_plan_bump(EngineState *st) { st->g_plan += 1; }
@@ -524,8 +534,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     for (int bt = 0; bt < kBatches; ++bt) {
         const int jb = jc + bt * kSpan * kSteps + warp * 64;
         if (!FULL && jb >= (int)c.Dp) break;
-        // mask bits first, then every genome load of the batch, then the wolf
-        // draws while the loads are in flight, then the math
+        // mask bits, then every genome load of the batch, the math and the
+        // stores, then the wolf draws (other warps' loads are in flight)
         uint32_t mb[kSteps];
         bool tie = false;
 #pragma unroll
@@ -580,7 +590,28 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 }
             }
         }
-        if (K > 0) {
+#pragma unroll
+        for (int st = 0; st < kSteps; ++st) {
+            const int j64 = jb + st * kSpan;  // this warp's 64-gene span
+            if (!FULL && j64 >= (int)c.Dp) break;
+            bool neg[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int j = j64 + lane + 32 * q;
+                neg[q] = false;
+                if (FULL || j < D) {
+                    const double v = ((mb[st] >> q) & 1u) ? p1[st][q] + F * (p2[st][q] - p3[st][q]) : y[st][q];
+                    out[j] = v;
+                    neg[q] = !(v >= 0.0);
+                } else if (j < (int)c.Dp) {
+                    out[j] = 0.0;
+                }
+            }
+            const uint32_t w0 = __ballot_sync(0xffffffffu, neg[0]);
+            const uint32_t w1 = __ballot_sync(0xffffffffu, neg[1]);
+            if (lane < 2) bout[(j64 >> 5) + lane] = lane ? w1 : w0;
+        }
+        if (K > 0) {  // after the stores: the load registers are free again
             uint32_t code[kSteps][2];
             bool wtie = false;
 #pragma unroll
@@ -614,27 +645,6 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 for (int q = 0; q < 2; ++q)
                     store_planes<PH != kLate>(prow + ((j64 >> 5) + q) * kPlanes, code[st][q], lane, q);
             }
-        }
-#pragma unroll
-        for (int st = 0; st < kSteps; ++st) {
-            const int j64 = jb + st * kSpan;  // this warp's 64-gene span
-            if (!FULL && j64 >= (int)c.Dp) break;
-            bool neg[2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int j = j64 + lane + 32 * q;
-                neg[q] = false;
-                if (FULL || j < D) {
-                    const double v = ((mb[st] >> q) & 1u) ? p1[st][q] + F * (p2[st][q] - p3[st][q]) : y[st][q];
-                    out[j] = v;
-                    neg[q] = !(v >= 0.0);
-                } else if (j < (int)c.Dp) {
-                    out[j] = 0.0;
-                }
-            }
-            const uint32_t w0 = __ballot_sync(0xffffffffu, neg[0]);
-            const uint32_t w1 = __ballot_sync(0xffffffffu, neg[1]);
-            if (lane < 2) bout[(j64 >> 5) + lane] = lane ? w1 : w0;
         }
     }
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[out_slot] = 0;
@@ -680,6 +690,33 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts
         de_trial_dispatch<K, kEarlyDyadic>(c, a, b, i, jc, F, t, bin);
     else
         de_trial_dispatch<K, kEarly>(c, a, b, i, jc, F, t, bin);
+}
+
+// Horizontal fusion (QPM_WOLF=mixed): even CTAs run the trial
+// of a (row, kDeChunk) item (HBM-bound), odd CTAs draw the same item's wolf
+// planes (integer-ALU-bound).  The block scheduler keeps both kinds resident
+// on every SM, so the draws fill the issue slots the trial's loads leave idle.
+template <int K>
+__global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(RunConsts c, TrialArgs a) {
+    pdl_wait();
+    const int64_t g = a.st->g;
+    const int64_t b = g & 1;
+    const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
+    const int64_t item = blockIdx.x >> 1;
+    const int64_t i = a.row_lo + item / nchunk;
+    const int jc = (int)(item % nchunk) * kDeChunk;
+    const GenThr t = a.gthr[g];
+    if (blockIdx.x & 1) {
+        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
+        wolf_chunk_phase<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
+                            kDeChunk);
+        return;
+    }
+    const double F = a.st->F;
+    const int4 pk = a.picks[b * c.NP + i];
+    const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
+                     a.slot_bin[a.slot_of[pk.z]];
+    de_trial_dispatch<0, kLate>(c, a, b, i, jc, F, t, bin);
 }
 
 // multi-GPU: all-gathered wolf candidates of accepted (non-leader) rows into
@@ -808,10 +845,11 @@ struct Cand {
     double v;
     int32_t i;
 };
+// (-value, index) order; index -1 marks an empty slot (worse than anything).
+// Bitwise, not short-circuit: straight-line code for the merge networks.
 __device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
-    if (a.i < 0) return false;
-    if (b.i < 0) return true;
-    return a.v > b.v || (a.v == b.v && a.i < b.i);
+    const bool gt = a.v > b.v, eq = a.v == b.v, lo = a.i < b.i;
+    return (a.i >= 0) & ((b.i < 0) | gt | (eq & lo));
 }
 
 // top-K by (-value, index) (parexec.reduce_best), whole CTA.  (-value,
@@ -824,11 +862,12 @@ __device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
 constexpr int kTopSlots = 4;
 
 __device__ __forceinline__ void cswap(Cand &a, Cand &b) {  // a := better of the two
-    if (better(b, a)) {
-        const Cand t = a;
-        a = b;
-        b = t;
-    }
+    const bool sw = better(b, a);
+    const Cand x = a, y = b;
+    a.v = sw ? y.v : x.v;
+    a.i = sw ? y.i : x.i;
+    b.v = sw ? x.v : y.v;
+    b.i = sw ? x.i : y.i;
 }
 
 __device__ __forceinline__ void topk_insert(Cand (&L)[kTopSlots], Cand e) {
@@ -847,8 +886,12 @@ __device__ __forceinline__ void topk_merge_xor(Cand (&L)[kTopSlots], int off) {
     // the better of L[t] and o[3-t] for every t is the top-4 of the union,
     // as a bitonic sequence; two compare-swap stages sort it
 #pragma unroll
-    for (int t = 0; t < kTopSlots; ++t)
-        if (better(o[kTopSlots - 1 - t], L[t])) L[t] = o[kTopSlots - 1 - t];
+    for (int t = 0; t < kTopSlots; ++t) {
+        const Cand &x = o[kTopSlots - 1 - t];
+        const bool take = better(x, L[t]);
+        L[t].v = take ? x.v : L[t].v;
+        L[t].i = take ? x.i : L[t].i;
+    }
     cswap(L[0], L[2]);
     cswap(L[1], L[3]);
     cswap(L[0], L[1]);
@@ -1225,6 +1268,7 @@ struct Engine {
     int plan_grid = 148;       // k_plan_wolf CTAs (QPM_PLAN_CTAS)
     bool plan_after_trial = false;  // fork the planner after k_de_trial (QPM_PLAN_FORK=trial)
     bool wolf_in_planner = false;   // wolf planes on the side stream (QPM_WOLF=planner)
+    bool wolf_mixed = false;        // wolf planes in separate CTAs of the trial kernel (QPM_WOLF=mixed)
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
     int64_t g_done = 0;
     bool initialized = false;
@@ -1503,11 +1547,18 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         };
         if (!e->plan_after_trial && (rc = fork())) return rc;
         mark("de_trial");
-        auto kern = (!hybrid || e->wolf_in_planner) ? k_de_trial<0> : (c.k == 4 ? k_de_trial<4> : k_de_trial<3>);
         // the generation's first kernel is never launched programmatically: a
         // graph's root node would otherwise overlap the previous replay's
         // tail, including its planner branch
-        QPM_CUDA_TRY(launch_k(false, kern, dim3((unsigned)(n_own * de_chunks)), dim3(kRowThreads), 0, s, c, own));
+        const unsigned items = (unsigned)(n_own * de_chunks);
+        if (!hybrid || e->wolf_in_planner)
+            QPM_CUDA_TRY(launch_k(false, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, own));
+        else if (e->wolf_mixed)
+            QPM_CUDA_TRY(launch_k(false, c.k == 4 ? k_de_trial_mixed<4> : k_de_trial_mixed<3>, dim3(2 * items),
+                                  dim3(kRowThreads), 0, s, c, own));
+        else
+            QPM_CUDA_TRY(launch_k(false, c.k == 4 ? k_de_trial<4> : k_de_trial<3>, dim3(items), dim3(kRowThreads), 0,
+                                  s, c, own));
         QPM_LAUNCH_CHECK();
         *n += 1;
         if (e->plan_after_trial && (rc = fork())) return rc;
@@ -1679,7 +1730,10 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         e->plan_grid = sms * 2;
         if (const char *v = getenv("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
         if (const char *v = getenv("QPM_PLAN_FORK")) e->plan_after_trial = strcmp(v, "trial") == 0;
-        if (const char *v = getenv("QPM_WOLF")) e->wolf_in_planner = strcmp(v, "planner") == 0;
+        if (const char *v = getenv("QPM_WOLF")) {
+            e->wolf_in_planner = strcmp(v, "planner") == 0;
+            e->wolf_mixed = strcmp(v, "mixed") == 0;
+        }
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
     }
     HostTree ht = build_tree(c.NP);

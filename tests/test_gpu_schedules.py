@@ -1,7 +1,8 @@
 """GPU: the engine's scheduling knobs change where and when work runs, never
-the result.  Every combination of wolf-plane placement (inside k_de_trial or
-on the planner stream), planner fork point, planner CTA count and
-programmatic dependent launch must reproduce the default trace bit for bit.
+the result.  Every combination of wolf-plane placement (separate CTAs of the
+trial kernel, inside each trial thread, or on the planner stream), planner
+fork point, planner CTA count and programmatic dependent launch must
+reproduce the default trace bit for bit.
 """
 
 import numpy as np
@@ -38,6 +39,7 @@ def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders
 
 VARIANTS = [
     {"QPM_PDL": "0"},
+    {"QPM_WOLF": "mixed"},
     {"QPM_WOLF": "planner"},
     {"QPM_WOLF": "planner", "QPM_PDL": "0"},
     {"QPM_WOLF": "planner", "QPM_PLAN_FORK": "trial"},
