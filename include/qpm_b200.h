@@ -77,6 +77,12 @@ int qpm_version(void);
 /* number of SMs and compute capability of the current device */
 int qpm_device_info(int *sm_count, int *cc_major, int *cc_minor);
 
+/* Engines return their device buffers to a process-wide cache on destroy so
+ * the next run of the same shape skips cudaMalloc/cudaFree; this frees the
+ * idle cached blocks (no engine may be mid-destruction on another thread).
+ * No reference counterpart (the reference allocates numpy arrays per run). */
+int qpm_release_cached_memory(void);
+
 /* ------------------------------------------------------------------ RNG */
 uint64_t qpm_fold_key(int64_t seed, int npath, const int64_t *path);
 int qpm_uniform_fill(uint64_t key, uint64_t start, int64_t n, double *out_dev, void *stream);

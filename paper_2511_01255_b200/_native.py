@@ -19,7 +19,7 @@ SCHED_COLS = 8
 
 # every symbol include/qpm_b200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
-    "qpm_last_error", "qpm_version", "qpm_device_info", "qpm_fold_key", "qpm_uniform_fill",
+    "qpm_last_error", "qpm_version", "qpm_device_info", "qpm_release_cached_memory", "qpm_fold_key", "qpm_uniform_fill",
     "qpm_problem_create", "qpm_problem_destroy", "qpm_problem_row_words", "qpm_pack_signs",
     "qpm_fitness_bits", "qpm_evaluate_block_host", "qpm_sum_block_host", "qpm_reduce_best",
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
@@ -84,6 +84,7 @@ def lib():
     sig = {
         "qpm_last_error": (ctypes.c_char_p, []),
         "qpm_version": (I32, []),
+        "qpm_release_cached_memory": (I32, []),
         "qpm_device_info": (I32, [P, P, P]),
         "qpm_fold_key": (ctypes.c_uint64, [I64, I32, P]),
         "qpm_uniform_fill": (I32, [ctypes.c_uint64, ctypes.c_uint64, I64, P, P]),

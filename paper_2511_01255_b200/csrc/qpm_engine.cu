@@ -1274,14 +1274,18 @@ struct Engine {
     bool initialized = false;
     bool owns_stream = false;
     int64_t device_bytes = 0;
-    std::vector<void *> allocs;
+    std::vector<std::pair<void *, size_t>> allocs;
 };
 
 template <typename T>
 static int dalloc(Engine *e, T **p, size_t count) {
-    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    QPM_CUDA_TRY(cudaMalloc((void **)p, bytes));
-    e->allocs.push_back((void *)*p);
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    *p = (T *)dev_cache_alloc(bytes);
+    if (!*p) {
+        set_error("out of device memory (%zu bytes)", bytes);
+        return QPM_ERR_CUDA;
+    }
+    e->allocs.emplace_back((void *)*p, bytes);
     e->device_bytes += (int64_t)bytes;
     return QPM_OK;
 }
@@ -1619,10 +1623,9 @@ static int enqueue_generation(Engine *e, int *launches, StageMarks *pm = nullptr
 }
 
 static void engine_free(Engine *e) {
-    if (e->owns_stream && e->stream) {
-        cudaStreamSynchronize(e->stream);
-        cudaStreamDestroy(e->stream);
-    }
+    // the buffers go back to the block cache: nothing queued may still use them
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    if (e->owns_stream && e->stream) cudaStreamDestroy(e->stream);
     if (e->side) {
         cudaStreamSynchronize(e->side);
         cudaStreamDestroy(e->side);
@@ -1632,7 +1635,7 @@ static void engine_free(Engine *e) {
     if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
-    for (void *p : e->allocs) cudaFree(p);
+    for (auto &pb : e->allocs) dev_cache_release(pb.first, pb.second);
     scratch_free(&e->fs);
     delete e;
 }

@@ -36,6 +36,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "qpm_common.cuh"
@@ -53,6 +54,67 @@ void set_error(const char *fmt, ...) {
     vsnprintf(buf, sizeof(buf), fmt, ap);
     va_end(ap);
     g_last_error = buf;
+}
+
+// ------------------------------------------------------------ device block cache
+namespace {
+struct CachedBlock {
+    int device;
+    size_t bytes;
+    void *ptr;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+size_t g_cache_bytes = 0;
+constexpr size_t kCacheCap = (size_t)16 << 30;  // keep at most 16 GB idle
+size_t cache_round(size_t b) { return (std::max<size_t>(b, 16) + 255) & ~(size_t)255; }
+}  // namespace
+
+void *dev_cache_alloc(size_t bytes) {
+    bytes = cache_round(bytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t k = 0; k < g_cache.size(); ++k) {
+            if (g_cache[k].device == dev && g_cache[k].bytes == bytes) {
+                void *p = g_cache[k].ptr;
+                g_cache[k] = g_cache.back();
+                g_cache.pop_back();
+                g_cache_bytes -= bytes;
+                return p;
+            }
+        }
+    }
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        dev_cache_trim();  // retry once with the idle blocks returned
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    }
+    return p;
+}
+
+// the caller guarantees no queued work still uses p
+void dev_cache_release(void *p, size_t bytes) {
+    if (!p) return;
+    bytes = cache_round(bytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (g_cache_bytes + bytes > kCacheCap) {
+        cudaFree(p);
+        return;
+    }
+    g_cache.push_back({dev, bytes, p});
+    g_cache_bytes += bytes;
+}
+
+void dev_cache_trim() {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (const CachedBlock &b : g_cache) cudaFree(b.ptr);
+    g_cache.clear();
+    g_cache_bytes = 0;
 }
 
 // ------------------------------------------------------------ small kernels
@@ -444,16 +506,24 @@ int scratch_reserve(const Problem *p, FitScratch *fs, int64_t rows) {
     scratch_free(fs);
     const int64_t S = std::max<int64_t>(p->S, 1);
     const size_t bytes = (size_t)p->n_wl * rows * S * kPartDoubles * sizeof(double);
-    QPM_CUDA_TRY(cudaMalloc(&fs->part, bytes));
-    QPM_CUDA_TRY(cudaMalloc(&fs->gains, (size_t)rows * p->n_wl * sizeof(double)));
+    const size_t gbytes = (size_t)rows * p->n_wl * sizeof(double);
+    fs->part = (double *)dev_cache_alloc(bytes);
+    fs->gains = (double *)dev_cache_alloc(gbytes);
+    if (!fs->part || !fs->gains) {
+        scratch_free(fs);
+        set_error("out of device memory for the fitness scratch (%zu bytes)", bytes + gbytes);
+        return QPM_ERR_CUDA;
+    }
     fs->rows = rows;
-    fs->bytes = (int64_t)bytes + rows * p->n_wl * 8;
+    fs->bytes = (int64_t)(bytes + gbytes);
+    fs->part_bytes = bytes;
+    fs->gains_bytes = gbytes;
     return QPM_OK;
 }
 
 void scratch_free(FitScratch *fs) {
-    cudaFree(fs->part);
-    cudaFree(fs->gains);
+    dev_cache_release(fs->part, fs->part_bytes);
+    dev_cache_release(fs->gains, fs->gains_bytes);
     *fs = FitScratch{};
 }
 
@@ -543,6 +613,11 @@ extern "C" {
 const char *qpm_last_error(void) { return g_last_error.c_str(); }
 
 int qpm_version(void) { return 10000; }
+
+int qpm_release_cached_memory(void) {
+    dev_cache_trim();
+    return QPM_OK;
+}
 
 int qpm_device_info(int *sm_count, int *cc_major, int *cc_minor) {
     int dev = 0;

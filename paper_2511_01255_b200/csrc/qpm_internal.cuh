@@ -82,7 +82,16 @@ struct FitScratch {
     double *gains = nullptr;
     int64_t rows = 0;
     int64_t bytes = 0;
+    size_t part_bytes = 0, gains_bytes = 0;
 };
+// Process-wide cache of device blocks (exact-size reuse): engines created
+// and destroyed back to back (one run_hybrid call after another) skip
+// cudaMalloc / cudaFree, whose implicit device synchronisation and page
+// mapping otherwise cost tens of milliseconds per run.
+void *dev_cache_alloc(size_t bytes);
+void dev_cache_release(void *p, size_t bytes);
+void dev_cache_trim();
+
 int scratch_reserve(const Problem *p, FitScratch *fs, int64_t rows);
 void scratch_free(FitScratch *fs);
 // launch the fitness of `rows` bit rows (row_index may be null) into out
