@@ -27,6 +27,8 @@
  *   qpm_pack_signs                  -> Individual.from_genome projection
  *                                      (optimizer.py:52-56), bit-packed
  *   qpm_reduce_best                 -> parexec.reduce_best (parexec.py:123-154)
+ *   qpm_brute_force                 -> bench.brute_force_oracle (bench.py:179-209)
+ *                                      with bench.lexicographic_signs (:169-176)
  *   qpm_engine_*                    -> optimizer.run_hybrid / run_de / run_gwo
  *                                      (optimizer.py:400-616) including
  *                                      de_mutate/de_crossover/de_select,
@@ -120,6 +122,15 @@ int qpm_sum_block_host(qpm_problem *p, int wl, const int8_t *signs, int64_t rows
 /* -------------------------------------------------------------- leaders */
 /* top-k indices by (-value, index) of values_dev[n]; idx_out_dev int32 [k]; k <= 64 */
 int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out_dev, void *stream);
+
+/* ------------------------------------------------------ exhaustive search */
+/* Global optimum over all 2^n sign patterns of a problem with D = n (n <= 63):
+ * pattern `index` has sign j = -1 iff bit n-1-j of index is set (+1 sorts
+ * first), patterns are generated on the device chunk_rows at a time, scored
+ * with `mode` and reduced; ties go to the lowest index.  Returns the index
+ * and its fitness.  Synchronous on `stream`. */
+int qpm_brute_force(qpm_problem *p, int n, int mode, int64_t chunk_rows, int64_t *best_index, double *best_fit,
+                    void *stream);
 
 /* --------------------------------------------------------------- engine */
 typedef struct {

@@ -41,6 +41,8 @@ from .optimizer import (
     run_hybrid,
     schedule_table,
 )
+from .search import brute_force_oracle, lexicographic_signs
+from .trials import ComparisonReport, RunStatistics, TrialRecord, compare_algorithms, run_trials
 from .parexec import BatchEvaluationError, BatchJob, TimingReport, evaluate_batch, reduce_best, time_run
 from .tables import (
     SELLMEIER_SETS,

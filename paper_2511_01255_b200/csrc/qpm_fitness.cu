@@ -138,6 +138,18 @@ __global__ void k_pack_signs(const int8_t *__restrict__ signs, int64_t rows, int
     if (lane == 0) bits[r * W + w] = word;
 }
 
+// bit rows of patterns start .. start+rows-1 (bench.lexicographic_signs:
+// sign j = -1 iff bit n-1-j of the index): the low n bits reversed
+__global__ void k_lex_bits(uint64_t start, int64_t rows, int n, int64_t W, uint32_t *__restrict__ bits) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= rows) return;
+    const uint64_t rev = __brevll(start + (uint64_t)t) >> (64 - n);
+    uint32_t *o = bits + t * W;
+    o[0] = (uint32_t)rev;
+    if (W > 1) o[1] = (uint32_t)(rev >> 32);
+    for (int64_t w = 2; w < W; ++w) o[w] = 0u;
+}
+
 // quad tables: entry rel (bit k-1 set <=> s_k != s_0) of B, E, I for quad q
 // (the s_0 = +1 values; the scan flips B and E by s_0)
 __global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__restrict__ b, int64_t D,
@@ -763,6 +775,55 @@ int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, d
     QPM_CUDA_TRY(cudaMemcpyAsync(out, p.hp_out, (size_t)rows * sizeof(double), cudaMemcpyDeviceToHost, p.hp_stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
     return QPM_OK;
+}
+
+int qpm_brute_force(qpm_problem *h, int n, int mode, int64_t chunk_rows, int64_t *best_index, double *best_fit,
+                    void *stream) {
+    QPM_ARG_CHECK(h && best_index && best_fit, "problem, outputs");
+    Problem &p = h->p;
+    QPM_ARG_CHECK(n >= 1 && n <= 63, "n in [1, 63]");
+    QPM_ARG_CHECK(n == p.D, "n must equal the problem's domain count");
+    QPM_ARG_CHECK(chunk_rows >= 1, "chunk_rows >= 1");
+    const cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t total = 1ULL << n;
+    const int64_t chunk = (int64_t)std::min<uint64_t>(total, (uint64_t)chunk_rows);
+    int rc = problem_reserve(&p, chunk);
+    if (rc) return rc;
+    const size_t bits_bytes = (size_t)chunk * p.W * sizeof(uint32_t);
+    uint32_t *bits = (uint32_t *)dev_cache_alloc(bits_bytes);
+    double *vals = (double *)dev_cache_alloc((size_t)chunk * sizeof(double));
+    int32_t *idx = (int32_t *)dev_cache_alloc(sizeof(int32_t) * 4);
+    auto done = [&](int code) {
+        if (s) cudaStreamSynchronize(s); else cudaDeviceSynchronize();
+        dev_cache_release(bits, bits_bytes);
+        dev_cache_release(vals, (size_t)chunk * sizeof(double));
+        dev_cache_release(idx, sizeof(int32_t) * 4);
+        return code;
+    };
+    if (!bits || !vals || !idx) return done((set_error("out of device memory"), QPM_ERR_CUDA));
+    double best = -INFINITY;
+    int64_t best_i = -1;
+    for (uint64_t start = 0; start < total; start += (uint64_t)chunk) {
+        const int64_t rows = (int64_t)std::min<uint64_t>((uint64_t)chunk, total - start);
+        k_lex_bits<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(start, rows, n, p.W, bits);
+        if (cudaGetLastError() != cudaSuccess) return done((set_error("k_lex_bits launch"), QPM_ERR_CUDA));
+        if ((rc = launch_fitness(&p, p.own, bits, p.W, nullptr, rows, vals, mode, s, nullptr))) return done(rc);
+        if ((rc = launch_reduce_best(vals, rows, 1, idx, s))) return done(rc);
+        int32_t li = 0;
+        double lv = 0.0;
+        if (cudaMemcpyAsync(&li, idx, sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess ||
+            cudaMemcpyAsync(&lv, vals + li, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return done((set_error("brute force read-back"), QPM_ERR_CUDA));
+        if (lv > best || best_i < 0) {  // strict: an earlier chunk keeps ties (bench.py:205-207)
+            best = lv;
+            best_i = (int64_t)start + li;
+        }
+    }
+    *best_index = best_i;
+    *best_fit = best;
+    return done(QPM_OK);
 }
 
 int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows, double *out) {

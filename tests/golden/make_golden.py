@@ -380,10 +380,45 @@ def gen_runs():
     save("runs.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+# bench.py: brute_force_oracle (exhaustive optimum, lexicographic tie-break)
+# ---------------------------------------------------------------------------
+
+def search_cases():
+    disp = default_dispersion(25.0)
+    mt = MismatchTable({1404.0: PhaseMismatchPair(0.3, 0.7)})
+    return [
+        ("thg_toy10", ObjectiveSpec("single_thg", (1404.0,)), mt, 1.0, 10),
+        ("thg_c1_12", ObjectiveSpec("single_thg", (1404.0,)), disp, 1.0, 12),
+        ("shg_9", ObjectiveSpec("single_shg", (1404.0,)), disp, 2.0, 9),
+        ("multi_thg2_11", ObjectiveSpec("multi_thg", (1404.0, 1650.0)), disp, 3.0, 11),
+        ("thg_raw_7", ObjectiveSpec("single_thg", (1404.0,), normalization="raw"), mt, 1.0, 7),
+        ("thg_1", ObjectiveSpec("single_thg", (1404.0,)), mt, 1.0, 1),
+    ]
+
+
+def gen_search():
+    out = {}
+    names = []
+    for name, spec, provider, t, n in search_cases():
+        obj = make_objective(spec, provider, t, n)
+        signs, fit = bench.brute_force_oracle(obj, n)
+        index = int(sum(int(s < 0) << (n - 1 - j) for j, s in enumerate(signs)))
+        assert np.array_equal(bench.lexicographic_signs(index, n), signs)
+        out[f"{name}__spec"] = np.array(json.dumps(spec_record(spec, provider, t, n)))
+        out[f"{name}__index"] = np.array(index)
+        out[f"{name}__fit"] = np.array(fit)
+        names.append(name)
+        print(f"  {name}: index={index} fit={fit!r}")
+    out["names"] = np.array(json.dumps(names))
+    out["meta"] = np.array("bench.brute_force_oracle(make_objective(...), n): optimum index and fitness")
+    save("search.npz", **out)
+
+
 if __name__ == "__main__":
     print("qpmdesign", qpmdesign.__version__, "backend", _kernels.backend(), "numpy", np.__version__)
-    gen_rng()
-    gen_tables()
-    gen_fitness()
-    gen_operators()
-    gen_runs()
+    only = sys.argv[1:]
+    for name, fn in (("rng", gen_rng), ("tables", gen_tables), ("fitness", gen_fitness),
+                     ("operators", gen_operators), ("runs", gen_runs), ("search", gen_search)):
+        if not only or name in only:
+            fn()
