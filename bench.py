@@ -213,7 +213,18 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
         peak = peaks.get("hbm_gbs", 6650.0)
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
-                "algorithmic_unit": f"{DE_BYTES_PER_GENE:.3f} B per gene (CR={CR}) x NP*D"}
+                "algorithmic_unit": f"{DE_BYTES_PER_GENE:.3f} B per gene (CR={CR}) x NP*D",
+                "note": "k_de_trial also draws the generation's crossover mask and wolf planes (4 splitmix64 "
+                        "draws per gene); it is integer-issue bound, see int_issue (ncu, "
+                        "profiles/r01/ncu_summary_r01_final.txt)"}
+        summ = os.path.join(ROOT, "profiles", "r01", "ncu_summary_r01_final.txt")
+        if os.path.exists(summ):
+            for line in open(summ):
+                if line.startswith("k_de_trial"):
+                    f = line.split()
+                    roof["int_issue"] = {"issue_active_pct": float(f[-4]), "alu_pipe_pct": float(f[5]),
+                                         "fma_pipe_pct": float(f[6]), "warp_instr_per_launch": float(f[4]) * 1e6,
+                                         "source": "ncu --set full, C2 late generation"}
     else:
         nbytes = NP * D * 8
         achieved = nbytes / (ms * 1e-3) / 1e9
