@@ -53,6 +53,7 @@ constexpr int kGenesPerThread = 4;  // genes per thread (strided by kRowThreads)
 constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
 constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
 constexpr int kDeChunk = 4096;
+constexpr int kApplyThreads = 128;  // k_gwo_apply: 32-gene words per CTA
 #ifndef QPM_DE_MINB
 #define QPM_DE_MINB 4  // k_de_trial CTAs per SM the register budget is sized for
 #endif      // genes per DE-trial CTA (amortizes the per-row setup)
@@ -350,7 +351,9 @@ __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &
     }
     const uint32_t soc_code = 1u | (pick << 1);
     const bool f2 = draw_lt<EXACT>(c, EARLY ? t.dist : t.flip, x2, h2, tie);
-    if (!EARLY && K == 3) return soc ? soc_code : (f2 ? 2u : 0u);  // majority of 3 never ties: no state draw
+    // late generations: a 3-leader majority never ties, and a 4-leader tie is
+    // rare, so the state draw is left to k_gwo_apply, which knows the leaders
+    if (!EARLY) return soc ? soc_code : (f2 ? 2u : 0u);
     const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c);
     const uint32_t h3 = mix_hi2(x3);
     const uint32_t st = (h3 >> 31) ^ 1u;  // u < 0.5
@@ -505,24 +508,55 @@ struct TrialArgs {
 // the same pass draws the row's wolf planes for this generation (three
 // draws per gene): the trial is HBM-bound (~30 B per gene) and the integer
 // work of the draws runs while the genome loads are in flight.
+// Per-row operands of a trial CTA, resolved once by thread 0 and shared
+// through shared memory (the slot lookups and pointer arithmetic would
+// otherwise be repeated by all eight warps).
+struct TrialRow {
+    RowRef xi, x1, x2, x3;
+    double *out;
+    uint32_t *bout, *prow;
+    uint64_t key;
+    int64_t out_slot;
+    double F;
+    GenThr t;
+    uint32_t p_mask;
+    int jr;
+    int bin;  // a source row is a +/-1 (bits-only) slot
+};
+
+__device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialArgs &a, int64_t g, int64_t i,
+                                                TrialRow &r) {
+    const int64_t b = g & 1;
+    const int4 pk = a.picks[b * c.NP + i];
+    r.key = a.keys[b * c.NP + i];
+    r.jr = a.jrand[b * c.NP + i];
+    r.xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
+    r.x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
+    r.x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
+    r.x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
+    r.bin = !r.xi.f || !r.x1.f || !r.x2.f || !r.x3.f;
+    r.out_slot = a.spare_of[i];
+    r.out = a.genome + r.out_slot * c.Dp;
+    r.bout = a.bits + r.out_slot * c.W;
+    r.prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
+    r.p_mask = (uint32_t)pk.w + 2;  // m + 1 + j, plus one
+    r.F = a.st->F;
+    r.t = a.gthr[g];
+}
+
 template <bool BIN, bool FULL, int K, int PH>
-__device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
-                                               double F, const GenThr &t) {
+__device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int jc) {
     // A warp covers 64 genes per step: lane l owns genes l and l+32, so every
     // load/store is one coalesced 256-byte warp access and the two sign words
     // are plain ballots.
-    const int4 pk = a.picks[b * c.NP + i];
-    const uint64_t key = a.keys[b * c.NP + i];
-    const int jr = a.jrand[b * c.NP + i];
-    const RowRef xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
-    const RowRef x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
-    const RowRef x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
-    const RowRef x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
-    const int64_t out_slot = a.spare_of[i];
-    double *out = a.genome + out_slot * c.Dp;
-    uint32_t *bout = a.bits + out_slot * c.W;
-    uint32_t *prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
-    const uint32_t p_mask = (uint32_t)pk.w + 2;      // m + 1 + j, plus one
+    const RowRef xi = r.xi, x1 = r.x1, x2 = r.x2, x3 = r.x3;
+    double *out = r.out;
+    uint32_t *bout = r.bout, *prow = r.prow;
+    const uint64_t key = r.key;
+    const int jr = r.jr;
+    const double F = r.F;
+    const GenThr t = r.t;
+    const uint32_t p_mask = r.p_mask;
     const uint32_t p_wolf = p_mask + (uint32_t)c.D;  // m + 1 + D + j, plus one
     const int D = (int)c.D;
     const int lane = threadIdx.x & 31;
@@ -647,23 +681,22 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             }
         }
     }
-    if (jc == 0 && threadIdx.x == 0) a.slot_bin[out_slot] = 0;
+    if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
 }
 
 template <int K, int PH>
-__device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const TrialArgs &a, int64_t b, int64_t i, int jc,
-                                                  double F, const GenThr &t, bool bin) {
+__device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int jc) {
     const bool full = jc + kDeChunk <= (int)c.D;
-    if (bin) {
+    if (r.bin) {
         if (full)
-            de_trial_chunk<true, true, K, PH>(c, a, b, i, jc, F, t);
+            de_trial_chunk<true, true, K, PH>(c, a, r, jc);
         else
-            de_trial_chunk<true, false, K, PH>(c, a, b, i, jc, F, t);
+            de_trial_chunk<true, false, K, PH>(c, a, r, jc);
     } else {
         if (full)
-            de_trial_chunk<false, true, K, PH>(c, a, b, i, jc, F, t);
+            de_trial_chunk<false, true, K, PH>(c, a, r, jc);
         else
-            de_trial_chunk<false, false, K, PH>(c, a, b, i, jc, F, t);
+            de_trial_chunk<false, false, K, PH>(c, a, r, jc);
     }
 }
 
@@ -673,23 +706,20 @@ __device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const Tria
 template <int K>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts c, TrialArgs a) {
     pdl_wait();
-    const int64_t g = a.st->g;
-    const int64_t b = g & 1;
-    const double F = a.st->F;
     const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
     const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
     if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
-    const GenThr t = a.gthr[g];
-    const int4 pk = a.picks[b * c.NP + i];
-    const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
-                     a.slot_bin[a.slot_of[pk.z]];
-    if (K == 0 || !t.early)
-        de_trial_dispatch<K, kLate>(c, a, b, i, jc, F, t, bin);
+    __shared__ TrialRow s_row;
+    if (threadIdx.x == 0) trial_row_setup(c, a, a.st->g, i, s_row);
+    __syncthreads();
+    const TrialRow &r = s_row;
+    if (K == 0 || !r.t.early)
+        de_trial_dispatch<K, kLate>(c, a, r, jc);
     else if (K == 4 && c.plus_dyadic)
-        de_trial_dispatch<K, kEarlyDyadic>(c, a, b, i, jc, F, t, bin);
+        de_trial_dispatch<K, kEarlyDyadic>(c, a, r, jc);
     else
-        de_trial_dispatch<K, kEarly>(c, a, b, i, jc, F, t, bin);
+        de_trial_dispatch<K, kEarly>(c, a, r, jc);
 }
 
 // Horizontal fusion (QPM_WOLF=mixed): even CTAs run the trial
@@ -712,11 +742,10 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(Run
                             kDeChunk);
         return;
     }
-    const double F = a.st->F;
-    const int4 pk = a.picks[b * c.NP + i];
-    const bool bin = a.slot_bin[a.slot_of[i]] | a.slot_bin[a.slot_of[pk.x]] | a.slot_bin[a.slot_of[pk.y]] |
-                     a.slot_bin[a.slot_of[pk.z]];
-    de_trial_dispatch<0, kLate>(c, a, b, i, jc, F, t, bin);
+    __shared__ TrialRow s_row;
+    if (threadIdx.x == 0) trial_row_setup(c, a, g, i, s_row);
+    __syncthreads();
+    de_trial_dispatch<0, kLate>(c, a, s_row, jc);
 }
 
 // multi-GPU: all-gathered wolf candidates of accepted (non-leader) rows into
@@ -739,44 +768,58 @@ __global__ void k_commit_cand_bits(RunConsts c, TrialArgs a) {
 }
 
 // ---------------------------------------------------------------- wolf update
-// One thread per (row, 32-gene word): the candidate's sign word from the
+// One thread per (row, 32-gene word), one CTA row per individual: the candidate's sign word from the
 // leaders' words and the row's 8 planes (bit-sliced, ~30 logic ops per 32
 // genes).  Leaders do not move (optimizer.py:454).
 template <int K>
-__global__ void __launch_bounds__(kRowThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
+__global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
     pdl_wait();
+    // one CTA row per individual: the row-level decisions are CTA-uniform
+    const int64_t i = a.row_lo + blockIdx.y;
+    const int w = (int)(blockIdx.x * kApplyThreads + threadIdx.x);
+    int32_t lead[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) lead[t] = a.st->leaders[t];
+    bool skip = false;
+#pragma unroll
+    for (int t = 0; t < K; ++t) skip |= lead[t] == i;
+    if (skip || w >= (int)c.W) return;
+    if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
     const int64_t g = a.st->g;
     const bool early = a.gthr[g].early != 0;
-    const uint32_t *planes = a.planes + (g & 1) * c.NP * c.W * kPlanes;
-    const int64_t total = a.n_rows * c.W;
-    int32_t lead[K];
-    const uint32_t *lrow[K];
+    uint32_t ld[4];
 #pragma unroll
-    for (int t = 0; t < K; ++t) {
-        lead[t] = a.st->leaders[t];
-        lrow[t] = a.bits + (int64_t)a.slot_of[lead[t]] * c.W;
+    for (int t = 0; t < 4; ++t) ld[t] = t < K ? a.bits[(int64_t)a.slot_of[lead[t]] * c.W + w] : 0u;
+    const uint32_t *pw = a.planes + (((g & 1) * c.NP + i) * c.W + w) * kPlanes;
+    const uint4 q0 = *reinterpret_cast<const uint4 *>(pw);
+    uint32_t pl[5] = {q0.x, q0.y, q0.z, q0.w, early ? pw[4] : 0u};
+    const int rem = (int)c.D - w * 32;
+    const uint32_t valid = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+    if (K == 4 && !early) {
+        // 2-2 ties of non-social genes need the state draw (row 3 of the 6 x D
+        // block), which k_de_trial skipped: draw it here for those genes only
+        const uint32_t z0 = ~ld[0], z1 = ~ld[1], z2 = ~ld[2], z3 = ~ld[3];
+        const uint32_t s0 = z0 ^ z1 ^ z2 ^ z3;
+        const uint32_t s1 = ((z0 & z1) | (z0 & z2) | (z1 & z2)) ^ ((z0 ^ z1 ^ z2) & z3);
+        const uint32_t s2 = ((z0 & z1) | (z0 & z2) | (z1 & z2)) & ((z0 ^ z1 ^ z2) & z3);
+        uint32_t ties = ~pl[0] & s1 & ~s0 & ~s2 & valid;  // count == 2
+        if (ties) {
+            const int64_t b = g & 1;
+            const uint64_t key = a.keys[b * c.NP + i];
+            const uint32_t p3 = (uint32_t)a.picks[b * c.NP + i].w + 2 + 4 * (uint32_t)c.D;  // m+1+D + 3D + j, plus one
+            uint32_t st = 0;
+            while (ties) {
+                const int bit = __ffs(ties) - 1;
+                ties &= ties - 1;
+                const uint64_t x3 = mix_pre2(key, p3 + (uint32_t)(w * 32 + bit), c);
+                st |= ((mix_hi2(x3) >> 31) == 0u ? 1u : 0u) << bit;  // u < 0.5
+            }
+            pl[2] |= st;
+        }
     }
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = a.row_lo + idx / c.W;
-        const int w = (int)(idx % c.W);
-        bool skip = false;
-#pragma unroll
-        for (int t = 0; t < K; ++t) skip |= lead[t] == i;
-        if (skip) continue;
-        if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) continue;
-        uint32_t ld[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) ld[t] = t < K ? lrow[t][w] : 0u;
-        const uint32_t *pw = planes + (i * c.W + w) * kPlanes;
-        const uint4 q0 = *reinterpret_cast<const uint4 *>(pw);
-        const uint32_t pl[5] = {q0.x, q0.y, q0.z, q0.w, early ? pw[4] : 0u};
-        const int rem = (int)c.D - w * 32;
-        const uint32_t valid = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        const uint32_t word = wolf_word<K>(ld, pl, early) & valid;
-        a.bits[(int64_t)a.spare_of[i] * c.W + w] = word;  // scored from the spare slot
-        if (a.cbits) a.cbits[i * c.W + w] = word;          // staged for the all-gather
-    }
+    const uint32_t word = wolf_word<K>(ld, pl, early) & valid;
+    a.bits[(int64_t)a.spare_of[i] * c.W + w] = word;  // scored from the spare slot
+    if (a.cbits) a.cbits[i * c.W + w] = word;          // staged for the all-gather
 }
 
 // ---------------------------------------------------------------- run_gwo
@@ -1264,7 +1307,7 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
-    int apply_grid = 148;
+    int apply_grid = 148;  // k_commit_cand_bits (grid-stride)
     int plan_grid = 148;       // k_plan_wolf CTAs (QPM_PLAN_CTAS)
     bool plan_after_trial = false;  // fork the planner after k_de_trial (QPM_PLAN_FORK=trial)
     bool wolf_in_planner = false;   // wolf planes on the side stream (QPM_WOLF=planner)
@@ -1588,8 +1631,9 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3(1), dim3(kCtaThreads), 0, s, c, e->st,
                               (const double *)e->cand, e->fit, e->slot_of, e->spare_of));
         mark("gwo_apply");
-        QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>, dim3(e->apply_grid),
-                              dim3(kRowThreads), 0, s, c, own));
+        QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
+                              dim3((unsigned)((c.W + kApplyThreads - 1) / kApplyThreads), (unsigned)n_own),
+                              dim3(kApplyThreads), 0, s, c, own));
         QPM_LAUNCH_CHECK();
         *n += 2;
         mark("fitness_gwo");
@@ -1725,10 +1769,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         int dev = 0, sms = 148, occ_a = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (c.k == 4)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_gwo_apply<4>, kRowThreads, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_gwo_apply<3>, kRowThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_commit_cand_bits, kRowThreads, 0);
         e->apply_grid = sms * std::max(occ_a, 1);
         e->plan_grid = sms * 2;
         if (const char *v = getenv("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
