@@ -115,6 +115,7 @@ struct RunConsts {
     int32_t n_leaf, n_levels;
     Thr thr_cr;      // u <= CR (de_crossover)
     int plus_dyadic; // K = 4 and p_plus(c) = c/4 exactly: plus level = 1 + floor(4u)
+    int plus_ends;   // p_plus(0) = 0 and p_plus(K) = 1 (discreteness 1)
     uint32_t m4, m32, m2;  // = 4, 32, 2: runtime constants (see xs_fma)
     Thr thr_plus[5]; // u_plus < p_plus(count), count = 0..K (hybrid K <= 4)
 };
@@ -323,23 +324,20 @@ __device__ __forceinline__ bool draw_lt(const RunConsts &c, const Thr &t, uint64
     return EXACT ? passes_hi(t, x, h) : lt_hi(t, h, tie, c.m2);
 }
 
-// Phase of the wolf draws: late (flip), early (disturb + plus level), or
-// early with dyadic plus thresholds c/4 (K = 4, discreteness 1: the level is
-// the top two bits of the draw).
-enum WolfPhase { kLate = 0, kEarly = 1, kEarlyDyadic = 2 };
-
-// the wolf draws of one gene (stream position p0 = m + 1 + D + j, plus one)
-// as its plane bits (P0..P4 above).  Straight-line code (selects only), so
-// the draws of several genes interleave.  EXACT = false decides every compare
-// on the high word and sets `tie` when one tied; the caller then redoes the
-// gene with EXACT = true.
-template <int K, int PH, bool EXACT>
+// The first two wolf draws of one gene (stream position p0 = m + 1 + D + j,
+// plus one) as plane bits P0..P2: social; then pick (social) or disturbed /
+// flipped (row 2 early, row 5 late).  The third draw (state or plus level)
+// matters only for a minority of genes, and which ones depends on the
+// leaders, so k_gwo_apply draws it for exactly those genes.  Straight-line
+// code (selects only), so the draws of several genes interleave.  EXACT =
+// false decides every compare on the high word and sets `tie` when one tied;
+// the caller then redoes the gene with EXACT = true.
+template <int K, bool EXACT>
 __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p0,
-                                              uint32_t D, bool &tie) {
-    constexpr bool EARLY = PH != kLate;
+                                              uint32_t D, bool early, bool &tie) {
     const uint64_t x1 = mix_pre2(key, p0, c);
     const bool soc = draw_lt<EXACT>(c, t.sl, x1, mix_hi2(x1), tie);
-    const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (EARLY ? 2 * D : 5 * D)), c);
+    const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (early ? 2 * D : 5 * D)), c);
     const uint32_t h2 = mix_hi2(x2);
     uint32_t pick;
     if (K == 4) {
@@ -349,51 +347,27 @@ __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &
         const int pv = (int)((double)((z ^ (z >> 31)) >> 11) * kTwoM53 * (double)K);
         pick = (uint32_t)min(pv, K - 1);
     }
-    const uint32_t soc_code = 1u | (pick << 1);
-    const bool f2 = draw_lt<EXACT>(c, EARLY ? t.dist : t.flip, x2, h2, tie);
-    // late generations: a 3-leader majority never ties, and a 4-leader tie is
-    // rare, so the state draw is left to k_gwo_apply, which knows the leaders
-    if (!EARLY) return soc ? soc_code : (f2 ? 2u : 0u);
-    const uint64_t x3 = mix_pre2(key, p0 + ((EARLY && !f2) ? 4 * D : 3 * D), c);
-    const uint32_t h3 = mix_hi2(x3);
-    const uint32_t st = (h3 >> 31) ^ 1u;  // u < 0.5
-    uint32_t L = 0;
-    if (PH == kEarlyDyadic) {
-        L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
-    } else if (PH == kEarly) {
-#pragma unroll
-        for (int cc = 0; cc <= K; ++cc) L += draw_lt<EXACT>(c, c.thr_plus[cc], x3, h3, tie) ? 0u : 1u;
-    }
-    const uint32_t rest = (EARLY && !f2) ? (L << 2) : ((f2 ? 2u : 0u) | (st << 2));
-    return soc ? soc_code : rest;
+    const bool f2 = draw_lt<EXACT>(c, early ? t.dist : t.flip, x2, h2, tie);
+    return soc ? 1u | (pick << 1) : (f2 ? 2u : 0u);
 }
 
-// the wolf planes of one 32-gene word from each lane's code: P0..P2, and
-// P3, P4 in early generations; lane `writer` stores them
-template <bool EARLY>
+// planes P0..P2 of one 32-gene word from each lane's code; lane `writer`
+// stores them (P3 cleared; k_gwo_apply completes P2..P4)
 __device__ __forceinline__ void store_planes(uint32_t *dst_word, uint32_t code, int lane, int writer) {
     const uint32_t p0 = __ballot_sync(0xffffffffu, code & 1u);
     const uint32_t p1 = __ballot_sync(0xffffffffu, code & 2u);
     const uint32_t p2 = __ballot_sync(0xffffffffu, code & 4u);
-    uint32_t p3 = 0, p4 = 0;
-    if (EARLY) {
-        p3 = __ballot_sync(0xffffffffu, code & 8u);
-        p4 = __ballot_sync(0xffffffffu, code & 16u);
-    }
-    if (lane == writer) {
-        uint4 *dst = reinterpret_cast<uint4 *>(dst_word);
-        dst[0] = make_uint4(p0, p1, p2, p3);
-        if (EARLY) dst_word[4] = p4;
-    }
+    if (lane == writer) *reinterpret_cast<uint4 *>(dst_word) = make_uint4(p0, p1, p2, 0u);
 }
 
 // The wolf planes of row genes [jc, jc + len) (len a multiple of
 // 2 * kRowThreads) by one CTA: each thread draws two genes at a time
 // (independent chains), warps ballot the plane words.
-template <int K, int PH>
+template <int K>
 __device__ __forceinline__ void wolf_chunk(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p_wolf,
                                            uint32_t *prow, int jc, int len) {
     const uint32_t D = (uint32_t)c.D;
+    const bool early = t.early != 0;
     const int lane = threadIdx.x & 31;
 #pragma unroll 1
     for (int it = 0; it < len; it += 2 * kRowThreads) {
@@ -403,31 +377,20 @@ __device__ __forceinline__ void wolf_chunk(const RunConsts &c, const GenThr &t, 
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             j[h] = jc + it + h * kRowThreads + (int)threadIdx.x;
-            code[h] = wolf_code<K, PH, false>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
+            code[h] = wolf_code<K, false>(c, t, key, p_wolf + (uint32_t)j[h], D, early, tie[h]);
             if (j[h] >= (int)D) code[h] = 0u, tie[h] = false;
         }
         if (__any_sync(0xffffffffu, tie[0] || tie[1])) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-                if (tie[h]) code[h] = wolf_code<K, PH, true>(c, t, key, p_wolf + (uint32_t)j[h], D, tie[h]);
+                if (tie[h]) code[h] = wolf_code<K, true>(c, t, key, p_wolf + (uint32_t)j[h], D, early, tie[h]);
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             if (j[h] - lane >= (int)c.Dp) break;  // warp-uniform
-            store_planes<PH != kLate>(prow + ((j[h] - lane) >> 5) * kPlanes, code[h], lane, 0);
+            store_planes(prow + ((j[h] - lane) >> 5) * kPlanes, code[h], lane, 0);
         }
     }
-}
-
-template <int K>
-__device__ __forceinline__ void wolf_chunk_phase(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p_wolf,
-                                                 uint32_t *prow, int jc, int len) {
-    if (!t.early)
-        wolf_chunk<K, kLate>(c, t, key, p_wolf, prow, jc, len);
-    else if (K == 4 && c.plus_dyadic)
-        wolf_chunk<K, kEarlyDyadic>(c, t, key, p_wolf, prow, jc, len);
-    else
-        wolf_chunk<K, kEarly>(c, t, key, p_wolf, prow, jc, len);
 }
 
 // the wolf planes of generation g_plan for this rank's rows on the side
@@ -444,7 +407,7 @@ __global__ void __launch_bounds__(kRowThreads) k_plan_wolf(RunConsts c, PlanArgs
         const int64_t i = a.row_lo + item / nchunk;
         const int jc = (int)(item % nchunk) * kGenesPerBlock;
         const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
-        wolf_chunk_phase<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
+        wolf_chunk<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
                             kGenesPerBlock);
     }
 }
@@ -544,7 +507,7 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
     r.t = a.gthr[g];
 }
 
-template <bool BIN, bool FULL, int K, int PH>
+template <bool BIN, bool FULL, int K>
 __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int jc) {
     // A warp covers 64 genes per step: lane l owns genes l and l+32, so every
     // load/store is one coalesced 256-byte warp access and the two sign words
@@ -556,6 +519,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const int jr = r.jr;
     const double F = r.F;
     const GenThr t = r.t;
+    const bool early = t.early != 0;
     const uint32_t p_mask = r.p_mask;
     const uint32_t p_wolf = p_mask + (uint32_t)c.D;  // m + 1 + D + j, plus one
     const int D = (int)c.D;
@@ -654,7 +618,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 for (int q = 0; q < 2; ++q) {
                     const int jj = jb + st * kSpan + lane + 32 * q;
                     bool ti = false;
-                    code[st][q] = wolf_code<K, PH, false>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, ti);
+                    code[st][q] = wolf_code<K, false>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, early, ti);
                     if (!FULL && jj >= D) code[st][q] = 0u, ti = false;
                     wtie |= ti;
                 }
@@ -667,7 +631,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                         const int jj = jb + st * kSpan + lane + 32 * q;
                         bool ti = false;
                         if (FULL || jj < D)
-                            code[st][q] = wolf_code<K, PH, true>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, ti);
+                            code[st][q] =
+                                wolf_code<K, true>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, early, ti);
                     }
                 }
             }
@@ -677,26 +642,26 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 if (!FULL && j64 >= (int)c.Dp) break;
 #pragma unroll
                 for (int q = 0; q < 2; ++q)
-                    store_planes<PH != kLate>(prow + ((j64 >> 5) + q) * kPlanes, code[st][q], lane, q);
+                    store_planes(prow + ((j64 >> 5) + q) * kPlanes, code[st][q], lane, q);
             }
         }
     }
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
 }
 
-template <int K, int PH>
+template <int K>
 __device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int jc) {
     const bool full = jc + kDeChunk <= (int)c.D;
     if (r.bin) {
         if (full)
-            de_trial_chunk<true, true, K, PH>(c, a, r, jc);
+            de_trial_chunk<true, true, K>(c, a, r, jc);
         else
-            de_trial_chunk<true, false, K, PH>(c, a, r, jc);
+            de_trial_chunk<true, false, K>(c, a, r, jc);
     } else {
         if (full)
-            de_trial_chunk<false, true, K, PH>(c, a, r, jc);
+            de_trial_chunk<false, true, K>(c, a, r, jc);
         else
-            de_trial_chunk<false, false, K, PH>(c, a, r, jc);
+            de_trial_chunk<false, false, K>(c, a, r, jc);
     }
 }
 
@@ -713,13 +678,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts
     __shared__ TrialRow s_row;
     if (threadIdx.x == 0) trial_row_setup(c, a, a.st->g, i, s_row);
     __syncthreads();
-    const TrialRow &r = s_row;
-    if (K == 0 || !r.t.early)
-        de_trial_dispatch<K, kLate>(c, a, r, jc);
-    else if (K == 4 && c.plus_dyadic)
-        de_trial_dispatch<K, kEarlyDyadic>(c, a, r, jc);
-    else
-        de_trial_dispatch<K, kEarly>(c, a, r, jc);
+    de_trial_dispatch<K>(c, a, s_row, jc);
 }
 
 // Horizontal fusion (QPM_WOLF=mixed): even CTAs run the trial
@@ -738,14 +697,14 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(Run
     const GenThr t = a.gthr[g];
     if (blockIdx.x & 1) {
         const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
-        wolf_chunk_phase<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
+        wolf_chunk<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
                             kDeChunk);
         return;
     }
     __shared__ TrialRow s_row;
     if (threadIdx.x == 0) trial_row_setup(c, a, g, i, s_row);
     __syncthreads();
-    de_trial_dispatch<0, kLate>(c, a, s_row, jc);
+    de_trial_dispatch<0>(c, a, s_row, jc);
 }
 
 // multi-GPU: all-gathered wolf candidates of accepted (non-leader) rows into
@@ -792,29 +751,53 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
     for (int t = 0; t < 4; ++t) ld[t] = t < K ? a.bits[(int64_t)a.slot_of[lead[t]] * c.W + w] : 0u;
     const uint32_t *pw = a.planes + (((g & 1) * c.NP + i) * c.W + w) * kPlanes;
     const uint4 q0 = *reinterpret_cast<const uint4 *>(pw);
-    uint32_t pl[5] = {q0.x, q0.y, q0.z, q0.w, early ? pw[4] : 0u};
+    uint32_t pl[5] = {q0.x, q0.y, q0.z, 0u, 0u};  // P0..P2 from k_de_trial
     const int rem = (int)c.D - w * 32;
     const uint32_t valid = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-    if (K == 4 && !early) {
-        // 2-2 ties of non-social genes need the state draw (row 3 of the 6 x D
-        // block), which k_de_trial skipped: draw it here for those genes only
-        const uint32_t z0 = ~ld[0], z1 = ~ld[1], z2 = ~ld[2], z3 = ~ld[3];
-        const uint32_t s0 = z0 ^ z1 ^ z2 ^ z3;
-        const uint32_t s1 = ((z0 & z1) | (z0 & z2) | (z1 & z2)) ^ ((z0 ^ z1 ^ z2) & z3);
-        const uint32_t s2 = ((z0 & z1) | (z0 & z2) | (z1 & z2)) & ((z0 ^ z1 ^ z2) & z3);
-        uint32_t ties = ~pl[0] & s1 & ~s0 & ~s2 & valid;  // count == 2
-        if (ties) {
-            const int64_t b = g & 1;
-            const uint64_t key = a.keys[b * c.NP + i];
-            const uint32_t p3 = (uint32_t)a.picks[b * c.NP + i].w + 2 + 4 * (uint32_t)c.D;  // m+1+D + 3D + j, plus one
-            uint32_t st = 0;
-            while (ties) {
-                const int bit = __ffs(ties) - 1;
-                ties &= ties - 1;
-                const uint64_t x3 = mix_pre2(key, p3 + (uint32_t)(w * 32 + bit), c);
-                st |= ((mix_hi2(x3) >> 31) == 0u ? 1u : 0u) << bit;  // u < 0.5
+    // the third draw (row 3 state / row 4 plus) for the non-social genes whose
+    // outcome depends on it: early, disturbed genes (state) and undisturbed
+    // genes whose leaders disagree (plus level); late, 2-2 ties of 4 leaders
+    const uint32_t z0 = ~ld[0], z1 = ~ld[1], z2 = ~ld[2], z3 = K == 4 ? ~ld[3] : 0u;
+    const uint32_t a3 = z0 ^ z1 ^ z2, c3 = (z0 & z1) | (z0 & z2) | (z1 & z2);
+    const uint32_t s0 = a3 ^ z3, s1 = c3 ^ (a3 & z3), s2 = c3 & (a3 & z3);  // count of +1 leaders
+    const uint32_t nsoc = ~pl[0] & valid;
+    const uint32_t f2 = pl[1] & nsoc;
+    uint32_t need;
+    if (early) {
+        const uint32_t none = ~(s0 | s1 | s2);
+        const uint32_t all = K == 4 ? (s2 & ~s1 & ~s0) : (s1 & s0);
+        const uint32_t agree = c.plus_ends ? (none | all) : 0u;
+        // agreeing leaders decide "plus" for any level L in [1, K]: take L = 1
+        pl[2] |= nsoc & ~f2 & agree;
+        need = nsoc & (f2 | ~agree);
+    } else {
+        need = K == 4 ? nsoc & s1 & ~s0 & ~s2 : 0u;  // count == 2
+    }
+    if (need) {
+        const int64_t b = g & 1;
+        const uint64_t key = a.keys[b * c.NP + i];
+        const uint32_t base = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D + (uint32_t)(w * 32);
+        const uint32_t D = (uint32_t)c.D;
+        while (need) {
+            const int bit = __ffs(need) - 1;
+            need &= need - 1;
+            const bool state = !early || ((f2 >> bit) & 1u);
+            const uint64_t x3 = mix_pre2(key, base + (uint32_t)bit + (state ? 3 * D : 4 * D), c);
+            const uint32_t h3 = mix_hi2(x3);
+            if (state) {
+                pl[2] |= ((h3 >> 31) == 0u ? 1u : 0u) << bit;  // u < 0.5
+            } else {
+                uint32_t L = 0;
+                if (K == 4 && c.plus_dyadic) {
+                    L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc <= K; ++cc) L += passes_hi(c.thr_plus[cc], x3, h3) ? 0u : 1u;
+                }
+                pl[2] |= (L & 1u) << bit;
+                pl[3] |= ((L >> 1) & 1u) << bit;
+                pl[4] |= ((L >> 2) & 1u) << bit;
             }
-            pl[2] |= st;
         }
     }
     const uint32_t word = wolf_word<K>(ld, pl, early) & valid;
@@ -1853,6 +1836,9 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (cnt < 5) c.thr_plus[cnt] = make_thr(hs.thr_plus[cnt]);
     }
     c.plus_dyadic = (c.k == 4 && P->discreteness_factor == 1.0) ? 1 : 0;
+    // p_plus(0) = 0 and p_plus(K) = 1: the plus level L lies in [1, K], so
+    // unanimous leaders decide "plus" without the draw
+    c.plus_ends = (c.k <= kMaxLeaders && hs.thr_plus[0] == 0 && hs.thr_plus[c.k] > kTwo53) ? 1 : 0;
     c.m4 = 4;
     c.m32 = 32;
     c.m2 = 2;
