@@ -27,6 +27,8 @@
  *   qpm_pack_signs                  -> Individual.from_genome projection
  *                                      (optimizer.py:52-56), bit-packed
  *   qpm_reduce_best                 -> parexec.reduce_best (parexec.py:123-154)
+ *   qpm_sweep_spectrum              -> physics.sweep_spectrum (physics.py:378-395),
+ *                                      batched over patterns
  *   qpm_brute_force                 -> bench.brute_force_oracle (bench.py:179-209)
  *                                      with bench.lexicographic_signs (:169-176)
  *   qpm_engine_*                    -> optimizer.run_hybrid / run_de / run_gwo
@@ -122,6 +124,20 @@ int qpm_sum_block_host(qpm_problem *p, int wl, const int8_t *signs, int64_t rows
 /* -------------------------------------------------------------- leaders */
 /* top-k indices by (-value, index) of values_dev[n]; idx_out_dev int32 [k]; k <= 64 */
 int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out_dev, void *stream);
+
+/* -------------------------------------------------------------- spectra */
+/* |d_eff| of P patterns at M pump wavelengths (physics.sweep_spectrum): the
+ * phase tables exp(-i dk z_j), z_j = j t, are generated on the device
+ * (sincos of the same double product j*t*dk numpy forms) instead of being
+ * uploaded, one CTA per (wavelength, pattern).
+ *   process QPM_PROCESS_SHG: d = w[m] * sum_j s_j e1_j
+ *   process QPM_PROCESS_THG: d = w[m] * sum_j s_j P_j b_j + hphi[m] * sum_j e1_j b_j
+ *     (w = w12, hphi = t^2 phi(i dk1 t, i dk2 t): hconst = hphi * sum e1 b)
+ * signs: host int8 [P][D]; dk, w, hphi: host [M][2]; out: host f64 [P][M]
+ * |d|.  Accuracy: the device sincos differs from libm by <= 1 ulp per phase;
+ * |d| agrees with the reference to ~1e-12 relative.  Synchronous. */
+int qpm_sweep_spectrum(int process, double thickness, int64_t D, const int8_t *signs, int64_t P, const double *dk,
+                       const double *w, const double *hphi, int64_t M, double *out);
 
 /* ------------------------------------------------------ exhaustive search */
 /* Global optimum over all 2^n sign patterns of a problem with D = n (n <= 63):

@@ -42,6 +42,7 @@ from .optimizer import (
     schedule_table,
 )
 from .search import brute_force_oracle, lexicographic_signs
+from .spectrum import sweep_spectra, sweep_spectrum
 from .trials import ComparisonReport, RunStatistics, TrialRecord, compare_algorithms, run_trials
 from .parexec import BatchEvaluationError, BatchJob, TimingReport, evaluate_batch, reduce_best, time_run
 from .tables import (

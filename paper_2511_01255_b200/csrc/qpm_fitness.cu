@@ -284,6 +284,95 @@ __device__ __forceinline__ Seg seg_cat(const Seg &x, const Seg &y) {
     return z;
 }
 
+// |d_eff| of pattern p at wavelength m: one CTA per (m, p), threads own
+// contiguous domain ranges, partial (acc, P, T) per thread stitched in
+// thread order (shuffles, then warps through shared memory)
+constexpr int kSpecThreads = 256;
+
+__global__ void __launch_bounds__(kSpecThreads) k_spectrum(int thg, double t, int64_t D, const int8_t *__restrict__ signs,
+                                                          const double2 *__restrict__ dk,
+                                                          const double2 *__restrict__ w,
+                                                          const double2 *__restrict__ hphi, int64_t M,
+                                                          double *__restrict__ out) {
+    const int64_t m = blockIdx.x, pat = blockIdx.y;
+    const double2 k = dk[m];
+    const int8_t *sp = signs + pat * D;
+    const int64_t per = (D + kSpecThreads - 1) / kSpecThreads;
+    const int64_t j0 = threadIdx.x * per, j1 = min(D, j0 + per);
+    Seg z = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    double er = 0.0, ei = 0.0;  // sum e1 b (THG's pattern-independent term)
+    for (int64_t j = j0; j < j1; ++j) {
+        const double zj = (double)j * t;  // np.arange(count) * t
+        double s1, c1;
+        sincos(k.x * zj, &s1, &c1);
+        const double e1r = c1, e1i = -s1;  // exp(-i dk1 z)
+        const double sg = sp[j] < 0 ? -1.0 : 1.0;
+        if (thg) {
+            double s2, c2;
+            sincos(k.y * zj, &s2, &c2);
+            const double br = c2, bi = -s2;
+            const double spr = sg * z.pr, spi = sg * z.pi;  // s_j P_j
+            z.ar += spr * br - spi * bi;
+            z.ai += spr * bi + spi * br;
+            z.tr += sg * br;
+            z.ti += sg * bi;
+            er += e1r * br - e1i * bi;
+            ei += e1r * bi + e1i * br;
+        }
+        z.pr += sg * e1r;
+        z.pi += sg * e1i;
+    }
+    // stitch thread ranges in order: lane tree, then warps
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int off = 1; off < 32; off <<= 1) {
+        Seg o;
+        o.ar = __shfl_down_sync(0xffffffffu, z.ar, off);
+        o.ai = __shfl_down_sync(0xffffffffu, z.ai, off);
+        o.pr = __shfl_down_sync(0xffffffffu, z.pr, off);
+        o.pi = __shfl_down_sync(0xffffffffu, z.pi, off);
+        o.tr = __shfl_down_sync(0xffffffffu, z.tr, off);
+        o.ti = __shfl_down_sync(0xffffffffu, z.ti, off);
+        const double oer = __shfl_down_sync(0xffffffffu, er, off);
+        const double oei = __shfl_down_sync(0xffffffffu, ei, off);
+        if ((lane & (2 * off - 1)) == 0) {
+            z = seg_cat(z, o);
+            er += oer;
+            ei += oei;
+        }
+    }
+    __shared__ double s_seg[kSpecThreads / 32][8];
+    if (lane == 0) {
+        s_seg[warp][0] = z.ar;
+        s_seg[warp][1] = z.ai;
+        s_seg[warp][2] = z.pr;
+        s_seg[warp][3] = z.pi;
+        s_seg[warp][4] = z.tr;
+        s_seg[warp][5] = z.ti;
+        s_seg[warp][6] = er;
+        s_seg[warp][7] = ei;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    Seg acc = {s_seg[0][0], s_seg[0][1], s_seg[0][2], s_seg[0][3], s_seg[0][4], s_seg[0][5]};
+    double sr = s_seg[0][6], si = s_seg[0][7];
+    for (int v = 1; v < kSpecThreads / 32; ++v) {
+        acc = seg_cat(acc, Seg{s_seg[v][0], s_seg[v][1], s_seg[v][2], s_seg[v][3], s_seg[v][4], s_seg[v][5]});
+        sr += s_seg[v][6];
+        si += s_seg[v][7];
+    }
+    const double2 ww = w[m];
+    double dr, di;
+    if (thg) {
+        const double2 hp = hphi[m];
+        dr = ww.x * acc.ar - ww.y * acc.ai + (hp.x * sr - hp.y * si);
+        di = ww.x * acc.ai + ww.y * acc.ar + (hp.x * si + hp.y * sr);
+    } else {
+        dr = ww.x * acc.pr - ww.y * acc.pi;
+        di = ww.x * acc.pi + ww.y * acc.pr;
+    }
+    out[pat * M + m] = hypot_glibc(dr, di);
+}
+
 constexpr int kChunkEntries = kQuadsPerChunk * kQuadEntries;  // 768 double2 = 12 KB
 constexpr uint32_t kChunkBytes = kChunkEntries * sizeof(double2);
 constexpr int kFitSmem = 2 * kChunkBytes;  // double-buffered chunks (dynamic shared memory)
@@ -775,6 +864,52 @@ int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, d
     QPM_CUDA_TRY(cudaMemcpyAsync(out, p.hp_out, (size_t)rows * sizeof(double), cudaMemcpyDeviceToHost, p.hp_stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
     return QPM_OK;
+}
+
+int qpm_sweep_spectrum(int process, double thickness, int64_t D, const int8_t *signs, int64_t P, const double *dk,
+                       const double *w, const double *hphi, int64_t M, double *out) {
+    QPM_ARG_CHECK(process == QPM_PROCESS_SHG || process == QPM_PROCESS_THG, "process");
+    QPM_ARG_CHECK(signs && dk && w && out && (process == QPM_PROCESS_SHG || hphi), "buffers");
+    QPM_ARG_CHECK(D >= 1 && P >= 1 && M >= 1 && M <= (1LL << 31) - 1 && P <= 65535, "sizes");
+    const size_t sb = (size_t)P * D, tb = (size_t)M * sizeof(double2), ob = (size_t)P * M * sizeof(double);
+    int8_t *d_signs = (int8_t *)dev_cache_alloc(sb);
+    double2 *d_dk = (double2 *)dev_cache_alloc(tb), *d_w = (double2 *)dev_cache_alloc(tb);
+    double2 *d_h = (double2 *)dev_cache_alloc(tb);
+    double *d_out = (double *)dev_cache_alloc(ob);
+    int rc = QPM_OK;
+    if (!d_signs || !d_dk || !d_w || !d_h || !d_out) {
+        set_error("out of device memory");
+        rc = QPM_ERR_CUDA;
+    }
+    cudaStream_t s = nullptr;
+    if (!rc && (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaMemcpyAsync(d_signs, signs, sb, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                cudaMemcpyAsync(d_dk, dk, tb, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                cudaMemcpyAsync(d_w, w, tb, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                (hphi && cudaMemcpyAsync(d_h, hphi, tb, cudaMemcpyHostToDevice, s) != cudaSuccess))) {
+        set_error("spectrum upload failed");
+        rc = QPM_ERR_CUDA;
+    }
+    if (!rc) {
+        k_spectrum<<<dim3((unsigned)M, (unsigned)P), kSpecThreads, 0, s>>>(
+            process == QPM_PROCESS_THG, thickness, D, d_signs, d_dk, d_w, d_h, M, d_out);
+        if (cudaGetLastError() != cudaSuccess ||
+            cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            set_error("spectrum kernel failed");
+            rc = QPM_ERR_CUDA;
+        }
+    }
+    if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+    dev_cache_release(d_signs, sb);
+    dev_cache_release(d_dk, tb);
+    dev_cache_release(d_w, tb);
+    dev_cache_release(d_h, tb);
+    dev_cache_release(d_out, ob);
+    return rc;
 }
 
 int qpm_brute_force(qpm_problem *h, int n, int mode, int64_t chunk_rows, int64_t *best_index, double *best_fit,

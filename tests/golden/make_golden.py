@@ -415,10 +415,38 @@ def gen_search():
     save("search.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+# physics.py: sweep_spectrum over pump wavelengths
+# ---------------------------------------------------------------------------
+
+def gen_spectra():
+    disp = default_dispersion(25.0)
+    out = {}
+    names = []
+    cases = [("thg_d1000", "thg", 1.0, 1000, 11, np.linspace(1250.0, 1700.0, 19)),
+             ("shg_d1000", "shg", 1.0, 1000, 12, np.linspace(1250.0, 1700.0, 19)),
+             ("thg_d4096_t05", "thg", 0.5, 4096, 13, np.linspace(1380.0, 1430.0, 64)),
+             ("shg_d33", "shg", 2.0, 33, 14, np.array([1404.0, 1300.0, 1550.0]))]
+    for name, process, t, n, seed, wls in cases:
+        signs = bench.random_population_matrix(1, n, seed)[0]
+        pattern = physics.DomainPattern(t, signs)
+        rows = physics.sweep_spectrum(pattern, disp, list(wls), process)
+        out[f"{name}__spec"] = np.array(json.dumps(dict(process=process, thickness=t, count=n, seed=seed)))
+        out[f"{name}__signs"] = np.asarray(signs, dtype=np.int8)
+        out[f"{name}__rows"] = np.array(rows, dtype=np.float64)
+        names.append(name)
+        print(f"  {name}: {len(rows)} wavelengths, max |d| {max(r[1] for r in rows):.6g}")
+    out["names"] = np.array(json.dumps(names))
+    out["meta"] = np.array("physics.sweep_spectrum(DomainPattern(t, bench.random_population_matrix(1, n, seed)[0]), "
+                           "default_dispersion(25.0), wavelengths, process) rows (wl, |d|, |d|/norm)")
+    save("spectra.npz", **out)
+
+
 if __name__ == "__main__":
     print("qpmdesign", qpmdesign.__version__, "backend", _kernels.backend(), "numpy", np.__version__)
     only = sys.argv[1:]
     for name, fn in (("rng", gen_rng), ("tables", gen_tables), ("fitness", gen_fitness),
-                     ("operators", gen_operators), ("runs", gen_runs), ("search", gen_search)):
+                     ("operators", gen_operators), ("runs", gen_runs), ("search", gen_search),
+                     ("spectra", gen_spectra)):
         if not only or name in only:
             fn()

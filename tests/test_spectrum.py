@@ -1,0 +1,78 @@
+"""batched spectra (physics.sweep_spectrum).
+
+CPU: the host tables (tables.py) and the oracle's kernel sums reproduce the
+reference's sweep_spectrum rows bit-exactly (tests/golden/spectra.npz).
+GPU: the device sweep (phase tables generated in the kernel) agrees with the
+reference rows to 1e-10 relative, for single patterns and batched.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden, spec_of
+from oracle import oracle as O
+from paper_2511_01255_b200 import tables as T
+
+NAMES = json.loads(str(golden("spectra.npz")["names"]))
+RTOL = 1e-10
+
+
+def reference_rows(name):
+    fx = golden("spectra.npz")
+    return spec_of(fx, name), fx[f"{name}__signs"], fx[f"{name}__rows"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_spectrum_matches_reference(name):
+    spec, signs, rows = reference_rows(name)
+    disp = T.default_dispersion(25.0)
+    for wl, mag, norm_mag in rows:
+        t = T.build_tables(spec["process"], spec["thickness"], spec["count"], disp.mismatches_at(wl))
+        prob = O.Problem(spec["process"], t.e1[None], t.b[None] if t.b is not None else None,
+                         np.array([t.w]), np.array([t.hconst]), 1.0)
+        acc = O.sum_block(prob, signs[None])[0]
+        d = acc * t.w + t.hconst if spec["process"] == "thg" else complex(acc * t.w)
+        assert abs(d) == mag
+        assert abs(d) / t.normalization == norm_mag
+
+
+def test_spectrum_validation():
+    import paper_2511_01255_b200 as q
+
+    pat = q.DomainPattern(1.0, np.ones(8, dtype=np.int8))
+    with pytest.raises(ValueError, match="process must be 'shg' or 'thg'"):
+        q.sweep_spectrum(pat, q.default_dispersion(), [1404.0], "sfg")
+    with pytest.raises(ValueError, match="below the model's valid minimum"):
+        q.default_dispersion().mismatches_at(100.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_device_spectrum_matches_reference(name):
+    import paper_2511_01255_b200 as q
+
+    spec, signs, rows = reference_rows(name)
+    pat = q.DomainPattern(spec["thickness"], signs)
+    got = q.sweep_spectrum(pat, q.default_dispersion(), rows[:, 0], spec["process"])
+    got = np.array(got)
+    assert np.array_equal(got[:, 0], rows[:, 0])
+    np.testing.assert_allclose(got[:, 1], rows[:, 1], rtol=RTOL)
+    np.testing.assert_allclose(got[:, 2], rows[:, 2], rtol=RTOL)
+
+
+@pytest.mark.gpu
+def test_device_spectra_batched_equal_single():
+    """Many patterns x many wavelengths in one launch = the per-pattern sweeps."""
+    import paper_2511_01255_b200 as q
+
+    rng = np.random.default_rng(3)
+    signs = np.where(rng.random((7, 2000)) < 0.5, -1, 1).astype(np.int8)
+    wls = np.linspace(1300.0, 1650.0, 97)
+    for process in ("thg", "shg"):
+        batch = q.sweep_spectra(signs, 0.8, q.default_dispersion(), wls, process)
+        assert batch.shape == (7, 97)
+        for p in (0, 6):
+            one = np.array(q.sweep_spectrum(q.DomainPattern(0.8, signs[p]), q.default_dispersion(), wls, process))
+            assert np.array_equal(batch[p], one[:, 1])
