@@ -778,25 +778,42 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
         const uint64_t key = a.keys[b * c.NP + i];
         const uint32_t base = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D + (uint32_t)(w * 32);
         const uint32_t D = (uint32_t)c.D;
+        // two genes per iteration: independent draws interleave
         while (need) {
-            const int bit = __ffs(need) - 1;
-            need &= need - 1;
-            const bool state = !early || ((f2 >> bit) & 1u);
-            const uint64_t x3 = mix_pre2(key, base + (uint32_t)bit + (state ? 3 * D : 4 * D), c);
-            const uint32_t h3 = mix_hi2(x3);
-            if (state) {
-                pl[2] |= ((h3 >> 31) == 0u ? 1u : 0u) << bit;  // u < 0.5
-            } else {
-                uint32_t L = 0;
-                if (K == 4 && c.plus_dyadic) {
-                    L = 1u + (h3 >> 30);  // thresholds c/4: L = 1 + floor(4u)
-                } else {
+            int bit[2];
+            bool have[2];
 #pragma unroll
-                    for (int cc = 0; cc <= K; ++cc) L += passes_hi(c.thr_plus[cc], x3, h3) ? 0u : 1u;
+            for (int h = 0; h < 2; ++h) {
+                have[h] = need != 0u;
+                bit[h] = have[h] ? __ffs(need) - 1 : 0;
+                need &= need - 1;
+            }
+            uint64_t x3[2];
+            uint32_t h3[2];
+            bool state[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                state[h] = !early || ((f2 >> bit[h]) & 1u);
+                x3[h] = mix_pre2(key, base + (uint32_t)bit[h] + (state[h] ? 3 * D : 4 * D), c);
+                h3[h] = mix_hi2(x3[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!have[h]) continue;
+                if (state[h]) {
+                    pl[2] |= ((h3[h] >> 31) == 0u ? 1u : 0u) << bit[h];  // u < 0.5
+                } else {
+                    uint32_t L = 0;
+                    if (K == 4 && c.plus_dyadic) {
+                        L = 1u + (h3[h] >> 30);  // thresholds c/4: L = 1 + floor(4u)
+                    } else {
+#pragma unroll
+                        for (int cc = 0; cc <= K; ++cc) L += passes_hi(c.thr_plus[cc], x3[h], h3[h]) ? 0u : 1u;
+                    }
+                    pl[2] |= (L & 1u) << bit[h];
+                    pl[3] |= ((L >> 1) & 1u) << bit[h];
+                    pl[4] |= ((L >> 2) & 1u) << bit[h];
                 }
-                pl[2] |= (L & 1u) << bit;
-                pl[3] |= ((L >> 1) & 1u) << bit;
-                pl[4] |= ((L >> 2) & 1u) << bit;
             }
         }
     }
