@@ -52,7 +52,10 @@ constexpr int kRowThreads = 256;    // threads per row-block in the elementwise 
 constexpr int kGenesPerThread = 4;  // genes per thread (strided by kRowThreads)
 constexpr int kGenesPerBlock = kRowThreads * kGenesPerThread;
 constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
-constexpr int kDeChunk = 4096;
+#ifndef QPM_DE_CHUNK
+#define QPM_DE_CHUNK 4096
+#endif
+constexpr int kDeChunk = QPM_DE_CHUNK;  // genes per DE-trial CTA (multiple of 1024)
 constexpr int kApplyThreads = 128;  // k_gwo_apply: 32-gene words per CTA
 #ifndef QPM_DE_MINB
 #define QPM_DE_MINB 4  // k_de_trial CTAs per SM the register budget is sized for
