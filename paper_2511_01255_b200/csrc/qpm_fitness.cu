@@ -420,15 +420,21 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
         Seg ch[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) ch[h] = Seg{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        // per word, SIMD within the register: s0 bits of the 8 quads and the
+        // nibbles flipped where s0 = 1, whose bits 1..3 are the relative signs
+        uint32_t s0w[4], xw[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            s0w[h] = words[h] & 0x11111111u;
+            xw[h] = words[h] ^ (s0w[h] * 15u);
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
                 const int q = 8 * h + u;
-                const uint32_t nib = (words[h] >> (4 * u)) & 0xFu;
-                const uint32_t s0 = nib & 1u;
-                const uint32_t rel = ((nib ^ (0u - s0)) >> 1) & 7u;
-                const uint64_t m = sign_mask64(s0);
+                const uint32_t rel = (xw[h] >> (4 * u + 1)) & 7u;
+                const uint64_t m = (uint64_t)((s0w[h] << (31 - 4 * u)) & 0x80000000u) << 32;  // s0 -> sign bit
                 const double2 *tq = tb + q * kQuadEntries + rel;
                 const double2 Et = tq[8];
                 const double2 E = make_double2(flip_if(Et.x, m), flip_if(Et.y, m));
