@@ -346,6 +346,25 @@ def run_cases():
     C.append(("hyb_oracle12", "hybrid", ObjectiveSpec("single_thg", (1404.0,)), mt, 1.0, 12, 64, 200, 0, {}))
     C.append(("hyb_np4", "hybrid", ObjectiveSpec("single_thg", (1404.0,)), mt, 1.0, 1, 4, 12, 2, {}))
     C.append(("hyb_g0", "hybrid", ObjectiveSpec("single_thg", (1404.0,)), mt, 1.0, 16, 8, 0, 3, {}))
+    # extreme operator settings (the reference's unit tests probe these branches)
+    thg = ObjectiveSpec("single_thg", (1404.0,))
+    S = optimizer.Schedules
+    C.append(("hyb_cr1", "hybrid", thg, disp, 1.0, 200, 16, 30, 21, dict(de_params=optimizer.DEParams(cr=1.0))))
+    C.append(("hyb_cr0", "hybrid", thg, disp, 1.0, 200, 16, 30, 22, dict(de_params=optimizer.DEParams(cr=0.0))))
+    C.append(("hyb_dist1", "hybrid", thg, disp, 1.0, 200, 16, 30, 23, dict(schedules=S(p_dist0=1.0, p_sl0=0.0))))
+    C.append(("hyb_sl1", "hybrid", thg, disp, 1.0, 200, 16, 30, 24, dict(schedules=S(p_sl0=1.0))))
+    C.append(("hyb_flip1", "hybrid", thg, disp, 1.0, 200, 16, 30, 25,
+              dict(schedules=S(p_flip0=1.0, phase_split=0.2))))
+    C.append(("hyb_all_late", "hybrid", thg, disp, 1.0, 200, 16, 30, 26, dict(schedules=S(phase_split=0.0))))
+    C.append(("hyb_all_early", "hybrid", thg, disp, 1.0, 200, 16, 30, 27, dict(schedules=S(phase_split=1.0))))
+    C.append(("hyb_fconst", "hybrid", thg, disp, 1.0, 200, 16, 30, 28,
+              dict(de_params=optimizer.DEParams(f=0.05, f_min=0.05, f_max=0.05))))
+    C.append(("hyb_zero_bounds", "hybrid", thg, disp, 1.0, 64, 8, 10, 29,
+              dict(de_params=optimizer.DEParams(x_min=0.0, x_max=0.0))))
+    C.append(("hyb_k3_d1", "hybrid", thg, disp, 1.0, 200, 16, 30, 30,
+              dict(gwo_params=optimizer.GWOParams(leader_count=3))))
+    C.append(("hyb_k4_d06", "hybrid", thg, disp, 1.0, 200, 16, 30, 31,
+              dict(gwo_params=optimizer.GWOParams(discreteness_factor=0.6))))
     return C
 
 
