@@ -76,10 +76,11 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise QpmError(f"{LIB_PATH} is missing: build it with `python -m paper_2511_01255_b200.build` "
+    path = os.environ.get("QPM_LIB", LIB_PATH)  # A/B builds of the same library (development)
+    if not os.path.exists(path):
+        raise QpmError(f"{path} is missing: build it with `python -m paper_2511_01255_b200.build` "
                        "(there is no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     sig = {
         "qpm_last_error": (ctypes.c_char_p, []),
