@@ -273,11 +273,35 @@ __device__ __forceinline__ uint64_t xs_fma(uint64_t z, uint32_t m) {
     const uint32_t nhi = hi ^ __umulhi(hi, m);
     return ((uint64_t)nhi << 32) | nlo;
 }
-// splitmix64 up to (excluding) the last multiply: position p1 = pos + 1
+// z ^= z >> s, pipe placement by MODE.  ncu (C2 late generation): IMAD.HI and
+// IMAD.WIDE occupy the FMA-heavy pipe twice as long as a plain IMAD, and
+// with every xorshift there (MODE 2) FMA-heavy was the busiest pipe (61 % of
+// elapsed vs ALU 41 %).  MODE 0: all ALU (two SHF, two LOP3); MODE 1: low
+// word by a funnel shift on the ALU, high word by IMAD.HI; MODE 2: xs_fma.
+#ifndef QPM_XS30
+#define QPM_XS30 0
+#endif
+#ifndef QPM_XS27
+#define QPM_XS27 0
+#endif
+template <int MODE>
+__device__ __forceinline__ uint64_t xs_mode(uint64_t z, int s, uint32_t m) {
+    if (MODE == 0) return z ^ (z >> s);
+    if (MODE == 2) return xs_fma(z, m);
+    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+    const uint32_t nlo = lo ^ __funnelshift_r(lo, hi, s);
+    const uint32_t nhi = hi ^ __umulhi(hi, m);
+    return ((uint64_t)nhi << 32) | nlo;
+}
+// splitmix64 up to (excluding) the last multiply, from the counter state
+// z = key + (pos + 1) * GOLD
+__device__ __forceinline__ uint64_t mix_pre2z(uint64_t z, const RunConsts &c) {
+    z = xs_mode<QPM_XS30>(z, 30, c.m4) * kMix1;  // z ^= z >> 30
+    return xs_mode<QPM_XS27>(z, 27, c.m32);      // z ^= z >> 27
+}
+// the same at position p1 = pos + 1
 __device__ __forceinline__ uint64_t mix_pre2(uint64_t key, uint32_t p1, const RunConsts &c) {
-    uint64_t z = key + (uint64_t)p1 * kGold;
-    z = xs_fma(z, c.m4) * kMix1;  // z ^= z >> 30
-    return xs_fma(z, c.m32);      // z ^= z >> 27
+    return mix_pre2z(key + (uint64_t)p1 * kGold, c);
 }
 __device__ __forceinline__ uint32_t mix_hi2(uint64_t x) {  // high word of x * kMix2
     const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
@@ -306,8 +330,18 @@ __device__ __forceinline__ bool lt_hi(const Thr &t, uint32_t h, bool &tie, uint3
     tie |= ho == hl;
     return ho < hl;
 }
+// the same decision without forming h ^ (h >> 31): that xor only touches bit
+// 0, so with H = hl & ~1 the high-word compare ho < hl is h < H whenever the
+// top 31 bits differ; equal top bits (h in {H, H + 1}, probability 2^-31)
+// count as a tie and go to the exact path.  Three ALU ops, no IMAD.HI.
+__device__ __forceinline__ bool lt_top(uint32_t H, uint32_t h, bool &tie) {
+    tie |= h - H < 2u;
+    return h < H;
+}
+__device__ __forceinline__ uint32_t top_thr(const Thr &t) { return (uint32_t)(t.le >> 32) & ~1u; }
 
 __global__ void k_plan_rows(RunConsts c, PlanArgs a) {
+    QTRACE(6);
     const int64_t g = a.st->g_plan;
     if (g > c.G) return;
     const int64_t b = g & 1;
@@ -324,23 +358,25 @@ __global__ void k_plan_rows(RunConsts c, PlanArgs a) {
 
 template <bool EXACT>
 __device__ __forceinline__ bool draw_lt(const RunConsts &c, const Thr &t, uint64_t x, uint32_t h, bool &tie) {
-    return EXACT ? passes_hi(t, x, h) : lt_hi(t, h, tie, c.m2);
+    return EXACT ? passes_hi(t, x, h) : lt_top(top_thr(t), h, tie);
 }
 
-// The first two wolf draws of one gene (stream position p0 = m + 1 + D + j,
-// plus one) as plane bits P0..P2: social; then pick (social) or disturbed /
-// flipped (row 2 early, row 5 late).  The third draw (state or plus level)
-// matters only for a minority of genes, and which ones depends on the
-// leaders, so k_gwo_apply draws it for exactly those genes.  Straight-line
-// code (selects only), so the draws of several genes interleave.  EXACT =
-// false decides every compare on the high word and sets `tie` when one tied;
-// the caller then redoes the gene with EXACT = true.
+// The first two wolf draws of one gene as plane bits P0..P2: social; then
+// pick (social) or disturbed / flipped (row 2 early, row 5 late).  The third
+// draw (state or plus level) matters only for a minority of genes, and which
+// ones depends on the leaders, so k_gwo_apply draws it for exactly those
+// genes.  Straight-line code (selects only), so the draws of several genes
+// interleave.  EXACT = false decides every compare on the high word and sets
+// `tie` when one tied; the caller then redoes the gene with EXACT = true.
+// zs is the social draw's counter state key + p0 * GOLD (p0 = m + 1 + D + j,
+// plus one); the second draw sits gsoc = D * GOLD (social: pick row) or gnon =
+// 2D * GOLD (early: disturb row) / 5D * GOLD (late: flip row) further on.
 template <int K, bool EXACT>
-__device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p0,
-                                              uint32_t D, bool early, bool &tie) {
-    const uint64_t x1 = mix_pre2(key, p0, c);
+__device__ __forceinline__ uint32_t wolf_code_z(const RunConsts &c, const GenThr &t, uint64_t zs, uint64_t gsoc,
+                                                uint64_t gnon, bool early, bool &tie) {
+    const uint64_t x1 = mix_pre2z(zs, c);
     const bool soc = draw_lt<EXACT>(c, t.sl, x1, mix_hi2(x1), tie);
-    const uint64_t x2 = mix_pre2(key, p0 + (soc ? D : (early ? 2 * D : 5 * D)), c);
+    const uint64_t x2 = mix_pre2z(zs + (soc ? gsoc : gnon), c);
     const uint32_t h2 = mix_hi2(x2);
     uint32_t pick;
     if (K == 4) {
@@ -352,6 +388,12 @@ __device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &
     }
     const bool f2 = draw_lt<EXACT>(c, early ? t.dist : t.flip, x2, h2, tie);
     return soc ? 1u | (pick << 1) : (f2 ? 2u : 0u);
+}
+template <int K, bool EXACT>
+__device__ __forceinline__ uint32_t wolf_code(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p0,
+                                              uint32_t D, bool early, bool &tie) {
+    return wolf_code_z<K, EXACT>(c, t, key + (uint64_t)p0 * kGold, (uint64_t)D * kGold,
+                                 (uint64_t)(early ? 2 * D : 5 * D) * kGold, early, tie);
 }
 
 // planes P0..P2 of one 32-gene word from each lane's code; lane `writer`
@@ -415,7 +457,10 @@ __global__ void __launch_bounds__(kRowThreads) k_plan_wolf(RunConsts c, PlanArgs
     }
 }
 
-__global__ void k_plan_bump(EngineState *st) { st->g_plan += 1; }
+__global__ void k_plan_bump(EngineState *st) {
+    QTRACE(7);
+    st->g_plan += 1;
+}
 
 // ---------------------------------------------------------------- init
 __global__ void __launch_bounds__(kRowThreads) k_init_population(RunConsts c, double *__restrict__ genome,
@@ -524,8 +569,12 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const GenThr t = r.t;
     const bool early = t.early != 0;
     const uint32_t p_mask = r.p_mask;
-    const uint32_t p_wolf = p_mask + (uint32_t)c.D;  // m + 1 + D + j, plus one
     const int D = (int)c.D;
+    // counter states advance by constant multiples of GOLD: one 64-bit add
+    // per draw instead of a 32 x 64 product (the wolf block starts D later)
+    const uint64_t gD = (uint64_t)(uint32_t)D * kGold;
+    const uint64_t gnon = (uint64_t)(uint32_t)(early ? 2 * D : 5 * D) * kGold;
+    const uint32_t Hcr = top_thr(c.thr_cr);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     constexpr int kSteps = 2;               // 64-gene warp steps per batch (registers)
@@ -539,6 +588,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
         // stores, then the wolf draws (other warps' loads are in flight)
         uint32_t mb[kSteps];
         bool tie = false;
+        const uint64_t zb = key + (uint64_t)(p_mask + (uint32_t)(jb + lane)) * kGold;  // mask draw of gene jb + lane
 #pragma unroll
         for (int st = 0; st < kSteps; ++st) {
             mb[st] = 0u;
@@ -546,8 +596,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             for (int q = 0; q < 2; ++q) {
                 const int jj = jb + st * kSpan + lane + 32 * q;
                 bool ti = false;
-                const uint64_t x = mix_pre2(key, p_mask + (uint32_t)jj, c);
-                const bool take = lt_hi(c.thr_cr, mix_hi2(x), ti, c.m2) || jj == jr;
+                const uint64_t x = mix_pre2z(zb + (uint64_t)(st * kSpan + 32 * q) * kGold, c);
+                const bool take = lt_top(Hcr, mix_hi2(x), ti) || jj == jr;
                 if (FULL || jj < D) {
                     mb[st] |= take ? 1u << q : 0u;
                     tie |= ti;
@@ -621,7 +671,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 for (int q = 0; q < 2; ++q) {
                     const int jj = jb + st * kSpan + lane + 32 * q;
                     bool ti = false;
-                    code[st][q] = wolf_code<K, false>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, early, ti);
+                    code[st][q] = wolf_code_z<K, false>(c, t, zb + (uint64_t)(st * kSpan + 32 * q) * kGold + gD, gD,
+                                                        gnon, early, ti);
                     if (!FULL && jj >= D) code[st][q] = 0u, ti = false;
                     wtie |= ti;
                 }
@@ -634,8 +685,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                         const int jj = jb + st * kSpan + lane + 32 * q;
                         bool ti = false;
                         if (FULL || jj < D)
-                            code[st][q] =
-                                wolf_code<K, true>(c, t, key, p_wolf + (uint32_t)jj, (uint32_t)D, early, ti);
+                            code[st][q] = wolf_code_z<K, true>(
+                                c, t, zb + (uint64_t)(st * kSpan + 32 * q) * kGold + gD, gD, gnon, early, ti);
                     }
                 }
             }
@@ -673,7 +724,9 @@ __device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const Tria
 // recomputes the trials of foreign rows that won (multi-GPU)
 template <int K>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts c, TrialArgs a) {
+    QTRACE(0);
     pdl_wait();
+    QTRACE_STARTED();
     const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
     const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
@@ -735,7 +788,9 @@ __global__ void k_commit_cand_bits(RunConsts c, TrialArgs a) {
 // genes).  Leaders do not move (optimizer.py:454).
 template <int K>
 __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
+    QTRACE(4);
     pdl_wait();
+    QTRACE_STARTED();
     // one CTA row per individual: the row-level decisions are CTA-uniform
     const int64_t i = a.row_lo + blockIdx.y;
     const int w = (int)(blockIdx.x * kApplyThreads + threadIdx.x);
@@ -901,10 +956,9 @@ __device__ __forceinline__ bool better(const Cand &a, const Cand &b) {
 // top-K by (-value, index) (parexec.reduce_best), whole CTA.  (-value,
 // index) is a strict total order on the elements, so the top-K set and its
 // order are unique: any merge structure gives the same, exact answer.  Each
-// thread keeps a sorted 4-slot list (unused slots are sentinels, index -1);
-// two sorted lists merge by a bitonic network (4 compare-selects, then a
-// 4-element bitonic sort), lanes merge by an xor butterfly, and warp 0
-// merges the per-warp lists.
+// thread keeps a sorted 4-slot list (unused slots are sentinels, index -1)
+// by insertion; each warp takes the top-k of its lanes' lists by k argmax
+// rounds over the list heads, and warp 0 does the same over the warps' lists.
 constexpr int kTopSlots = 4;
 
 __device__ __forceinline__ void cswap(Cand &a, Cand &b) {  // a := better of the two
@@ -921,32 +975,35 @@ __device__ __forceinline__ void topk_insert(Cand (&L)[kTopSlots], Cand e) {
     for (int t = 0; t < kTopSlots; ++t) cswap(L[t], e);
 }
 
-// L := top-4 of L and the list in lane (lane ^ off)
-__device__ __forceinline__ void topk_merge_xor(Cand (&L)[kTopSlots], int off) {
-    Cand o[kTopSlots];
+// top-k (k <= 4, warp-uniform) of the union of the lanes' sorted lists: k
+// rounds of a warp argmax over the list heads (xor butterfly, so every lane
+// sees the winner); the lane whose head won pops it.  About half the
+// instructions of merging whole 4-lists at every butterfly level, which
+// dominated the single-CTA selection kernels (ncu: ~700 warp instructions
+// per warp, issue-bound on one SM).
+__device__ __forceinline__ void topk_warp_rounds(Cand (&L)[kTopSlots], int k, Cand (&R)[kTopSlots]) {
 #pragma unroll
     for (int t = 0; t < kTopSlots; ++t) {
-        o[t].v = __shfl_xor_sync(0xffffffffu, L[t].v, off);
-        o[t].i = __shfl_xor_sync(0xffffffffu, L[t].i, off);
-    }
-    // the better of L[t] and o[3-t] for every t is the top-4 of the union,
-    // as a bitonic sequence; two compare-swap stages sort it
+        R[t] = Cand{0.0, -1};
+        if (t >= k) continue;
+        Cand b = L[0];
 #pragma unroll
-    for (int t = 0; t < kTopSlots; ++t) {
-        const Cand &x = o[kTopSlots - 1 - t];
-        const bool take = better(x, L[t]);
-        L[t].v = take ? x.v : L[t].v;
-        L[t].i = take ? x.i : L[t].i;
+        for (int off = 16; off > 0; off >>= 1) {
+            Cand o;
+            o.v = __shfl_xor_sync(0xffffffffu, b.v, off);
+            o.i = __shfl_xor_sync(0xffffffffu, b.i, off);
+            const bool tk = better(o, b);
+            b.v = tk ? o.v : b.v;
+            b.i = tk ? o.i : b.i;
+        }
+        R[t] = b;
+        if (L[0].i == b.i) {  // indices are unique: this lane's head won (or both are sentinels)
+            L[0] = L[1];
+            L[1] = L[2];
+            L[2] = L[3];
+            L[3] = Cand{0.0, -1};
+        }
     }
-    cswap(L[0], L[2]);
-    cswap(L[1], L[3]);
-    cswap(L[0], L[1]);
-    cswap(L[2], L[3]);
-}
-
-__device__ __forceinline__ void topk_warp(Cand (&L)[kTopSlots]) {
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) topk_merge_xor(L, off);
 }
 
 // the CTA's top-k (k <= 4) of the per-thread lists into out[0..k); every
@@ -956,23 +1013,24 @@ __device__ void block_topk_lists(Cand (&L)[kTopSlots], int k, int32_t *out) {
     __shared__ int32_t s_i[32][kTopSlots];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = (int)(blockDim.x >> 5);
-    topk_warp(L);
+    Cand R[kTopSlots];
+    topk_warp_rounds(L, k, R);
     if (lane == 0) {
 #pragma unroll
         for (int t = 0; t < kTopSlots; ++t) {
-            s_v[warp][t] = L[t].v;
-            s_i[warp][t] = L[t].i;
+            s_v[warp][t] = R[t].v;
+            s_i[warp][t] = R[t].i;
         }
     }
     __syncthreads();
     if (warp == 0) {
 #pragma unroll
         for (int t = 0; t < kTopSlots; ++t) L[t] = lane < nwarps ? Cand{s_v[lane][t], s_i[lane][t]} : Cand{0.0, -1};
-        topk_warp(L);
-        if (lane < k) {
+        topk_warp_rounds(L, k, R);
+        if (lane == 0) {
 #pragma unroll
             for (int t = 0; t < kTopSlots; ++t)
-                if (t == lane) out[t] = L[t].i;
+                if (t < k) out[t] = R[t].i;
         }
     }
     __syncthreads();
@@ -1050,7 +1108,9 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, Engine
                                                              const double *cand,
                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                              int32_t *__restrict__ spare_of) {
+    QTRACE(3);
     pdl_wait();
+    QTRACE_STARTED();
     Cand L[kTopSlots];
 #pragma unroll
     for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
@@ -1090,6 +1150,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
                                                               uint8_t *__restrict__ slot_bin,
                                                               double *__restrict__ scratch, SumTree tr,
                                                               double *__restrict__ trace) {
+    QTRACE(5);
     const int64_t n = c.NP;
     // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
     // then the pairwise-sum tree (values, leaf offsets, children, levels)
@@ -1107,6 +1168,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     for (int t = threadIdx.x; t < 2 * (c.n_leaf - 1); t += blockDim.x) ts.kid[t] = tr.kid[t];
     for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
     pdl_wait();
+    QTRACE_STARTED();
     __shared__ EngineState s_state;
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(st);
@@ -1781,6 +1843,11 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
             e->wolf_in_planner = strcmp(v, "planner") == 0;
             e->wolf_mixed = strcmp(v, "mixed") == 0;
         }
+        // wolf planes on the side stream are drawn after the trial: forked at
+        // the start of the generation, C2 traces differed from run to run
+        // (tools/gen_sweep.py, B200, with and without PDL), after the trial
+        // they never did
+        if (e->wolf_in_planner) e->plan_after_trial = true;
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
     }
     HostTree ht = build_tree(c.NP);
@@ -2209,6 +2276,21 @@ int qpm_engine_fitness_ptr(qpm_engine *h, double **fit_dev) {
     QPM_ARG_CHECK(h && fit_dev, "engine, out");
     *fit_dev = h->e->fit;
     return QPM_OK;
+}
+
+// development timeline (-DQPM_TRACE builds; -2 otherwise): reset, or copy
+// this translation unit's log [kTraceIds][kTraceLen][3] (globaltimer ns) and
+// per-id launch counts.  Not part of include/qpm_b200.h.
+int qpm_dev_trace_engine(int reset, unsigned long long *log, unsigned int *launches) {
+#ifdef QPM_TRACE
+    if (reset) return qpm::trace_reset_tu();
+    return qpm::trace_read_tu(log, launches);
+#else
+    (void)reset;
+    (void)log;
+    (void)launches;
+    return -2;
+#endif
 }
 
 }  // extern "C"

@@ -403,18 +403,27 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
         bulk_load(tab, qtl + c0 * kChunkEntries, kChunkBytes, &bar[0]);
         if (n > 1) bulk_load(tab + kChunkEntries, qtl + (c0 + 1) * kChunkEntries, kChunkBytes, &bar[1]);
     }
+    QTRACE(1);
     pdl_wait();
+    QTRACE_STARTED();
     const uint4 *rb =
         reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? __ldcg(row_index + r) : r) : 0) * W);
     // The 32 quads of a chunk are scanned as 4 independent sub-chains (one
     // per bit word, 8 quads each) interleaved for instruction-level
     // parallelism, then stitched in a fixed order: (c0 . c1) . (c2 . c3).
     Seg run = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    uint4 w4 = active ? __ldcg(rb + c0) : make_uint4(0, 0, 0, 0);
+    // the row's sign words, four chunks ahead (a C2 segment is four chunks:
+    // one L2 round trip instead of one per chunk)
+    uint4 wq[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) wq[p] = active && p < n ? __ldcg(rb + c0 + p) : make_uint4(0, 0, 0, 0);
     for (int k = 0; k < n; ++k) {
         const int buf = k & 1;
-        const uint32_t words[4] = {w4.x, w4.y, w4.z, w4.w};
-        if (k + 1 < n) w4 = active ? __ldcg(rb + c0 + k + 1) : make_uint4(0, 0, 0, 0);  // next chunk's bits
+        const uint32_t words[4] = {wq[0].x, wq[0].y, wq[0].z, wq[0].w};
+        wq[0] = wq[1];
+        wq[1] = wq[2];
+        wq[2] = wq[3];
+        wq[3] = active && k + 4 < n ? __ldcg(rb + c0 + k + 4) : make_uint4(0, 0, 0, 0);
         mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
         const double2 *tb = tab + buf * kChunkEntries;
         Seg ch[4];
@@ -489,7 +498,9 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
     const double *part, int S, int64_t rows, int n_wl, const double2 *__restrict__ w,
     const double2 *__restrict__ h, int thg, double scale, int multi, double g0, double beta,
     double *__restrict__ gains, double *__restrict__ out) {
+    QTRACE(2);
     pdl_wait();
+    QTRACE_STARTED();
     const int64_t r = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
@@ -991,6 +1002,21 @@ int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows
 
 int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out_dev, void *stream) {
     return launch_reduce_best(values_dev, n, k, idx_out_dev, (cudaStream_t)stream);
+}
+
+// development timeline (-DQPM_TRACE builds; -2 otherwise): reset, or copy
+// this translation unit's log [kTraceIds][kTraceLen][3] (globaltimer ns) and
+// per-id launch counts.  Not part of include/qpm_b200.h.
+int qpm_dev_trace_fitness(int reset, unsigned long long *log, unsigned int *launches) {
+#ifdef QPM_TRACE
+    if (reset) return qpm::trace_reset_tu();
+    return qpm::trace_read_tu(log, launches);
+#else
+    (void)reset;
+    (void)log;
+    (void)launches;
+    return -2;
+#endif
 }
 
 }  // extern "C"

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <utility>
+#include <vector>
 
 #include "../../include/qpm_b200.h"
 
@@ -107,6 +108,70 @@ int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64
 // dependents observe stale data in about one C2 run in eight, and the early
 // residents slowed the primary down.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Device-side kernel timeline (development builds with -DQPM_TRACE only):
+// thread 0 of every CTA stamps %globaltimer at entry, after pdl_wait and at
+// exit; the last CTA of a launch logs (min entry, min start, max exit).  The
+// graph-replayed generation can then be read back as it really ran (PDL
+// overlap included), which CUDA events between stages cannot show.
+// Ids: 0 de_trial, 1 fit_fast, 2 fit_finish, 3 select_topk, 4 gwo_apply,
+// 5 select_stats, 6 plan_rows, 7 plan_bump.  Each translation unit has its own log.
+constexpr int kTraceIds = 8, kTraceLen = 4096;
+#ifdef QPM_TRACE
+struct TraceAcc {
+    unsigned long long t_entry, t_start, t_end;
+    unsigned int done, launch;
+};
+static __device__ TraceAcc g_tacc[kTraceIds];
+static __device__ unsigned long long g_tlog[kTraceIds][kTraceLen][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct TraceScope {
+    int id;
+    __device__ __forceinline__ static bool lead() { return threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0; }
+    __device__ explicit TraceScope(int i) : id(i) {
+        if (lead()) atomicMin(&g_tacc[id].t_entry, gtimer());
+    }
+    __device__ void started() {
+        if (lead()) atomicMin(&g_tacc[id].t_start, gtimer());
+    }
+    __device__ ~TraceScope() {
+        if (!lead()) return;
+        atomicMax(&g_tacc[id].t_end, gtimer());
+        __threadfence();
+        const unsigned n = atomicAdd(&g_tacc[id].done, 1u);
+        if (n + 1 == gridDim.x * gridDim.y * gridDim.z) {
+            __threadfence();
+            const unsigned L = g_tacc[id].launch % kTraceLen;
+            g_tlog[id][L][0] = atomicExch(&g_tacc[id].t_entry, ~0ULL);
+            g_tlog[id][L][1] = atomicExch(&g_tacc[id].t_start, ~0ULL);
+            g_tlog[id][L][2] = atomicExch(&g_tacc[id].t_end, 0ULL);
+            g_tacc[id].done = 0;
+            g_tacc[id].launch += 1;
+            __threadfence();
+        }
+    }
+};
+#define QTRACE(id) ::qpm::TraceScope qtrace_scope_(id)
+#define QTRACE_STARTED() qtrace_scope_.started()
+// host: reset the accumulators / copy the log of this translation unit
+static inline int trace_reset_tu() {
+    std::vector<TraceAcc> init(kTraceIds, TraceAcc{~0ULL, ~0ULL, 0ULL, 0u, 0u});
+    return cudaMemcpyToSymbol(g_tacc, init.data(), sizeof(TraceAcc) * kTraceIds) == cudaSuccess ? 0 : -1;
+}
+static inline int trace_read_tu(unsigned long long *log, unsigned int *launches) {
+    std::vector<TraceAcc> acc(kTraceIds);
+    if (cudaMemcpyFromSymbol(acc.data(), g_tacc, sizeof(TraceAcc) * kTraceIds) != cudaSuccess) return -1;
+    for (int i = 0; i < kTraceIds; ++i) launches[i] = acc[i].launch;
+    return cudaMemcpyFromSymbol(log, g_tlog, sizeof(g_tlog)) == cudaSuccess ? 0 : -1;
+}
+#else
+#define QTRACE(id)
+#define QTRACE_STARTED()
+#endif
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -80,3 +80,17 @@ def test_repeated_runs_are_identical(q, monkeypatch):
         del eng
     for t in traces[1:]:
         assert np.array_equal(t, traces[0])
+
+
+@pytest.mark.parametrize("env", [{}, {"QPM_WOLF": "planner"}, {"QPM_WOLF": "planner", "QPM_PDL": "0"},
+                                 {"QPM_WOLF": "mixed"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+def test_c2_shape_runs_match_default(q, monkeypatch, env):
+    """The C2 shape (NP 1024, D 10^4) for 600 generations, twice per schedule:
+    both runs equal the default schedule's trace.  At this size a planner
+    forked at the start of the generation gave run-to-run differences that
+    the small cases above did not show (it now forks after the trial)."""
+    base = _trace(q, monkeypatch, {}, D=10_000, NP=1024, G=600)[0]
+    for _ in range(2):
+        got = _trace(q, monkeypatch, env, D=10_000, NP=1024, G=600)[0]
+        assert np.array_equal(got, base)
