@@ -440,9 +440,12 @@ __device__ __forceinline__ void wolf_chunk(const RunConsts &c, const GenThr &t, 
 
 // the wolf planes of generation g_plan for this rank's rows on the side
 // stream (QPM_WOLF=planner)
-template <int K>
+// NOW: the current generation's planes instead (QPM_WOLF=side: forked after
+// the trial, joined before k_gwo_apply)
+template <int K, bool NOW = false>
 __global__ void __launch_bounds__(kRowThreads) k_plan_wolf(RunConsts c, PlanArgs a) {
-    const int64_t g = a.st->g_plan;
+    QTRACE(8);
+    const int64_t g = NOW ? a.st->g : a.st->g_plan;
     if (g > c.G) return;
     const int64_t b = g & 1;
     const GenThr t = a.gthr[g];
@@ -511,7 +514,8 @@ struct TrialArgs {
     uint8_t *slot_bin;
     double *genome;
     uint32_t *bits;
-    uint32_t *cbits;  // [NP][W] wolf candidates staged for the all-gather (multi-GPU), else null
+    uint32_t *cbits;  // [NP][W] the generation's candidate sign rows, dense by individual: scored from
+                      // here (no slot indirection) and, multi-GPU, all-gathered from here
 };
 
 // The trial of row i over genes [jc, jc + kDeChunk) with the crossover mask
@@ -526,6 +530,7 @@ struct TrialRow {
     RowRef xi, x1, x2, x3;
     double *out;
     uint32_t *bout, *prow;
+    uint32_t *dout;  // the candidate's dense row (own rows), null when recomputing foreign rows
     uint64_t key;
     int64_t out_slot;
     double F;
@@ -549,6 +554,7 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
     r.out_slot = a.spare_of[i];
     r.out = a.genome + r.out_slot * c.Dp;
     r.bout = a.bits + r.out_slot * c.W;
+    r.dout = a.filter || !a.cbits ? nullptr : a.cbits + i * c.W;
     r.prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
     r.p_mask = (uint32_t)pk.w + 2;  // m + 1 + j, plus one
     r.F = a.st->F;
@@ -660,7 +666,10 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             }
             const uint32_t w0 = __ballot_sync(0xffffffffu, neg[0]);
             const uint32_t w1 = __ballot_sync(0xffffffffu, neg[1]);
-            if (lane < 2) bout[(j64 >> 5) + lane] = lane ? w1 : w0;
+            if (lane < 2) {
+                bout[(j64 >> 5) + lane] = lane ? w1 : w0;
+                if (r.dout) r.dout[(j64 >> 5) + lane] = lane ? w1 : w0;
+            }
         }
         if (K > 0) {  // after the stores: the load registers are free again
             uint32_t code[kSteps][2];
@@ -877,7 +886,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
     }
     const uint32_t word = wolf_word<K>(ld, pl, early) & valid;
     a.bits[(int64_t)a.spare_of[i] * c.W + w] = word;  // scored from the spare slot
-    if (a.cbits) a.cbits[i * c.W + w] = word;          // staged for the all-gather
+    a.cbits[i * c.W + w] = word;                       // scored from here; multi-GPU: all-gathered
 }
 
 // ---------------------------------------------------------------- run_gwo
@@ -1377,6 +1386,10 @@ struct Engine {
     bool plan_after_trial = false;  // fork the planner after k_de_trial (QPM_PLAN_FORK=trial)
     bool wolf_in_planner = false;   // wolf planes on the side stream (QPM_WOLF=planner)
     bool wolf_mixed = false;        // wolf planes in separate CTAs of the trial kernel (QPM_WOLF=mixed)
+    bool wolf_side = false;         // this generation's planes on the side stream during the DE fitness (QPM_WOLF=side)
+    cudaEvent_t ev_wfork = nullptr, ev_wjoin = nullptr;
+    int topk_threads = kCtaThreads;   // k_select_topk block (QPM_TOPK_THREADS)
+    int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
     int64_t g_done = 0;
     bool initialized = false;
@@ -1482,7 +1495,7 @@ static size_t stats_smem_bytes(const RunConsts &c) {
 }
 
 static int launch_select_stats(Engine *e, int mode, cudaStream_t s) {
-    QPM_CUDA_TRY(launch_k(e->pdl, k_select_stats, dim3(1), dim3(kCtaThreads), stats_smem_bytes(e->c), s, e->c, mode,
+    QPM_CUDA_TRY(launch_k(e->pdl, k_select_stats, dim3(1), dim3(e->stats_threads), stats_smem_bytes(e->c), s, e->c, mode,
                           e->st, (const double *)e->sched, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
                           e->slot_bin, e->scratch, e->tree, e->trace));
     return QPM_OK;
@@ -1503,7 +1516,7 @@ static TrialArgs trial_args(const Engine *e, int64_t row_lo, int64_t n_rows) {
     a.keys = e->keys;
     a.jrand = e->jrand;
     a.planes = e->planes;
-    a.cbits = e->world > 1 ? e->cbits : nullptr;
+    a.cbits = e->cbits;
     a.slot_of = e->slot_of;
     a.spare_of = e->spare_of;
     a.slot_bin = e->slot_bin;
@@ -1663,7 +1676,8 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         // graph's root node would otherwise overlap the previous replay's
         // tail, including its planner branch
         const unsigned items = (unsigned)(n_own * de_chunks);
-        if (!hybrid || e->wolf_in_planner)
+        const bool wolf_side = hybrid && e->wolf_side && !sharded;
+        if (!hybrid || e->wolf_in_planner || wolf_side)
             QPM_CUDA_TRY(launch_k(false, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, own));
         else if (e->wolf_mixed)
             QPM_CUDA_TRY(launch_k(false, c.k == 4 ? k_de_trial_mixed<4> : k_de_trial_mixed<3>, dim3(2 * items),
@@ -1673,9 +1687,22 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
                                   s, c, own));
         QPM_LAUNCH_CHECK();
         *n += 1;
+        if (wolf_side) {  // the planes of this generation, concurrent with the DE fitness and selection
+            QPM_CUDA_TRY(cudaEventRecord(e->ev_wfork, s));
+            QPM_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_wfork, 0));
+            const PlanArgs pa = plan_args(e);
+            if (c.k == 4)
+                k_plan_wolf<4, true><<<e->plan_grid, kRowThreads, 0, e->side>>>(c, pa);
+            else
+                k_plan_wolf<3, true><<<e->plan_grid, kRowThreads, 0, e->side>>>(c, pa);
+            QPM_LAUNCH_CHECK();
+            QPM_CUDA_TRY(cudaEventRecord(e->ev_wjoin, e->side));
+            *n += 1;
+        }
         if (e->plan_after_trial && (rc = fork())) return rc;
         mark("fitness_de");
-        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n, e->pdl);
+        return launch_fitness(e->prob, &e->fs, e->cbits + lo * c.W, c.W, nullptr, n_own, e->cand + lo, e->P.fitness_mode, s, n,
+                              e->pdl);
     }
     if (phase == 1) {
         if (sharded) {
@@ -1693,8 +1720,9 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             return QPM_OK;
         }
         mark("select_topk");
-        QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3(1), dim3(kCtaThreads), 0, s, c, e->st,
+        QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3(1), dim3(e->topk_threads), 0, s, c, e->st,
                               (const double *)e->cand, e->fit, e->slot_of, e->spare_of));
+        if (e->wolf_side && !sharded) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
         QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
                               dim3((unsigned)((c.W + kApplyThreads - 1) / kApplyThreads), (unsigned)n_own),
@@ -1702,7 +1730,8 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         QPM_LAUNCH_CHECK();
         *n += 2;
         mark("fitness_gwo");
-        return launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n, e->pdl);
+        return launch_fitness(e->prob, &e->fs, e->cbits + lo * c.W, c.W, nullptr, n_own, e->cand + lo, e->P.fitness_mode, s, n,
+                              e->pdl);
     }
     // phase 2 (hybrid)
     if (sharded) {
@@ -1742,6 +1771,8 @@ static void engine_free(Engine *e) {
     if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
+    if (e->ev_wfork) cudaEventDestroy(e->ev_wfork);
+    if (e->ev_wjoin) cudaEventDestroy(e->ev_wjoin);
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
     for (auto &pb : e->allocs) dev_cache_release(pb.first, pb.second);
@@ -1793,7 +1824,9 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
         if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
             cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e->ev_wfork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e->ev_wjoin, cudaEventDisableTiming) != cudaSuccess) {
             set_error("planner stream/event creation failed");
             engine_free(e);
             return QPM_ERR_CUDA;
@@ -1842,6 +1875,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (const char *v = getenv("QPM_WOLF")) {
             e->wolf_in_planner = strcmp(v, "planner") == 0;
             e->wolf_mixed = strcmp(v, "mixed") == 0;
+            e->wolf_side = strcmp(v, "side") == 0;
         }
         // wolf planes on the side stream are drawn after the trial: forked at
         // the start of the generation, C2 traces differed from run to run
@@ -1849,6 +1883,11 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         // they never did
         if (e->wolf_in_planner) e->plan_after_trial = true;
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
+        auto cta_knob = [](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
+            if (const char *v = getenv(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
+        };
+        cta_knob("QPM_TOPK_THREADS", e->topk_threads);
+        cta_knob("QPM_STATS_THREADS", e->stats_threads);
     }
     HostTree ht = build_tree(c.NP);
     c.n_leaf = (int32_t)ht.leaf_off.size() - 1;
@@ -1882,7 +1921,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->bits, (size_t)2 * NP * c.W);
     QPM_ALLOC(e->slot_bin, (size_t)2 * NP);
     QPM_ALLOC(e->planes, P->algorithm == QPM_ALGO_HYBRID ? (size_t)2 * NP * c.W * kPlanes : 16);
-    QPM_ALLOC(e->cbits, P->algorithm == QPM_ALGO_HYBRID ? (size_t)NP * c.W : 16);
+    QPM_ALLOC(e->cbits, P->algorithm != QPM_ALGO_GWO ? (size_t)NP * c.W : 16);
     QPM_ALLOC(e->gthr, (size_t)(P->G + 1));
     QPM_ALLOC(e->slot_of, NP);
     QPM_ALLOC(e->spare_of, NP);

@@ -375,7 +375,8 @@ __global__ void __launch_bounds__(kSpecThreads) k_spectrum(int thg, double t, in
 
 constexpr int kChunkEntries = kQuadsPerChunk * kQuadEntries;  // 768 double2 = 12 KB
 constexpr uint32_t kChunkBytes = kChunkEntries * sizeof(double2);
-constexpr int kFitSmem = 2 * kChunkBytes;  // double-buffered chunks (dynamic shared memory)
+constexpr int kFitBufs = 4;  // table chunks in flight: a C2 segment (4 chunks) is staged at once
+constexpr int kFitSmem = kFitBufs * kChunkBytes;  // dynamic shared memory (48 KB)
 
 template <bool THG>
 __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,
@@ -383,8 +384,8 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
                                                           const uint32_t *bits, int64_t W,
                                                           const int32_t *row_index, int64_t rows,
                                                           double *__restrict__ part) {
-    extern __shared__ __align__(128) double2 tab[];  // 2 x 12 KB
-    __shared__ __align__(8) uint64_t bar[2];
+    extern __shared__ __align__(128) double2 tab[];  // kFitBufs x 12 KB
+    __shared__ __align__(8) uint64_t bar[kFitBufs];
     const int s = blockIdx.x;
     const int lam = blockIdx.z;
     const int tid = threadIdx.x;
@@ -394,18 +395,23 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
     const int64_t c0 = (int64_t)s * seg_chunks;
     const int n = (int)((c0 + seg_chunks < nchunks ? c0 + seg_chunks : nchunks) - c0);
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int b = 0; b < kFitBufs; ++b) mbar_init(&bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {  // the tables are the problem's own: staged before waiting on the predecessor
-        bulk_load(tab, qtl + c0 * kChunkEntries, kChunkBytes, &bar[0]);
-        if (n > 1) bulk_load(tab + kChunkEntries, qtl + (c0 + 1) * kChunkEntries, kChunkBytes, &bar[1]);
+    // the tables are the problem's own: staged before waiting on the
+    // predecessor, kFitBufs chunks deep (a 2-deep ring left the ~1 us L2->smem
+    // latency exposed on every chunk: compute per chunk is ~0.3 us)
+    if (tid == 0) {
+#pragma unroll
+        for (int b = 0; b < kFitBufs; ++b)
+            if (b < n) bulk_load(tab + b * kChunkEntries, qtl + (c0 + b) * kChunkEntries, kChunkBytes, &bar[b]);
     }
     QTRACE(1);
     pdl_wait();
     QTRACE_STARTED();
+    QSTAMP(0);
     const uint4 *rb =
         reinterpret_cast<const uint4 *>(bits + (int64_t)(active ? (row_index ? __ldcg(row_index + r) : r) : 0) * W);
     // The 32 quads of a chunk are scanned as 4 independent sub-chains (one
@@ -418,13 +424,16 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
 #pragma unroll
     for (int p = 0; p < 4; ++p) wq[p] = active && p < n ? __ldcg(rb + c0 + p) : make_uint4(0, 0, 0, 0);
     for (int k = 0; k < n; ++k) {
-        const int buf = k & 1;
+        const int buf = k % kFitBufs;
         const uint32_t words[4] = {wq[0].x, wq[0].y, wq[0].z, wq[0].w};
+        if (k == 0 && words[0] == 0xdeadbeefu) QSTAMP(7);  // (never) keeps the bits load ahead of stamp 1
+        if (k == 0) QSTAMP(1);
         wq[0] = wq[1];
         wq[1] = wq[2];
         wq[2] = wq[3];
         wq[3] = active && k + 4 < n ? __ldcg(rb + c0 + k + 4) : make_uint4(0, 0, 0, 0);
-        mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
+        mbar_wait(&bar[buf], (uint32_t)((k / kFitBufs) & 1));
+        if (k == 0) QSTAMP(2);
         const double2 *tb = tab + buf * kChunkEntries;
         Seg ch[4];
 #pragma unroll
@@ -465,28 +474,34 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
                 z.pi += E.y;
             }
         }
-        __syncthreads();  // every lane is done with tab[buf]
-        if (tid == 0 && k + 2 < n) bulk_load(tab + buf * kChunkEntries, qtl + (c0 + k + 2) * kChunkEntries, kChunkBytes, &bar[buf]);
+        if (k + kFitBufs < n) {  // CTA-uniform
+            __syncthreads();  // every lane is done with tab[buf]
+            if (tid == 0)
+                bulk_load(tab + buf * kChunkEntries, qtl + (c0 + k + kFitBufs) * kChunkEntries, kChunkBytes, &bar[buf]);
+        }
         run = seg_cat(run, seg_cat(seg_cat(ch[0], ch[1]), seg_cat(ch[2], ch[3])));
     }
+    QSTAMP(3);
     const double ar = run.ar, ai = run.ai, pr = run.pr, pi = run.pi, tr = run.tr, ti = run.ti;
-    if (!active) return;
-    double *o = part + (((int64_t)lam * rows + r) * S + s) * kPartDoubles;
-    if (THG) {
-        o[0] = ar;
-        o[1] = ai;
-        o[2] = pr;
-        o[3] = pi;
-        o[4] = tr;
-        o[5] = ti;
-    } else {  // SHG: the sum is the prefix itself
-        o[0] = pr;
-        o[1] = pi;
-        o[2] = 0.0;
-        o[3] = 0.0;
-        o[4] = 0.0;
-        o[5] = 0.0;
+    if (active) {
+        double *o = part + (((int64_t)lam * rows + r) * S + s) * kPartDoubles;
+        if (THG) {
+            o[0] = ar;
+            o[1] = ai;
+            o[2] = pr;
+            o[3] = pi;
+            o[4] = tr;
+            o[5] = ti;
+        } else {  // SHG: the sum is the prefix itself
+            o[0] = pr;
+            o[1] = pi;
+            o[2] = 0.0;
+            o[3] = 0.0;
+            o[4] = 0.0;
+            o[5] = 0.0;
+        }
     }
+    QSTAMP(4);
 }
 
 // stitch segments, apply w/hconst, |.| (glibc hypot), scale, objective.
@@ -772,6 +787,7 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
     QPM_ARG_CHECK(process == QPM_PROCESS_SHG || (b && hconst), "THG needs b and hconst tables");
     auto *h = new qpm_problem();
     Problem &p = h->p;
+    p.mu = new std::mutex();
     p.process = process;
     p.multi = multi ? 1 : 0;
     p.n_wl = n_wl;
@@ -833,6 +849,8 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
 int qpm_problem_destroy(qpm_problem *h) {
     if (!h) return QPM_OK;
     Problem &p = h->p;
+    delete p.mu;
+    p.mu = nullptr;
     cudaFree(p.e1);
     cudaFree(p.b);
     cudaFree(p.qt);
@@ -871,6 +889,7 @@ int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, d
     QPM_ARG_CHECK(h && signs && out, "problem, signs, out");
     QPM_ARG_CHECK(rows >= 1, "batch items must be non-empty");
     Problem &p = h->p;
+    std::lock_guard<std::mutex> lock(*p.mu);
     int rc = host_path_reserve(&p, rows);
     if (rc) return rc;
     QPM_CUDA_TRY(cudaMemcpyAsync(p.hp_signs, signs, (size_t)rows * p.D, cudaMemcpyHostToDevice, p.hp_stream));
@@ -933,6 +952,7 @@ int qpm_brute_force(qpm_problem *h, int n, int mode, int64_t chunk_rows, int64_t
                     void *stream) {
     QPM_ARG_CHECK(h && best_index && best_fit, "problem, outputs");
     Problem &p = h->p;
+    std::lock_guard<std::mutex> lock(*p.mu);
     QPM_ARG_CHECK(n >= 1 && n <= 63, "n in [1, 63]");
     QPM_ARG_CHECK(n == p.D, "n must equal the problem's domain count");
     QPM_ARG_CHECK(chunk_rows >= 1, "chunk_rows >= 1");
@@ -982,6 +1002,7 @@ int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows
     QPM_ARG_CHECK(h && signs && out, "problem, signs, out");
     QPM_ARG_CHECK(rows >= 1, "rows >= 1");
     Problem &p = h->p;
+    std::lock_guard<std::mutex> lock(*p.mu);
     QPM_ARG_CHECK(wl >= 0 && wl < p.n_wl, "wavelength index");
     int rc = host_path_reserve(&p, rows);
     if (rc) return rc;
@@ -1009,6 +1030,7 @@ int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out
 // per-id launch counts.  Not part of include/qpm_b200.h.
 int qpm_dev_trace_fitness(int reset, unsigned long long *log, unsigned int *launches) {
 #ifdef QPM_TRACE
+    if (reset == 2) return qpm::trace_stamps_tu(log);  // intra-kernel stamps [8][64][8]
     if (reset) return qpm::trace_reset_tu();
     return qpm::trace_read_tu(log, launches);
 #else

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -75,6 +76,11 @@ struct Problem {
     int64_t hp_rows = 0;
     cudaStream_t hp_stream = nullptr;
     int64_t device_bytes = 0;
+    // serialises the host-synchronous entry points (evaluate_block_host,
+    // sum_block_host, brute_force): the reference's parexec calls
+    // evaluate_block from several worker threads at once (parexec.py:88-105)
+    // and they share hp_* and the scratch
+    std::mutex *mu = nullptr;
 };
 
 // per-row segment partials and per-wavelength gains of one fitness launch
@@ -107,6 +113,9 @@ int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64
 // (griddepcontrol.launch_dependents): measured on B200, an early trigger let
 // dependents observe stale data in about one C2 run in eight, and the early
 // residents slowed the primary down.
+// (Measured again with the device timeline, tools/timeline.py: triggering
+// dependents once every CTA has passed its wait made the C2 generation
+// 119.7 -> 133.3 us; the early-resident k_fit_finish CTAs doubled k_fit_fast.)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Device-side kernel timeline (development builds with -DQPM_TRACE only):
@@ -115,8 +124,8 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // graph-replayed generation can then be read back as it really ran (PDL
 // overlap included), which CUDA events between stages cannot show.
 // Ids: 0 de_trial, 1 fit_fast, 2 fit_finish, 3 select_topk, 4 gwo_apply,
-// 5 select_stats, 6 plan_rows, 7 plan_bump.  Each translation unit has its own log.
-constexpr int kTraceIds = 8, kTraceLen = 4096;
+// 5 select_stats, 6 plan_rows, 7 plan_bump, 8 plan_wolf.  Each translation unit has its own log.
+constexpr int kTraceIds = 9, kTraceLen = 4096;
 #ifdef QPM_TRACE
 struct TraceAcc {
     unsigned long long t_entry, t_start, t_end;
@@ -157,6 +166,14 @@ struct TraceScope {
 };
 #define QTRACE(id) ::qpm::TraceScope qtrace_scope_(id)
 #define QTRACE_STARTED() qtrace_scope_.started()
+// intra-kernel stamps of CTA 0, thread 0: g_stamp[id][launch % 64][slot]
+static __device__ unsigned long long g_stamp[kTraceIds][64][8];
+#define QSTAMP(slot)                                                                                   \
+    do {                                                                                               \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && ::qpm::TraceScope::lead())        \
+            ::qpm::g_stamp[qtrace_scope_.id][::qpm::g_tacc[qtrace_scope_.id].launch % 64][slot] =      \
+                ::qpm::gtimer();                                                                       \
+    } while (0)
 // host: reset the accumulators / copy the log of this translation unit
 static inline int trace_reset_tu() {
     std::vector<TraceAcc> init(kTraceIds, TraceAcc{~0ULL, ~0ULL, 0ULL, 0u, 0u});
@@ -168,9 +185,13 @@ static inline int trace_read_tu(unsigned long long *log, unsigned int *launches)
     for (int i = 0; i < kTraceIds; ++i) launches[i] = acc[i].launch;
     return cudaMemcpyFromSymbol(log, g_tlog, sizeof(g_tlog)) == cudaSuccess ? 0 : -1;
 }
+static inline int trace_stamps_tu(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_stamp, sizeof(g_stamp)) == cudaSuccess ? 0 : -1;
+}
 #else
 #define QTRACE(id)
 #define QTRACE_STARTED()
+#define QSTAMP(slot)
 #endif
 
 template <typename... KArgs, typename... Args>

@@ -122,6 +122,38 @@ def test_fitness_pure_function_of_row_bits(q):
     assert np.array_equal(obj.evaluate_block(-signs), a)
 
 
+@pytest.mark.parametrize("D", [300, 2000, 20_000, 70_000])
+def test_fitness_fused_finish_batch_invariant(q, D):
+    """Single-wavelength fitness is finished by the last segment CTA of each
+    128-row block (one stitch run per lane for S <= 32 segments, several for
+    S > 32): values are identical whatever the batch size and row position,
+    and within 1e-9 of exact mode."""
+    spec = q.ObjectiveSpec("single_thg", (1404.0,))
+    obj = q.make_objective(spec, q.default_dispersion(), 1.0, D, mode="fast")
+    ex = q.make_objective(spec, q.default_dispersion(), 1.0, D, mode="exact")
+    signs = O.random_population_matrix(131, D, seed=D)
+    a = obj.evaluate_block(signs)
+    for lo, hi in ((0, 1), (5, 133), (130, 131), (3, 131)):
+        assert np.array_equal(obj.evaluate_block(signs[lo:hi]), a[lo:hi])
+    np.testing.assert_allclose(a, ex.evaluate_block(signs), rtol=FAST_RTOL, atol=0)
+
+
+def test_evaluate_block_concurrent_threads(q):
+    """The reference's parexec calls evaluate_block from worker threads at once
+    (parexec.py:88-105): concurrent calls on one objective give the serial values."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    spec = q.ObjectiveSpec("single_thg", (1404.0,))
+    obj = q.make_objective(spec, q.default_dispersion(), 1.0, 4000, mode="fast")
+    signs = O.random_population_matrix(256, 4000, seed=11)
+    want = obj.evaluate_block(signs)
+    chunks = [signs[k:k + 16] for k in range(0, 256, 16)]
+    with ThreadPoolExecutor(8) as ex:
+        for _ in range(3):
+            got = np.concatenate(list(ex.map(obj.evaluate_block, chunks)))
+            assert np.array_equal(got, want)
+
+
 def test_fitness_edge_shapes(q):
     spec = q.ObjectiveSpec("single_thg", (1404.0,))
     prov = q.MismatchTable({1404.0: q.PhaseMismatchPair(0.3, 0.7)})

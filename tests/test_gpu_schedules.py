@@ -10,7 +10,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL")
+KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL", "QPM_TOPK_THREADS", "QPM_STATS_THREADS")
 
 
 @pytest.fixture(scope="module")
@@ -40,6 +40,8 @@ def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders
 VARIANTS = [
     {"QPM_PDL": "0"},
     {"QPM_WOLF": "mixed"},
+    {"QPM_WOLF": "side"},
+    {"QPM_WOLF": "side", "QPM_PDL": "0", "QPM_PLAN_CTAS": "7"},
     {"QPM_WOLF": "planner"},
     {"QPM_WOLF": "planner", "QPM_PDL": "0"},
     {"QPM_WOLF": "planner", "QPM_PLAN_FORK": "trial"},
@@ -83,7 +85,7 @@ def test_repeated_runs_are_identical(q, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{}, {"QPM_WOLF": "planner"}, {"QPM_WOLF": "planner", "QPM_PDL": "0"},
-                                 {"QPM_WOLF": "mixed"}],
+                                 {"QPM_WOLF": "mixed"}, {"QPM_WOLF": "side"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_c2_shape_runs_match_default(q, monkeypatch, env):
     """The C2 shape (NP 1024, D 10^4) for 600 generations, twice per schedule:

@@ -13,8 +13,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-NAMES = ["de_trial", "fit_fast", "fit_finish", "select_topk", "gwo_apply", "select_stats", "plan_rows", "plan_bump"]
-IDS, LEN = 8, 4096
+NAMES = ["de_trial", "fit_fast", "fit_finish", "select_topk", "gwo_apply", "select_stats", "plan_rows", "plan_bump", "plan_wolf"]
+IDS, LEN = 9, 4096
 
 
 def main():
@@ -60,7 +60,9 @@ def main():
     rec = {}
     for k in range(IDS):
         u = 1 if k in (1, 2) else 0
-        rec[k] = (logs[u][k][:counts[u][k]].astype(np.int64), int(counts[u][k]))
+        lg = logs[u][k][:counts[u][k]].copy()
+        lg[:, 1] = np.where(lg[:, 1] == np.uint64(2**64 - 1), lg[:, 0], lg[:, 1])  # no QTRACE_STARTED: entry
+        rec[k] = (lg.astype(np.int64), int(counts[u][k]))
     g = args.gens
     base = rec[0][0][:, 1]  # de_trial start per generation
     n_per = {k: rec[k][1] // g for k in rec}
@@ -83,6 +85,21 @@ def main():
     for _, name, r, rel in sorted(rows):
         print(f"{name:14s} {r:2d} {rel[:, 0].mean():8.2f} {rel[:, 1].mean():8.2f} {rel[:, 2].mean():8.2f} "
               f"{(rel[:, 2] - rel[:, 1]).mean():8.2f}")
+    print("fit_fast CTA 0 stamps (us from start): bits, first table, loop end, stored =",
+          [round(float(x), 2) for x in stamps(L)[1:5]])
+
+
+
+def stamps(L, fn_name="qpm_dev_trace_fitness", kid=1, n=8):
+    """Intra-kernel stamps of CTA 0 (QSTAMP slots) for kernel id kid, relative to slot 0, in us."""
+    import numpy as np
+
+    buf = np.zeros((IDS, 64, 8), dtype=np.uint64)
+    assert getattr(L, fn_name)(2, buf.ctypes.data_as(ctypes.c_void_p), None) == 0
+    s = buf[kid].astype(np.int64)
+    s = s[s[:, 0] > 0]
+    rel = (s[:, :n] - s[:, :1]) / 1e3
+    return rel.mean(axis=0)
 
 
 if __name__ == "__main__":
