@@ -15,6 +15,8 @@ reported.  `value` is domain-fitness evaluations per second,
 (2 x NP x D f64 = 164 MB) exceeds the 126 MB L2, so no extra flush is done.
 
 Extra keys: `roofline` (dominant kernel, measured live with CUDA events),
+`fitness_kernel` (the north-star fitness kernel alone at the C5 and C2 shapes,
+live CUDA events, against the FP64 CUDA-core peak),
 `cpu_baseline` (the CPU oracle port on this host's cores, bounded sample),
 `e2e` (the public run_hybrid() call end to end: engine creation, table
 upload, all generations, trace + best read back), `clocks`, `stages`.
@@ -214,17 +216,20 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
                 "algorithmic_unit": f"{DE_BYTES_PER_GENE:.3f} B per gene (CR={CR}) x NP*D",
-                "note": "k_de_trial also draws the generation's crossover mask and wolf planes (4 splitmix64 "
-                        "draws per gene); it is integer-issue bound, see int_issue (ncu, "
-                        "profiles/r01/ncu_summary_r01_final.txt)"}
+                "note": "k_de_trial also draws the generation's crossover mask and the first two wolf draws "
+                        "(3 splitmix64 draws per gene, ~57 of its ~130 instructions per gene); it is "
+                        "integer-issue bound, see int_issue (ncu, profiles/r01/ncu_summary_r01_final.txt)"}
         summ = os.path.join(ROOT, "profiles", "r01", "ncu_summary_r01_final.txt")
         if os.path.exists(summ):
-            for line in open(summ):
-                if line.startswith("k_de_trial"):
+            for line in open(summ):  # tools/ncu_summary.py table: ... Minst ALU% FMAheavy% FP64% issue% warps% regs grid
+                if "k_de_trial" in line and not line.startswith("#"):
                     f = line.split()
-                    roof["int_issue"] = {"issue_active_pct": float(f[-4]), "alu_pipe_pct": float(f[5]),
-                                         "fma_pipe_pct": float(f[6]), "warp_instr_per_launch": float(f[4]) * 1e6,
-                                         "source": "ncu --set full, C2 late generation"}
+                    roof["int_issue"] = {"issue_active_pct": float(f[-4]), "alu_pipe_pct": float(f[-7]),
+                                         "fmaheavy_pipe_pct_of_elapsed": float(f[-6]),
+                                         "warp_instr_per_launch": float(f[-8]) * 1e6,
+                                         "source": "ncu --set full, C2 late generation "
+                                                   "(profiles/r01/ncu_summary_r01_final.txt)"}
+                    break
     else:
         nbytes = NP * D * 8
         achieved = nbytes / (ms * 1e-3) / 1e9
@@ -237,6 +242,49 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
     t = traffic_db.get(name) if traffic_db else None
     roof["traffic"] = t
     return roof
+
+
+def fitness_kernel_roofline(q, torch, sm_count, peaks, iters=20):
+    """The fitness kernel alone, timed live with CUDA events on its launch stream,
+    at the fitness-roofline shape north_star quotes its FP64 target on (C5:
+    4,092 candidate rows = one generation of NP 2,048, 64 pump wavelengths,
+    D = 2*10^4, multi_thg) and at the C2 engine shape (1,020 rows, one
+    wavelength, D = 10^4).  Random sign rows resident in HBM."""
+    out = []
+    for tag, rows, d, nwl, thick in (("C5", 2 * 2048 - 4, 20_000, 64, 0.5), ("C2", NP - 4, D, 1, THICKNESS_UM)):
+        pumps = tuple(float(w) for w in np.linspace(1380.0, 1430.0, nwl)) if nwl > 1 else (PUMP_NM,)
+        spec = q.ObjectiveSpec("multi_thg" if nwl > 1 else "single_thg", pumps)
+        obj = q.make_objective(spec, q.default_dispersion(25.0), thick, d)
+        W = obj.row_words
+        g = torch.Generator(device="cuda").manual_seed(1)
+        bits = torch.randint(-2**31, 2**31 - 1, (rows, W), dtype=torch.int32, device="cuda", generator=g)
+        full, rem = divmod(d, 32)
+        bits[:, full + (1 if rem else 0):] = 0
+        if rem:
+            bits[:, full] &= (1 << rem) - 1
+        res = torch.empty(rows, dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        for _ in range(3):
+            obj.evaluate_bits(bits, res, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(iters):
+            obj.evaluate_bits(bits, res, stream=s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) * 1e-3 / iters
+        evals = rows * d * nwl
+        achieved = evals * FLOP_PER_EVAL / sec / 1e12
+        peak = sm_count * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        out.append({"shape": tag, "rows": rows, "D": d, "wavelengths": nwl, "us_per_launch": sec * 1e6,
+                    "domain_evals_per_s": evals / sec, "bound": "fp64", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak,
+                    "peak_basis": f"nominal FP64 CUDA-core peak ({sm_count} SMs x 64 DFMA/clk x 2 x sm_max_mhz "
+                                  f"from MEASURED_PEAKS.json; no measured FP64 entry)",
+                    "algorithmic_unit": f"{FLOP_PER_EVAL} flop per domain-eval x rows x D x wavelengths"})
+        del obj
+    return out
 
 
 def run_ours(args):
@@ -309,6 +357,8 @@ def run_ours(args):
     ms_gen = ms / args.steps
     roof = stage_roofline(stages, sum(s[1] for s in stages), peaks, peaks_kind, sm_count, traffic_db)
 
+    fit_roof = fitness_kernel_roofline(q, torch, sm_count, peaks) if rank == 0 else None
+
     # end to end through the public API (host buffers, everything inside the clock)
     torch.cuda.synchronize()
     if world > 1:
@@ -346,7 +396,7 @@ def run_ours(args):
                                            f"wolf rows, replicated genome") if world > 1 else "1 GPU",
                            "l2": "genome pool 2 x NP x D f64 (164 MB per 1,024 rows) > 126 MB L2; no flush"},
                 "generations_per_s": 1e3 / ms_gen, "best_after_timed": best_after,
-                "roofline": roof, "stages": [{"name": n, "ms": m} for n, m in stages],
+                "roofline": roof, "fitness_kernel": fit_roof, "stages": [{"name": n, "ms": m} for n, m in stages],
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
                 "peaks": peaks_kind}
         print(json.dumps(line), flush=True)
