@@ -392,8 +392,10 @@ def run_ours(args):
                                        f"(NP={np_total}), {G} generations",
                            "NP": np_total, "D": D, "generations": G, "fitness_mode": "fast",
                            "timed_generations": [args.warmup + 1, args.warmup + args.steps],
-                           "parallelism": (f"row-sharded x{world}: NCCL all-gather of candidate fitness and "
-                                           f"wolf rows, replicated genome") if world > 1 else "1 GPU",
+                           "parallelism": (f"column-sharded x{world}: each GPU owns the genes under 1/{world} of "
+                                           f"the fitness segments for all rows; NCCL all-gather of the segment "
+                                           f"partials twice per generation, replicated selection") if world > 1
+                           else "1 GPU",
                            "l2": "genome pool 2 x NP x D f64 (164 MB per 1,024 rows) > 126 MB L2; no flush"},
                 "generations_per_s": 1e3 / ms_gen, "best_after_timed": best_after,
                 "roofline": roof, "fitness_kernel": fit_roof, "stages": [{"name": n, "ms": m} for n, m in stages],

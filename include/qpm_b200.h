@@ -167,8 +167,10 @@ typedef struct {
     int adaptive_branches;
     /* run_gwo bounds and a0 (trace row 0) */
     double gwo_lo, gwo_hi, gwo_a0;
-    /* row shard owned by this rank [row_lo, row_hi); 0, NP for one GPU */
-    int64_t row_lo, row_hi;
+    /* column shard of a multi-GPU run: this engine owns the genes under the
+     * fitness segments [floor(rank S / world), floor((rank+1) S / world)) of
+     * every individual (S = segments of the problem); 0, 1 for one GPU */
+    int shard_rank, shard_world;
 } qpm_run_params;
 
 typedef struct qpm_engine qpm_engine;
@@ -194,23 +196,30 @@ int qpm_engine_read_trace(qpm_engine *e, int64_t first_row, int64_t n_rows, doub
 int qpm_engine_read_best(qpm_engine *e, double *genome, int8_t *proj, double *fitness);
 int qpm_engine_read_population(qpm_engine *e, double *genome, double *fitness);
 /* ------------------------------------------------------------ multi-GPU
- * One process per GPU, rows sharded in equal contiguous slices
- * [rank NP/world, (rank+1) NP/world) (set row_lo/row_hi in qpm_run_params).
- * Every rank keeps the whole population; after each fitness phase the
- * candidate fitness vector is all-gathered over NCCL and foreign accepted
- * trials / wolf candidates are recomputed locally from the same counter
- * streams (bit-identical to one GPU).  Replaces the reference's in-process
+ * One process per GPU; the genes are sharded in contiguous column ranges
+ * aligned to the fitness segments (qpm_run_params.shard_rank/shard_world).
+ * Every rank runs the per-gene work (DE trials, wolf moves, draws, fitness
+ * segment scans) on its columns of all NP individuals; after each fitness
+ * scan the segment partials (NP x 48 B per segment) are all-gathered over
+ * NCCL and every rank stitches and scores all rows, so selection, leaders,
+ * statistics and the F update run replicated on identical data.  Fitness
+ * segments are the single-GPU ones, so a sharded run is bit-identical to
+ * the same run on one GPU (fast mode).  Replaces the reference's in-process
  * thread pool (parexec.py:73-120). */
 /* rank 0 creates the NCCL id (128 bytes) and broadcasts it to the others */
 int qpm_nccl_unique_id(uint8_t *id_out);
+/* before qpm_engine_init; rank / world must match the engine's shard */
 int qpm_engine_set_comm(qpm_engine *e, int rank, int world, const uint8_t *id);
-/* shard without a communicator: the caller exchanges qpm_engine_cand_ptr()
- * slices between phases (single-GPU emulation of several ranks in tests) */
-int qpm_engine_set_shard(qpm_engine *e, int rank, int world);
+/* this engine's genes [g0, g0 + d) of the run (0, D on one GPU); genomes and
+ * projections read back from a shard cover these columns */
+int qpm_engine_columns(const qpm_engine *e, int64_t *g0, int64_t *d);
 int qpm_engine_phases(const qpm_engine *e);
 int qpm_engine_run_phase(qpm_engine *e, int phase);
-/* emulated exchange before `phase`: copy src's own slices (candidate
- * fitness; staged wolf candidates before phase 2) into dst (synchronous) */
+/* emulated ranks on one GPU (no communicator): qpm_engine_init stops after
+ * the generation-0 fitness scan; exchange, then qpm_engine_init_finish */
+int qpm_engine_init_finish(qpm_engine *e);
+/* emulated exchange before a phase (or before qpm_engine_init_finish): copy
+ * src's segment partials into dst (synchronous) */
 int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase);
 int qpm_engine_cand_ptr(qpm_engine *e, double **cand_dev);
 int qpm_engine_stream(qpm_engine *e, void **stream);

@@ -25,7 +25,8 @@ EXPORTS = (
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
     "qpm_engine_step", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
     "qpm_engine_read_best", "qpm_engine_read_population", "qpm_engine_profile", "qpm_engine_launches_per_generation",
-    "qpm_engine_fitness_ptr", "qpm_nccl_unique_id", "qpm_engine_set_comm", "qpm_engine_set_shard",
+    "qpm_engine_fitness_ptr", "qpm_nccl_unique_id", "qpm_engine_set_comm", "qpm_engine_columns",
+    "qpm_engine_init_finish",
     "qpm_engine_phases", "qpm_engine_run_phase", "qpm_engine_exchange_from", "qpm_engine_cand_ptr",
     "qpm_engine_stream",
 )
@@ -63,8 +64,8 @@ class RunParams(ctypes.Structure):
         ("gwo_lo", ctypes.c_double),
         ("gwo_hi", ctypes.c_double),
         ("gwo_a0", ctypes.c_double),
-        ("row_lo", ctypes.c_int64),
-        ("row_hi", ctypes.c_int64),
+        ("shard_rank", ctypes.c_int),
+        ("shard_world", ctypes.c_int),
     ]
 
 
@@ -114,7 +115,8 @@ def lib():
         "qpm_engine_fitness_ptr": (I32, [P, P]),
         "qpm_nccl_unique_id": (I32, [P]),
         "qpm_engine_set_comm": (I32, [P, I32, I32, P]),
-        "qpm_engine_set_shard": (I32, [P, I32, I32]),
+        "qpm_engine_columns": (I32, [P, P, P]),
+        "qpm_engine_init_finish": (I32, [P]),
         "qpm_engine_phases": (I32, [P]),
         "qpm_engine_run_phase": (I32, [P, I32]),
         "qpm_engine_exchange_from": (I32, [P, P, I32]),

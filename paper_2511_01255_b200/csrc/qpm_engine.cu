@@ -102,7 +102,11 @@ __device__ __forceinline__ bool passes(const Thr &t, uint64_t mix) { return !t.n
 
 struct RunConsts {
     int algorithm;
+    // D, Dp, W: this engine's genes (a column shard [g0, g0 + D) of the run's
+    // Dg genes on a multi-GPU run; g0 = 0, D = Dg on one GPU).  Stream
+    // positions always use the global gene index g0 + j and Dg.
     int64_t NP, D, Dp, W, G;
+    int64_t Dg, g0;
     uint64_t seed;
     double f_max, f_min;
     uint64_t cr_thr;
@@ -182,7 +186,7 @@ __device__ void de_row_draws(const RunConsts &c, uint64_t key, int64_t i, int4 &
         if (!dup) r[n++] = cand;
     }
     pk = make_int4((int)r[0], (int)r[1], (int)r[2], (int)m);
-    jr = (int32_t)randint(key, m, c.D);
+    jr = (int32_t)randint(key, m, c.Dg);
 }
 
 
@@ -411,7 +415,8 @@ __device__ __forceinline__ void store_planes(uint32_t *dst_word, uint32_t code, 
 template <int K>
 __device__ __forceinline__ void wolf_chunk(const RunConsts &c, const GenThr &t, uint64_t key, uint32_t p_wolf,
                                            uint32_t *prow, int jc, int len) {
-    const uint32_t D = (uint32_t)c.D;
+    const uint32_t Dg = (uint32_t)c.Dg;  // stream layout
+    const int D = (int)c.D;              // this shard's genes
     const bool early = t.early != 0;
     const int lane = threadIdx.x & 31;
 #pragma unroll 1
@@ -422,13 +427,13 @@ __device__ __forceinline__ void wolf_chunk(const RunConsts &c, const GenThr &t, 
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             j[h] = jc + it + h * kRowThreads + (int)threadIdx.x;
-            code[h] = wolf_code<K, false>(c, t, key, p_wolf + (uint32_t)j[h], D, early, tie[h]);
-            if (j[h] >= (int)D) code[h] = 0u, tie[h] = false;
+            code[h] = wolf_code<K, false>(c, t, key, p_wolf + (uint32_t)j[h], Dg, early, tie[h]);
+            if (j[h] >= D) code[h] = 0u, tie[h] = false;
         }
         if (__any_sync(0xffffffffu, tie[0] || tie[1])) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-                if (tie[h]) code[h] = wolf_code<K, true>(c, t, key, p_wolf + (uint32_t)j[h], D, early, tie[h]);
+                if (tie[h]) code[h] = wolf_code<K, true>(c, t, key, p_wolf + (uint32_t)j[h], Dg, early, tie[h]);
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(kRowThreads) k_plan_wolf(RunConsts c, PlanArgs
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int64_t i = a.row_lo + item / nchunk;
         const int jc = (int)(item % nchunk) * kGenesPerBlock;
-        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
+        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)(c.Dg + c.g0);  // m + 1 + Dg + (g0 + j), plus one
         wolf_chunk<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
                             kGenesPerBlock);
     }
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kRowThreads) k_init_population(RunConsts c, do
             const int j = jb + it * kRowThreads + threadIdx.x;
             bool neg = false;
             if (j < (int)c.D) {
-                const double x = c.x_lo + (double)(mix_at(key, (uint32_t)j + 1) >> 11) * kTwoM53 * c.x_span;
+                const double x = c.x_lo + (double)(mix_at(key, (uint32_t)(c.g0 + j) + 1) >> 11) * kTwoM53 * c.x_span;
                 row[j] = x;
                 neg = !(x >= 0.0);
             }
@@ -503,9 +508,6 @@ struct TrialArgs {
     const EngineState *st;
     const GenThr *gthr;
     int64_t row_lo, n_rows;
-    int filter;  // recompute only foreign rows whose trial won (multi-GPU)
-    int64_t own_lo, own_hi;
-    const double *cand, *fit;
     const int4 *picks;       // [2][NP]
     const uint64_t *keys;    // [2][NP]
     const int32_t *jrand;    // [2][NP]
@@ -530,7 +532,7 @@ struct TrialRow {
     RowRef xi, x1, x2, x3;
     double *out;
     uint32_t *bout, *prow;
-    uint32_t *dout;  // the candidate's dense row (own rows), null when recomputing foreign rows
+    uint32_t *dout;  // the candidate's dense row
     uint64_t key;
     int64_t out_slot;
     double F;
@@ -554,9 +556,10 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
     r.out_slot = a.spare_of[i];
     r.out = a.genome + r.out_slot * c.Dp;
     r.bout = a.bits + r.out_slot * c.W;
-    r.dout = a.filter || !a.cbits ? nullptr : a.cbits + i * c.W;
+    r.dout = a.cbits ? a.cbits + i * c.W : nullptr;
     r.prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
-    r.p_mask = (uint32_t)pk.w + 2;  // m + 1 + j, plus one
+    r.p_mask = (uint32_t)(pk.w + 2 + c.g0);  // m + 1 + (g0 + j), plus one: j counts this shard's genes
+    r.jr -= (int)c.g0;                      // j_rand relative to the shard (never matches outside it)
     r.F = a.st->F;
     r.t = a.gthr[g];
 }
@@ -578,8 +581,8 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const int D = (int)c.D;
     // counter states advance by constant multiples of GOLD: one 64-bit add
     // per draw instead of a 32 x 64 product (the wolf block starts D later)
-    const uint64_t gD = (uint64_t)(uint32_t)D * kGold;
-    const uint64_t gnon = (uint64_t)(uint32_t)(early ? 2 * D : 5 * D) * kGold;
+    const uint64_t gD = (uint64_t)(uint32_t)c.Dg * kGold;
+    const uint64_t gnon = (uint64_t)(uint32_t)(early ? 2 * c.Dg : 5 * c.Dg) * kGold;
     const uint32_t Hcr = top_thr(c.thr_cr);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -739,7 +742,6 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts
     const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
     const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
-    if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
     __shared__ TrialRow s_row;
     if (threadIdx.x == 0) trial_row_setup(c, a, a.st->g, i, s_row);
     __syncthreads();
@@ -761,7 +763,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(Run
     const int jc = (int)(item % nchunk) * kDeChunk;
     const GenThr t = a.gthr[g];
     if (blockIdx.x & 1) {
-        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D;  // m + 1 + D + j, plus one
+        const uint32_t p_wolf = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)(c.Dg + c.g0);  // m + 1 + Dg + (g0 + j), plus one
         wolf_chunk<K>(c, t, a.keys[b * c.NP + i], p_wolf, a.planes + (b * c.NP + i) * c.W * kPlanes, jc,
                             kDeChunk);
         return;
@@ -770,25 +772,6 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(Run
     if (threadIdx.x == 0) trial_row_setup(c, a, g, i, s_row);
     __syncthreads();
     de_trial_dispatch<0>(c, a, s_row, jc);
-}
-
-// multi-GPU: all-gathered wolf candidates of accepted (non-leader) rows into
-// their spare slots, ahead of the selection
-__global__ void k_commit_cand_bits(RunConsts c, TrialArgs a) {
-    pdl_wait();
-    const int64_t total = c.NP * c.W;
-    int32_t lead[kMaxLeaders];
-#pragma unroll
-    for (int t = 0; t < kMaxLeaders; ++t) lead[t] = t < c.k ? a.st->leaders[t] : -1;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = idx / c.W;
-        bool skip = !(a.cand[i] > a.fit[i]);
-#pragma unroll
-        for (int t = 0; t < kMaxLeaders; ++t) skip |= lead[t] == i;
-        if (skip) continue;
-        a.bits[(int64_t)a.spare_of[i] * c.W + idx % c.W] = a.cbits[idx];
-    }
 }
 
 // ---------------------------------------------------------------- wolf update
@@ -810,7 +793,6 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
 #pragma unroll
     for (int t = 0; t < K; ++t) skip |= lead[t] == i;
     if (skip || w >= (int)c.W) return;
-    if (a.filter && ((i >= a.own_lo && i < a.own_hi) || !(a.cand[i] > a.fit[i]))) return;
     const int64_t g = a.st->g;
     const bool early = a.gthr[g].early != 0;
     uint32_t ld[4];
@@ -843,8 +825,8 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
     if (need) {
         const int64_t b = g & 1;
         const uint64_t key = a.keys[b * c.NP + i];
-        const uint32_t base = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)c.D + (uint32_t)(w * 32);
-        const uint32_t D = (uint32_t)c.D;
+        const uint32_t base = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)(c.Dg + c.g0) + (uint32_t)(w * 32);
+        const uint32_t D = (uint32_t)c.Dg;  // stream layout
         // two genes per iteration: independent draws interleave
         while (need) {
             int bit[2];
@@ -905,7 +887,7 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, con
     const double a = sched[g * QPM_SCHED_COLS + QPM_SCHED_A_NOW];
     const double two_a = 2.0 * a;
     const uint64_t key = fold_key3(c.seed, (uint64_t)g, (uint64_t)i);
-    const uint64_t D = (uint64_t)c.D;
+    const uint64_t D = (uint64_t)c.Dg;  // stream layout; genes j of this shard sit at g0 + j
     const RowRef x = row_ref(c, slot_of[i], slot_bin, genome, bits);
     const RowRef L0 = row_ref(c, slot_of[st->leaders[0]], slot_bin, genome, bits);
     const RowRef L1 = row_ref(c, slot_of[st->leaders[1]], slot_bin, genome, bits);
@@ -919,7 +901,7 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, con
         const int64_t j = jb + it * kRowThreads + threadIdx.x;
         bool neg = false;
         if (j < c.D) {
-            const uint64_t jj = (uint64_t)j;
+            const uint64_t jj = (uint64_t)(c.g0 + j);
             const double xj = x.at(j);
             const double Lm[3] = {L0.at(j), L1.at(j), L2.at(j)};
             double moved[3];
@@ -1076,8 +1058,16 @@ __device__ double block_pairwise(const double *v, const RunConsts &c, const Tree
         const int m = len - len % 8;
         double r = 0.0;
         if (len >= 8) {
-            r = a[sub];
-            for (int i = 8 + sub; i < m; i += 8) r += a[i];
+            // a leaf has <= 128 elements, so <= 16 per accumulator: every
+            // shared-memory load is issued first, then the adds run in numpy's
+            // order (a dependent chain of adds instead of load-add round trips)
+            double x[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) x[t] = sub + 8 * t < m ? a[sub + 8 * t] : 0.0;
+            r = x[0];
+#pragma unroll
+            for (int t = 1; t < 16; ++t)
+                if (sub + 8 * t < m) r += x[t];
         }
         r += __shfl_xor_sync(0xffffffffu, r, 1);
         r += __shfl_xor_sync(0xffffffffu, r, 2);
@@ -1124,11 +1114,13 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, Engine
 #pragma unroll
     for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
     for (int64_t i = threadIdx.x; i < c.NP; i += blockDim.x) {
+        // the slot ids are loaded with the fitness values (one L2 round trip,
+        // not two) and written back only on acceptance
         const double f = cand[i];
         double v = fit[i];
+        const int32_t a = slot_of[i], b = spare_of[i];
         if (f > v) {
-            const int32_t a = slot_of[i];
-            slot_of[i] = spare_of[i];
+            slot_of[i] = b;
             spare_of[i] = a;
             fit[i] = f;
             v = f;
@@ -1178,6 +1170,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
     pdl_wait();
     QTRACE_STARTED();
+    QSTAMP(0);
     __shared__ EngineState s_state;
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(st);
@@ -1197,9 +1190,8 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
 #pragma unroll
             for (int t = 0; t < kMaxLeaders; ++t) is_leader |= lead[t] == i;
             const double f = cand[i];
+            const int32_t a = slot_of[i], b = spare_of[i];  // with the values: one L2 round trip
             if (!is_leader && (mode == 2 || f > v)) {
-                const int32_t a = slot_of[i];
-                const int32_t b = spare_of[i];
                 slot_of[i] = b;
                 spare_of[i] = a;
                 fit[i] = f;
@@ -1232,7 +1224,9 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
         s_mn[threadIdx.x >> 5] = mn;
         s_am[threadIdx.x >> 5] = amx;
     }
+    QSTAMP(1);
     __syncthreads();  // also publishes fv (and, without on-chip staging, fit)
+    QSTAMP(2);
     mx = lane < nw ? s_mx[lane] : -INFINITY;
     mn = lane < nw ? s_mn[lane] : INFINITY;
     amx = lane < nw ? s_am[lane] : n;
@@ -1249,13 +1243,16 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     mx = __shfl_sync(0xffffffffu, mx, 0);
     mn = __shfl_sync(0xffffffffu, mn, 0);
     amx = __shfl_sync(0xffffffffu, amx, 0);
+    QSTAMP(3);
     const double mean = block_pairwise(fv, c, ts) / (double)n;
+    QSTAMP(4);
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = fv[i] - mean;
         sq[i] = d * d;
     }
     __syncthreads();
     const double var = block_pairwise(sq, c, ts) / (double)n;
+    QSTAMP(5);
     if (threadIdx.x != 0) return;
     // serial tail on the shared-memory copy of the state (fetched at entry);
     // only the fields this kernel owns are written back (g_plan belongs to
@@ -1320,6 +1317,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
         st->F = f;
         row[3] = f;
     }
+    QSTAMP(6);
     st->g = g + 1;
 }
 
@@ -1363,9 +1361,19 @@ struct Engine {
     uint32_t *cbits = nullptr;   // [NP][W] wolf candidates staged for exchange
     GenThr *gthr = nullptr;
     cudaStream_t side = nullptr;  // low-priority planner stream
-    int rank = 0, world = 1;       // row shard of this engine (multi-GPU)
-    int64_t own_lo = 0, own_hi = 0;
+    // column shard of this engine (multi-GPU): genes [c.g0, c.g0 + c.D) of
+    // every individual, the fitness segments [seg_lo, seg_lo + seg_n) of the
+    // problem; one GPU: rank 0 of 1, all of it
+    int rank = 0, world = 1;
+    int seg_lo = 0, seg_n = 0;
+    qpm_problem *lprob = nullptr;  // the shard's columns of the problem (world > 1, owned)
+    int S_slot = 1;                // partial slots per rank in gpart
+    double *gpart = nullptr;       // [world][n_wl][NP][S_slot][6] all-gathered segment partials (world > 1)
+    double *ggains = nullptr;      // [NP][n_wl] finish scratch (world > 1)
     void *comm = nullptr;          // ncclComm_t
+    // the sharded flow (scan, all-gather, finish): several ranks, or one rank
+    // with a communicator (exercises the collective path on one GPU)
+    bool sharded() const { return world > 1 || comm != nullptr; }
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int32_t *slot_of = nullptr, *spare_of = nullptr, *jrand = nullptr;
     double *fit = nullptr, *cand = nullptr, *scratch = nullptr;
@@ -1381,7 +1389,6 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
-    int apply_grid = 148;  // k_commit_cand_bits (grid-stride)
     int plan_grid = 148;       // k_plan_wolf CTAs (QPM_PLAN_CTAS)
     bool plan_after_trial = false;  // fork the planner after k_de_trial (QPM_PLAN_FORK=trial)
     bool wolf_in_planner = false;   // wolf planes on the side stream (QPM_WOLF=planner)
@@ -1393,6 +1400,7 @@ struct Engine {
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
     int64_t g_done = 0;
     bool initialized = false;
+    bool init_pending = false;  // emulated shard: fitness scan of generation 0 done, exchange pending
     bool owns_stream = false;
     int64_t device_bytes = 0;
     std::vector<std::pair<void *, size_t>> allocs;
@@ -1507,11 +1515,6 @@ static TrialArgs trial_args(const Engine *e, int64_t row_lo, int64_t n_rows) {
     a.gthr = e->gthr;
     a.row_lo = row_lo;
     a.n_rows = n_rows;
-    a.filter = 0;
-    a.own_lo = 0;
-    a.own_hi = e->c.NP;
-    a.cand = e->cand;
-    a.fit = e->fit;
     a.picks = e->picks;
     a.keys = e->keys;
     a.jrand = e->jrand;
@@ -1529,8 +1532,8 @@ static PlanArgs plan_args(const Engine *e) {
     PlanArgs a;
     a.st = e->st;
     a.gthr = e->gthr;
-    a.row_lo = e->own_lo;
-    a.n_rows = e->own_hi - e->own_lo;
+    a.row_lo = 0;
+    a.n_rows = e->c.NP;
     a.keys = e->keys;
     a.picks = e->picks;
     a.jrand = e->jrand;
@@ -1594,15 +1597,14 @@ static int nccl_load() {
     return QPM_OK;
 }
 
-// exchange before phase `phase`: every rank's own slice of the candidate
-// fitness (and, before the wolf selection, of the staged wolf candidates)
+// exchange before phase `phase`: every rank's segment partials of the
+// candidates' fitness (its columns of every row), all-gathered into gpart
+static size_t gpart_slot(const Engine *e) { return (size_t)e->prob->n_wl * e->c.NP * e->S_slot * kPartDoubles; }
 static int enqueue_exchange(Engine *e, int phase) {
-    if (!e->comm) return QPM_OK;  // one rank (a 1-rank communicator still runs the collective)
-    const int64_t n_own = e->own_hi - e->own_lo;
-    int r = g_nccl.allgather(e->cand + e->own_lo, e->cand, (size_t)n_own, kNcclFloat64, e->comm, e->stream);
-    if (r == 0 && phase == 2)
-        r = g_nccl.allgather(e->cbits + e->own_lo * e->c.W, e->cbits, (size_t)(n_own * e->c.W * 4), kNcclUint8,
-                             e->comm, e->stream);
+    (void)phase;
+    if (!e->comm) return QPM_OK;  // one GPU, or emulated ranks (qpm_engine_exchange_from)
+    const size_t n = gpart_slot(e);
+    const int r = g_nccl.allgather(e->gpart + e->rank * n, e->gpart, n, kNcclFloat64, e->comm, e->stream);
     if (r != 0) {
         set_error("ncclAllGather: %s", g_nccl.err(r));
         return QPM_ERR_NCCL;
@@ -1610,14 +1612,32 @@ static int enqueue_exchange(Engine *e, int phase) {
     return QPM_OK;
 }
 
+// the candidates' fitness into out[NP]: one GPU scores them now; a column
+// shard scans its segments into its gpart slot and fit_finish scores them
+// after the exchange
+static int fit_scan(Engine *e, const uint32_t *bits, const int32_t *row_index, double *out, cudaStream_t s, int *n) {
+    const RunConsts &c = e->c;
+    if (!e->sharded())
+        return launch_fitness(e->prob, &e->fs, bits, c.W, row_index, c.NP, out, e->P.fitness_mode, s, n, e->pdl);
+    return launch_fitness_scan(e->lprob ? &e->lprob->p : e->prob, bits, c.W, row_index, c.NP,
+                               e->gpart + e->rank * gpart_slot(e), e->S_slot, s, n, e->pdl);
+}
+static int fit_finish(Engine *e, double *out, cudaStream_t s, int *n) {
+    if (!e->sharded()) return QPM_OK;
+    return launch_fitness_finish(e->prob, e->gpart, e->prob->S, e->world, e->S_slot, e->c.NP, e->ggains, out, s, n,
+                                 e->pdl);
+}
+
 static int phase_count(const Engine *e) { return e->c.algorithm == QPM_ALGO_HYBRID ? 3 : 2; }
 
-// One generation = phases separated by candidate-fitness exchanges:
-//   hybrid  P0 trial(own) fit(own) | X | P1 trial(foreign accepted) select+top-k
-//           wolf(own) fit(own) | X | P2 wolf(foreign accepted) select+stats
-//   de      P0 trial(own) fit(own) | X | P1 trial(foreign accepted) select+stats
-//   gwo     P0 top-k, wolf move (all rows) fit(own) | X | P1 replace+stats
-// With one rank own = all rows and the foreign kernels are skipped.
+// One generation = phases separated by exchanges of the candidates' fitness
+// partials (column shards; with one GPU the exchange is empty and each
+// fitness is scored at once):
+//   hybrid  P0 trial, scan | X | P1 finish, select+top-k, wolf, scan | X | P2 finish, select+stats
+//   de      P0 trial, scan | X | P1 finish, select+stats
+//   gwo     P0 top-k, wolf move, scan | X | P1 finish, replace+stats
+// Every rank runs the per-gene kernels on its columns of all NP rows and the
+// per-row kernels (finish, selection, statistics) on all rows, replicated.
 static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
@@ -1625,9 +1645,13 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     auto mark = [&](const char *next) {
         if (pm) pm->mark(s, next);
     };
-    const int64_t NP = c.NP, lo = e->own_lo, n_own = e->own_hi - e->own_lo;
-    const bool sharded = e->world > 1;
+    const int64_t NP = c.NP;
+    const bool sharded = e->sharded();
     const int64_t de_chunks = (c.Dp + kDeChunk - 1) / kDeChunk;
+    if (phase > 0 && sharded) {
+        mark("fitness_finish");
+        if ((rc = fit_finish(e, e->cand, s, n))) return rc;
+    }
     if (c.algorithm == QPM_ALGO_GWO) {
         if (phase == 0) {
             mark("topk");
@@ -1641,8 +1665,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             QPM_LAUNCH_CHECK();
             *n += 2;
             mark("fitness");
-            rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->spare_of + lo, n_own, e->cand + lo, e->P.fitness_mode, s, n, e->pdl);
-            if (rc) return rc;
+            if ((rc = fit_scan(e, e->bits, e->spare_of, e->cand, s, n))) return rc;
         } else {
             mark("replace_stats");
             if ((rc = launch_select_stats(e, 2, s))) return rc;
@@ -1654,11 +1677,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         return QPM_OK;
     }
     const bool hybrid = c.algorithm == QPM_ALGO_HYBRID;
-    TrialArgs own = trial_args(e, lo, n_own);
-    TrialArgs foreign = trial_args(e, 0, NP);
-    foreign.filter = 1;
-    foreign.own_lo = e->own_lo;
-    foreign.own_hi = e->own_hi;
+    TrialArgs all = trial_args(e, 0, NP);
     if (phase == 0) {
         // fork: the planner draws generation g+1 on the side stream
         auto fork = [&]() -> int {
@@ -1675,16 +1694,16 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         // the generation's first kernel is never launched programmatically: a
         // graph's root node would otherwise overlap the previous replay's
         // tail, including its planner branch
-        const unsigned items = (unsigned)(n_own * de_chunks);
-        const bool wolf_side = hybrid && e->wolf_side && !sharded;
+        const unsigned items = (unsigned)(NP * de_chunks);
+        const bool wolf_side = hybrid && e->wolf_side;
         if (!hybrid || e->wolf_in_planner || wolf_side)
-            QPM_CUDA_TRY(launch_k(false, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, own));
+            QPM_CUDA_TRY(launch_k(false, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, all));
         else if (e->wolf_mixed)
             QPM_CUDA_TRY(launch_k(false, c.k == 4 ? k_de_trial_mixed<4> : k_de_trial_mixed<3>, dim3(2 * items),
-                                  dim3(kRowThreads), 0, s, c, own));
+                                  dim3(kRowThreads), 0, s, c, all));
         else
             QPM_CUDA_TRY(launch_k(false, c.k == 4 ? k_de_trial<4> : k_de_trial<3>, dim3(items), dim3(kRowThreads), 0,
-                                  s, c, own));
+                                  s, c, all));
         QPM_LAUNCH_CHECK();
         *n += 1;
         if (wolf_side) {  // the planes of this generation, concurrent with the DE fitness and selection
@@ -1701,17 +1720,9 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         }
         if (e->plan_after_trial && (rc = fork())) return rc;
         mark("fitness_de");
-        return launch_fitness(e->prob, &e->fs, e->cbits + lo * c.W, c.W, nullptr, n_own, e->cand + lo, e->P.fitness_mode, s, n,
-                              e->pdl);
+        return fit_scan(e, e->cbits, nullptr, e->cand, s, n);
     }
     if (phase == 1) {
-        if (sharded) {
-            mark("de_trial_foreign");
-            QPM_CUDA_TRY(launch_k(e->pdl, k_de_trial<0>, dim3((unsigned)(NP * de_chunks)), dim3(kRowThreads), 0, s, c,
-                                  foreign));
-            QPM_LAUNCH_CHECK();
-            *n += 1;
-        }
         if (!hybrid) {
             mark("select_stats");
             if ((rc = launch_select_stats(e, 0, s))) return rc;
@@ -1722,24 +1733,17 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         mark("select_topk");
         QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3(1), dim3(e->topk_threads), 0, s, c, e->st,
                               (const double *)e->cand, e->fit, e->slot_of, e->spare_of));
-        if (e->wolf_side && !sharded) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
+        if (e->wolf_side) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
         QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
-                              dim3((unsigned)((c.W + kApplyThreads - 1) / kApplyThreads), (unsigned)n_own),
-                              dim3(kApplyThreads), 0, s, c, own));
+                              dim3((unsigned)((c.W + kApplyThreads - 1) / kApplyThreads), (unsigned)NP),
+                              dim3(kApplyThreads), 0, s, c, all));
         QPM_LAUNCH_CHECK();
         *n += 2;
         mark("fitness_gwo");
-        return launch_fitness(e->prob, &e->fs, e->cbits + lo * c.W, c.W, nullptr, n_own, e->cand + lo, e->P.fitness_mode, s, n,
-                              e->pdl);
+        return fit_scan(e, e->cbits, nullptr, e->cand, s, n);
     }
     // phase 2 (hybrid)
-    if (sharded) {
-        mark("commit_wolves");
-        QPM_CUDA_TRY(launch_k(e->pdl, k_commit_cand_bits, dim3(e->apply_grid), dim3(kRowThreads), 0, s, c, foreign));
-        QPM_LAUNCH_CHECK();
-        *n += 1;
-    }
     mark("select_stats");
     if ((rc = launch_select_stats(e, 1, s))) return rc;
     *n += 1;
@@ -1777,6 +1781,7 @@ static void engine_free(Engine *e) {
     if (e->graph) cudaGraphDestroy(e->graph);
     for (auto &pb : e->allocs) dev_cache_release(pb.first, pb.second);
     scratch_free(&e->fs);
+    if (e->lprob) qpm_problem_destroy(e->lprob);
     delete e;
 }
 
@@ -1800,13 +1805,22 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ARG_CHECK(P->algorithm == QPM_ALGO_GWO || P->leader_count == 3 || P->leader_count == 4,
                   "leader_count must be 3 or 4");
     QPM_ARG_CHECK(P->conv_window >= 1 && P->conv_window <= kMaxWindow, "conv_window in [1, 256]");
-    QPM_ARG_CHECK(P->row_lo >= 0 && P->row_lo < P->row_hi && P->row_hi <= P->NP, "row shard [row_lo, row_hi)");
+    QPM_ARG_CHECK(P->shard_world >= 1 && P->shard_rank >= 0 && P->shard_rank < P->shard_world,
+                  "shard_rank in [0, shard_world)");
     QPM_ARG_CHECK(P->NP < (1LL << 30), "NP < 2^30");
+    const Problem &gp = prob->p;
+    if (P->shard_world > 1) {
+        QPM_ARG_CHECK(P->fitness_mode == QPM_MODE_FAST,
+                      "multi-GPU runs score in fast mode (exact mode is the single-GPU parity tool)");
+        QPM_ARG_CHECK(gp.S >= P->shard_world,
+                      "fewer fitness segments than ranks: D is too small for this many GPUs "
+                      "(QPM_SEG_CHUNKS can shorten the segments)");
+    }
     Engine *e = new Engine();
     e->prob = &prob->p;
     e->P = *P;
-    e->own_lo = P->row_lo;
-    e->own_hi = P->row_hi;
+    e->rank = P->shard_rank;
+    e->world = P->shard_world;
     e->stream = (cudaStream_t)stream;
     if (!e->stream) {
         // graphs cannot be captured on the legacy default stream: own a stream
@@ -1835,8 +1849,31 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     RunConsts &c = e->c;
     c.algorithm = P->algorithm;
     c.NP = P->NP;
-    c.D = prob->p.D;
-    c.W = prob->p.W;
+    c.Dg = gp.D;
+    if (e->world > 1) {
+        // rank k owns the fitness segments [floor(k S / W), floor((k+1) S / W))
+        // and the genes under them (segment boundaries are 128-domain aligned)
+        e->seg_lo = (int)((int64_t)e->rank * gp.S / e->world);
+        const int seg_hi = (int)((int64_t)(e->rank + 1) * gp.S / e->world);
+        e->seg_n = seg_hi - e->seg_lo;
+        e->S_slot = (gp.S + e->world - 1) / e->world;
+        const int64_t seg_len = (int64_t)gp.seg_chunks * 128;
+        c.g0 = e->seg_lo * seg_len;
+        const int64_t g1 = std::min<int64_t>(gp.D, seg_hi * seg_len);
+        const int rc = problem_slice(&gp, c.g0, g1 - c.g0, &e->lprob);
+        if (rc) {
+            engine_free(e);
+            return rc;
+        }
+        c.D = e->lprob->p.D;
+        c.W = e->lprob->p.W;
+    } else {
+        e->seg_n = gp.S;
+        e->S_slot = gp.S;
+        c.g0 = 0;
+        c.D = gp.D;
+        c.W = gp.W;
+    }
     c.Dp = c.W * 32;
     c.G = P->G;
     c.seed = (uint64_t)P->seed;
@@ -1864,11 +1901,9 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     c.adaptive = P->adaptive_branches;
     c.gwo_a0 = P->gwo_a0;
     {
-        int dev = 0, sms = 148, occ_a = 1;
+        int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_commit_cand_bits, kRowThreads, 0);
-        e->apply_grid = sms * std::max(occ_a, 1);
         e->plan_grid = sms * 2;
         if (const char *v = getenv("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
         if (const char *v = getenv("QPM_PLAN_FORK")) e->plan_after_trial = strcmp(v, "trial") == 0;
@@ -1938,6 +1973,10 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->st, 1);
     QPM_ALLOC(e->best_genome, c.Dp);
     QPM_ALLOC(e->best_bits, c.W);
+    if (e->world > 1) {
+        QPM_ALLOC(e->gpart, (size_t)e->world * gpart_slot(e));
+        QPM_ALLOC(e->ggains, (size_t)NP * gp.n_wl);
+    }  // one rank with a communicator: allocated by qpm_engine_set_comm
 #undef QPM_ALLOC
     if ((rc = scratch_reserve(e->prob, &e->fs, NP)) != 0) {
         engine_free(e);
@@ -2016,14 +2055,14 @@ int qpm_engine_destroy(qpm_engine *h) {
 
 int64_t qpm_engine_device_bytes(const qpm_engine *h) { return h ? h->e->device_bytes : -1; }
 
-int qpm_engine_init(qpm_engine *h) {
-    QPM_ARG_CHECK(h, "engine");
-    Engine *e = h->e;
+// generation 0: init_population, its fitness, statistics and trace row, and
+// the planner's draws for generation 1.  An emulated column shard (world > 1,
+// no communicator) stops after its fitness scan: the caller exchanges the
+// partials (qpm_engine_exchange_from) and calls qpm_engine_init_finish.
+static int init_tail(Engine *e) {
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
-    k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of);
-    QPM_LAUNCH_CHECK();
-    int rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->slot_of, c.NP, e->fit, e->P.fitness_mode, s, nullptr);
+    int rc = fit_finish(e, e->fit, s, nullptr);
     if (rc) return rc;
     if ((rc = launch_select_stats(e, 3, s))) return rc;
     k_copy_best<<<64, 256, 0, s>>>(c, e->st, e->slot_of, e->slot_bin, e->genome, e->bits, e->best_genome,
@@ -2031,8 +2070,40 @@ int qpm_engine_init(qpm_engine *h) {
     QPM_LAUNCH_CHECK();
     if (c.algorithm != QPM_ALGO_GWO && (rc = enqueue_planner(e, s))) return rc;  // generation 1's draws
     e->initialized = true;
+    e->init_pending = false;
     e->g_done = 0;
     return QPM_OK;
+}
+
+int qpm_engine_init(qpm_engine *h) {
+    QPM_ARG_CHECK(h, "engine");
+    Engine *e = h->e;
+    const RunConsts &c = e->c;
+    cudaStream_t s = e->stream;
+    k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of);
+    QPM_LAUNCH_CHECK();
+    int rc;
+    if (e->sharded()) {
+        if ((rc = fit_scan(e, e->bits, e->slot_of, e->fit, s, nullptr))) return rc;
+        if (!e->comm) {
+            e->init_pending = true;
+            return QPM_OK;
+        }
+        if ((rc = enqueue_exchange(e, 0))) return rc;
+    } else if ((rc = launch_fitness(e->prob, &e->fs, e->bits, c.W, e->slot_of, c.NP, e->fit, e->P.fitness_mode, s,
+                                    nullptr))) {
+        return rc;
+    }
+    return init_tail(e);
+}
+
+int qpm_engine_init_finish(qpm_engine *h) {
+    QPM_ARG_CHECK(h, "engine");
+    if (!h->e->init_pending) {
+        set_error("qpm_engine_init_finish without a pending emulated-shard init");
+        return QPM_ERR_STATE;
+    }
+    return init_tail(h->e);
 }
 
 int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
@@ -2224,26 +2295,21 @@ int qpm_nccl_unique_id(uint8_t *id_out) {
     return QPM_OK;
 }
 
-static int check_shard(Engine *e, int rank, int world) {
-    QPM_ARG_CHECK(world >= 1 && rank >= 0 && rank < world, "rank in [0, world)");
-    QPM_ARG_CHECK(e->c.NP % world == 0, "NP must be a multiple of the rank count (equal all-gather slices)");
-    const int64_t per = e->c.NP / world;
-    QPM_ARG_CHECK(e->own_lo == rank * per && e->own_hi == (rank + 1) * per,
-                  "row_lo/row_hi must be this rank's equal slice [rank NP/world, (rank+1) NP/world)");
-    QPM_ARG_CHECK(!e->exec, "the shard must be set before the first graph step");
-    e->rank = rank;
-    e->world = world;
-    return QPM_OK;
-}
-
 int qpm_engine_set_comm(qpm_engine *h, int rank, int world, const uint8_t *id) {
     QPM_ARG_CHECK(h && id, "engine, id");
     Engine *e = h->e;
-    int rc = check_shard(e, rank, world);
-    if (rc) return rc;
+    QPM_ARG_CHECK(rank == e->rank && world == e->world, "rank / world must match the engine's shard_rank / shard_world");
+    QPM_ARG_CHECK(!e->exec && !e->initialized, "the communicator must be set before qpm_engine_init");
+    int rc;
     if ((rc = nccl_load())) return rc;
     ncclUniqueIdPod uid;
     memcpy(uid.internal, id, sizeof(uid.internal));
+    if (!e->gpart) {  // one rank: the sharded flow needs its partial buffers too
+        QPM_ARG_CHECK(e->P.fitness_mode == QPM_MODE_FAST, "the collective path scores in fast mode");
+        if ((rc = dalloc(e, &e->gpart, (size_t)e->world * gpart_slot(e))) ||
+            (rc = dalloc(e, &e->ggains, (size_t)e->c.NP * e->prob->n_wl)))
+            return rc;
+    }
     const int r = g_nccl.init_rank(&e->comm, world, uid, rank);
     if (r != 0) {
         e->comm = nullptr;
@@ -2253,9 +2319,11 @@ int qpm_engine_set_comm(qpm_engine *h, int rank, int world, const uint8_t *id) {
     return QPM_OK;
 }
 
-int qpm_engine_set_shard(qpm_engine *h, int rank, int world) {
-    QPM_ARG_CHECK(h, "engine");
-    return check_shard(h->e, rank, world);
+int qpm_engine_columns(const qpm_engine *h, int64_t *g0, int64_t *d) {
+    QPM_ARG_CHECK(h && g0 && d, "engine, out");
+    *g0 = h->e->c.g0;
+    *d = h->e->c.D;
+    return QPM_OK;
 }
 
 int qpm_engine_phases(const qpm_engine *h) { return h ? phase_count(h->e) : -1; }
@@ -2279,15 +2347,15 @@ int qpm_engine_run_phase(qpm_engine *h, int phase) {
 
 int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase) {
     QPM_ARG_CHECK(dst && src, "engines");
+    (void)phase;  // every exchange moves the same buffer: the scanning rank's partial slot
     Engine *d = dst->e, *s = src->e;
-    QPM_ARG_CHECK(d->c.NP == s->c.NP && d->c.W == s->c.W, "engines of one sharded run");
-    const int64_t n_own = s->own_hi - s->own_lo;
+    QPM_ARG_CHECK(d->world > 1 && d->world == s->world && d->c.NP == s->c.NP && d->S_slot == s->S_slot &&
+                      d->rank != s->rank,
+                  "engines of one sharded run");
+    const size_t n = gpart_slot(s);
     QPM_CUDA_TRY(cudaStreamSynchronize(s->stream));
-    QPM_CUDA_TRY(cudaMemcpyAsync(d->cand + s->own_lo, s->cand + s->own_lo, sizeof(double) * n_own,
+    QPM_CUDA_TRY(cudaMemcpyAsync(d->gpart + s->rank * n, s->gpart + s->rank * n, sizeof(double) * n,
                                  cudaMemcpyDeviceToDevice, d->stream));
-    if (phase == 2 && d->c.algorithm == QPM_ALGO_HYBRID)
-        QPM_CUDA_TRY(cudaMemcpyAsync(d->cbits + s->own_lo * s->c.W, s->cbits + s->own_lo * s->c.W,
-                                     sizeof(uint32_t) * n_own * s->c.W, cudaMemcpyDeviceToDevice, d->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(d->stream));
     return QPM_OK;
 }
@@ -2322,6 +2390,7 @@ int qpm_engine_fitness_ptr(qpm_engine *h, double **fit_dev) {
 // per-id launch counts.  Not part of include/qpm_b200.h.
 int qpm_dev_trace_engine(int reset, unsigned long long *log, unsigned int *launches) {
 #ifdef QPM_TRACE
+    if (reset == 2) return qpm::trace_stamps_tu(log);  // intra-kernel stamps [kTraceIds][64][8]
     if (reset) return qpm::trace_reset_tu();
     return qpm::trace_read_tu(log, launches);
 #else

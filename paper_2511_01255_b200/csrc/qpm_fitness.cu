@@ -67,7 +67,19 @@ std::mutex g_cache_mu;
 std::vector<CachedBlock> g_cache;
 size_t g_cache_bytes = 0;
 constexpr size_t kCacheCap = (size_t)16 << 30;  // keep at most 16 GB idle
-size_t cache_round(size_t b) { return (std::max<size_t>(b, 16) + 255) & ~(size_t)255; }
+// size classes, so that engines whose small buffers differ a little (the
+// trace and schedule tables scale with G) still reuse blocks: powers of two
+// up to 4 MB, then multiples of 2 MB (waste < 2x below 4 MB, < 2 MB above)
+size_t cache_round(size_t b) {
+    b = std::max<size_t>(b, 256);
+    if (b <= ((size_t)4 << 20)) {
+        size_t p = 256;
+        while (p < b) p <<= 1;
+        return p;
+    }
+    const size_t m = (size_t)2 << 20;
+    return (b + m - 1) / m * m;
+}
 }  // namespace
 
 void *dev_cache_alloc(size_t bytes) {
@@ -509,8 +521,22 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
 // 32 runs are stitched by a fixed shuffle tree (deterministic).
 constexpr int kFinishWarps = 4;
 
+// Column-sharded runs (multi-GPU): rank k scored the global segments
+// [floor(k S / world), floor((k+1) S / world)) into its slot of the
+// all-gathered partials, laid out [world][n_wl][rows][S_slot][6]; segment s
+// lives in rank (world (s+1) - 1) / S.  One GPU: world = 1, S_slot = S.
+__device__ __forceinline__ const double *seg_ptr(const double *part, int s, int lam, int64_t r, int64_t rows, int n_wl,
+                                                 int S, int world, int S_slot) {
+    int rk = 0, loc = s;
+    if (world > 1) {
+        rk = (world * (s + 1) - 1) / S;
+        loc = s - (rk * S) / world;
+    }
+    return part + ((((int64_t)rk * n_wl + lam) * rows + r) * S_slot + loc) * kPartDoubles;
+}
+
 __global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
-    const double *part, int S, int64_t rows, int n_wl, const double2 *__restrict__ w,
+    const double *part, int S, int world, int S_slot, int64_t rows, int n_wl, const double2 *__restrict__ w,
     const double2 *__restrict__ h, int thg, double scale, int multi, double g0, double beta,
     double *__restrict__ gains, double *__restrict__ out) {
     QTRACE(2);
@@ -524,15 +550,15 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
     const int s1 = s0 + per < S ? s0 + per : S;
     double gmax = 0.0, gmin = 0.0;
     for (int lam = 0; lam < n_wl; ++lam) {
-        const double *p = part + ((int64_t)lam * rows + r) * S * kPartDoubles;
         double ar, ai;
         if (S == 1) {
+            const double *p = part + ((int64_t)lam * rows + r) * kPartDoubles;
             ar = __ldcg(p);  // exact mode: the row's sum, untouched
             ai = __ldcg(p + 1);
         } else {
             Seg acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             for (int s = s0; s < s1; ++s) {
-                const double *q = p + (int64_t)s * kPartDoubles;
+                const double *q = seg_ptr(part, s, lam, r, rows, n_wl, S, world, S_slot);
                 const Seg y = {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5)};
                 acc = s == s0 ? y : seg_cat(acc, y);
             }
@@ -671,6 +697,31 @@ static int problem_reserve(Problem *p, int64_t rows) {
 // With pdl the kernels may become resident while their predecessor still
 // writes: everything a predecessor produces (bits, row ids, partials) is read
 // with ld.global.cg (__ldcg), never through the non-coherent read-only path.
+int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index,
+                        int64_t rows, double *part, int S_stride, cudaStream_t stream, int *launches, bool pdl) {
+    QPM_ARG_CHECK(row_words == p->W, "row_words must equal the problem's row words");
+    if (rows == 0) return QPM_OK;
+    const int thg = p->process == QPM_PROCESS_THG;
+    const dim3 grid((unsigned)p->S, (unsigned)((rows + kFitThreads - 1) / kFitThreads), (unsigned)p->n_wl);
+    QPM_CUDA_TRY(launch_k(pdl, thg ? k_fit_fast<true> : k_fit_fast<false>, grid, dim3(kFitThreads), kFitSmem, stream,
+                          (const double2 *)p->qt, p->nquads, p->nchunks, p->seg_chunks, S_stride, bits, p->W, row_index,
+                          rows, part));
+    if (launches) *launches += 1;
+    return QPM_OK;
+}
+
+int launch_fitness_finish(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
+                          double *gains, double *out, cudaStream_t stream, int *launches, bool pdl) {
+    if (rows == 0) return QPM_OK;
+    const int thg = p->process == QPM_PROCESS_THG;
+    QPM_CUDA_TRY(launch_k(pdl, k_fit_finish, dim3((unsigned)((rows + kFinishWarps - 1) / kFinishWarps)),
+                          dim3(32 * kFinishWarps), 0, stream, part, S, world, S_slot, rows, p->n_wl,
+                          (const double2 *)p->w, (const double2 *)p->h, thg, p->scale, p->multi, p->g0, p->beta,
+                          gains, out));
+    if (launches) *launches += 1;
+    return QPM_OK;
+}
+
 int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
                    const int32_t *row_index, int64_t rows, double *out, int mode, cudaStream_t stream, int *launches,
                    bool pdl) {
@@ -685,18 +736,62 @@ int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64
         const dim3 grid((unsigned)((rows + 127) / 128), (unsigned)p->n_wl);
         QPM_CUDA_TRY(launch_k(pdl, k_fit_exact, grid, dim3(128), 0, stream, (const double2 *)p->e1, (const double2 *)p->b,
                               p->D, thg, bits, p->W, row_index, rows, fs->part));
+        if (launches) *launches += 1;
     } else {
         S = p->S;
-        const dim3 grid((unsigned)S, (unsigned)((rows + kFitThreads - 1) / kFitThreads), (unsigned)p->n_wl);
-        QPM_CUDA_TRY(launch_k(pdl, thg ? k_fit_fast<true> : k_fit_fast<false>, grid, dim3(kFitThreads), kFitSmem,
-                              stream, (const double2 *)p->qt, p->nquads, p->nchunks, p->seg_chunks, S, bits, p->W,
-                              row_index, rows, fs->part));
+        const int rc = launch_fitness_scan(p, bits, row_words, row_index, rows, fs->part, S, stream, launches, pdl);
+        if (rc) return rc;
     }
-    QPM_CUDA_TRY(launch_k(pdl, k_fit_finish, dim3((unsigned)((rows + kFinishWarps - 1) / kFinishWarps)),
-                          dim3(32 * kFinishWarps), 0, stream, (const double *)fs->part, S, rows, p->n_wl,
-                          (const double2 *)p->w, (const double2 *)p->h, thg, p->scale, p->multi, p->g0, p->beta,
-                          fs->gains, out));
-    if (launches) *launches += 2;
+    return launch_fitness_finish(p, fs->part, S, 1, S, rows, fs->gains, out, stream, launches, pdl);
+}
+
+// A problem over domains [g0, g0 + Dl) of `p` (column shard of a multi-GPU
+// run): tables sliced on the device, the parent's segment length, so its
+// segments are exactly the parent's segments in that range (g0 is a segment
+// boundary).  w / hconst / scale are copied but only the parent's are used
+// to finish (the shard only scans).
+int problem_slice(const Problem *p, int64_t g0, int64_t Dl, qpm_problem **out) {
+    QPM_ARG_CHECK(g0 >= 0 && Dl >= 1 && g0 + Dl <= p->D && g0 % ((int64_t)p->seg_chunks * 128) == 0,
+                  "slice must start on a segment boundary");
+    auto *h = new qpm_problem();
+    Problem &q = h->p;
+    q.mu = new std::mutex();
+    q.process = p->process;
+    q.multi = p->multi;
+    q.n_wl = p->n_wl;
+    q.D = Dl;
+    q.W = round_up((Dl + 31) / 32, 4);
+    q.nquads = q.W * 8;
+    q.nchunks = q.W / 4;
+    q.seg_chunks = p->seg_chunks;
+    q.S = (int)((q.nchunks + q.seg_chunks - 1) / q.seg_chunks);
+    q.scale = p->scale;
+    q.g0 = p->g0;
+    q.beta = p->beta;
+    const int n_wl = p->n_wl;
+    const size_t tab = (size_t)n_wl * Dl * sizeof(double2);
+    const size_t qtb = (size_t)n_wl * q.nquads * kQuadEntries * sizeof(double2);
+    auto fail = [&](const char *what) {
+        set_error("problem slice: %s", what);
+        qpm_problem_destroy(h);
+        return QPM_ERR_CUDA;
+    };
+    if (cudaMalloc(&q.e1, tab) != cudaSuccess || cudaMalloc(&q.b, tab) != cudaSuccess ||
+        cudaMalloc(&q.qt, qtb) != cudaSuccess || cudaMalloc(&q.w, n_wl * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&q.h, n_wl * sizeof(double2)) != cudaSuccess)
+        return fail("cudaMalloc");
+    q.device_bytes = (int64_t)(2 * tab + qtb + 2 * n_wl * sizeof(double2));
+    const size_t row = (size_t)Dl * sizeof(double2), pitch = (size_t)p->D * sizeof(double2);
+    if (cudaMemcpy2D(q.e1, row, p->e1 + g0, pitch, row, n_wl, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy2D(q.b, row, p->b + g0, pitch, row, n_wl, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy(q.w, p->w, n_wl * sizeof(double2), cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy(q.h, p->h, n_wl * sizeof(double2), cudaMemcpyDeviceToDevice) != cudaSuccess)
+        return fail("table copy");
+    const int64_t nt = q.nquads * n_wl;
+    k_build_quads<<<(unsigned)((nt + 127) / 128), 128>>>(q.e1, q.b, Dl, q.nquads, n_wl, q.process == QPM_PROCESS_THG,
+                                                          q.qt);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return fail("quad tables");
+    *out = h;
     return QPM_OK;
 }
 

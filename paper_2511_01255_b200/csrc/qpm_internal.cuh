@@ -211,6 +211,17 @@ cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
 }
 
 int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out, cudaStream_t stream);
+// fast-mode segment scan into part ([n_wl][rows][S_stride][6], S_stride >= p->S)
+int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index,
+                        int64_t rows, double *part, int S_stride, cudaStream_t stream, int *launches, bool pdl);
+// stitch + objective of rows whose S segment partials are in part (world > 1:
+// all-gathered column-shard slots [world][n_wl][rows][S_slot][6])
+int launch_fitness_finish(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
+                          double *gains, double *out, cudaStream_t stream, int *launches, bool pdl);
+}  // namespace qpm
+struct qpm_problem;
+namespace qpm {
+int problem_slice(const Problem *p, int64_t g0, int64_t Dl, qpm_problem **out);
 
 }  // namespace qpm
 

@@ -1,26 +1,30 @@
-"""Multi-GPU HWSDA: one process per GPU, rows sharded, NCCL over NVLink.
+"""Multi-GPU HWSDA: one process per GPU, genes sharded by columns, NCCL over NVLink.
 
-Scheme ("exact scheme"):
+Scheme (a column variant of SURVEY.md §8(e)'s exact scheme):
 
-* every rank keeps the whole population (C3: 6.5 GB of f64 genome, far below
-  180 GB of HBM) and owns an equal contiguous slice of rows;
-* per generation each rank builds and scores the DE trials of its own rows,
-  then the candidate fitness vector (NP doubles) is all-gathered; every rank
-  recomputes the trials other ranks accepted from the same counter streams
-  (bit-identical arithmetic), so the replicas stay identical without moving
-  genomes;
-* the wolf phase scores own rows, then all-gathers the candidate fitness and
-  the candidates' sign bits (D/8 bytes per row), which is cheaper than
-  recomputing three random draws per gene;
-* leaders, selection, statistics and the F update are computed redundantly
-  on every rank from identical data, so they need no further collective.
+* the genes are split into contiguous column ranges aligned to the fitness
+  segments: rank k owns the genes under segments [floor(k S / W),
+  floor((k+1) S / W)) of every individual (S = the problem's segments);
+* every per-gene operation only touches its own column of other rows: the DE
+  trial x_r1 + F (x_r2 - x_r3) and the crossover mask, the wolf draws and the
+  leader vote (leaders' columns are local), init_population, run_gwo's
+  continuous move; so each rank runs them on its columns of all NP rows, with
+  the stream positions of the global gene index (bit-identical draws);
+* each rank scans the fitness segments of its columns for all rows; the
+  segment partials (NP x 48 B per segment) are all-gathered and every rank
+  stitches and scores all rows in the single-GPU segment order (fast mode
+  fitness is bit-identical to one GPU);
+* selection, leaders, statistics and the F update run replicated on every
+  rank from identical data, so they need no further collective.
 
-The collectives run inside the engine (libqpm_b200.so calls ncclAllGather on
-the engine stream, captured into the per-generation CUDA graph).  The NCCL
+Per generation a hybrid run all-gathers the partials twice (DE and wolf
+candidates); nothing else moves: no genome rows, no recomputation.  The
+collectives run inside the engine (libqpm_b200.so calls ncclAllGather on the
+engine stream, captured into the per-generation CUDA graph).  The NCCL
 communicator is bootstrapped from a unique id that rank 0 creates and
 torch.distributed broadcasts.  `EmulatedShards` drives W shard engines on one
-GPU with host-side exchanges between phases, so the sharded path can be
-tested bit-exactly against the single engine without several GPUs.
+GPU with device-copy exchanges between phases, so the sharded path is tested
+bit-exactly against the single engine without several GPUs.
 """
 
 import ctypes
@@ -29,17 +33,26 @@ from dataclasses import replace
 import numpy as np
 
 from . import _native
-from .optimizer import DEParams, Engine, GWOParams, RunResult, Schedules, _trace_rows
+from .optimizer import DEParams, Engine, GWOParams, Individual, RunResult, Schedules, _trace_rows
 
 
-def shard_rows(pop_size: int, world: int, rank: int) -> tuple[int, int]:
-    """Equal contiguous row slice of `rank` (NP must be a multiple of world)."""
+def shard_columns(D: int, world: int, rank: int, n_wl: int = 1, seg_chunks: int | None = None) -> tuple[int, int]:
+    """Gene columns [g0, g1) of `rank` (the engine's split, qpm_engine_create):
+    rank k owns the fitness segments [floor(k S / W), floor((k+1) S / W)) of
+    the problem and the genes under them; a segment is seg_chunks 128-domain
+    chunks (4, or 4 min(n_wl, 8) with several wavelengths)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside [0, {world})")
-    if pop_size % world:
-        raise ValueError(f"population size {pop_size} is not a multiple of the rank count {world}")
-    per = pop_size // world
-    return rank * per, (rank + 1) * per
+    words = -(-(-(-D // 32)) // 4) * 4
+    nchunks = words // 4
+    if seg_chunks is None:
+        seg_chunks = max(1, min(nchunks, 4 * min(n_wl, 8) if n_wl > 1 else 4))
+    S = -(-nchunks // seg_chunks)
+    if S < world:
+        raise ValueError(f"{S} fitness segments cannot be split over {world} ranks")
+    lo, hi = rank * S // world, (rank + 1) * S // world
+    seg = seg_chunks * 128
+    return lo * seg, min(D, hi * seg)
 
 
 def nccl_unique_id() -> bytes:
@@ -58,22 +71,22 @@ def broadcast_unique_id(group=None) -> bytes:
 
 
 class ShardedEngine(Engine):
-    """An Engine owning rows [lo, hi) of a run spread over `world` ranks."""
+    """An Engine owning the gene columns [g0, g0 + Dl) of a run spread over `world` ranks."""
 
     @classmethod
     def create(cls, objective, algorithm, *, pop_size, generations, seed, de, gwo, sch, rank, world,
                nccl_id=None, fitness_mode=None, bounds=(-1.0, 1.0), stream=None):
+        if world < 1 or not 0 <= rank < world:
+            raise ValueError(f"rank {rank} outside [0, {world})")
         eng = Engine.__new__(cls)
         eng.rank, eng.world = rank, world
-        eng.row_lo, eng.row_hi = shard_rows(pop_size, world, rank)
         Engine.__init__(eng, objective, algorithm, pop_size=pop_size, generations=generations, seed=seed, de=de,
                         gwo=gwo, sch=sch, fitness_mode=fitness_mode, bounds=bounds, stream=stream,
-                        row_range=(eng.row_lo, eng.row_hi))
+                        shard=(rank, world))
+        eng.emulated = nccl_id is None and world > 1
         if nccl_id is not None:
             idb = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
             _native.check(_native.lib().qpm_engine_set_comm(eng.handle, rank, world, idb), "qpm_engine_set_comm")
-        elif world > 1:
-            _native.check(_native.lib().qpm_engine_set_shard(eng.handle, rank, world), "qpm_engine_set_shard")
         return eng
 
     @property
@@ -83,9 +96,28 @@ class ShardedEngine(Engine):
     def run_phase(self, phase: int):
         _native.check(_native.lib().qpm_engine_run_phase(self.handle, int(phase)), "qpm_engine_run_phase")
 
+    def init_finish(self):
+        _native.check(_native.lib().qpm_engine_init_finish(self.handle), "qpm_engine_init_finish")
+
     def exchange_from(self, other: "ShardedEngine", phase: int):
         _native.check(_native.lib().qpm_engine_exchange_from(self.handle, other.handle, int(phase)),
                       "qpm_engine_exchange_from")
+
+    def best_columns(self) -> tuple[int, Individual]:
+        """(g0, this shard's columns of the final best individual)."""
+        return self.g0, Engine.best(self)
+
+
+def assemble_best(parts, D: int) -> Individual:
+    """The full best individual from every rank's (g0, columns) part."""
+    genome = np.empty(D, dtype=np.float64)
+    proj = np.empty(D, dtype=np.int8)
+    fit = None
+    for g0, ind in parts:
+        genome[g0:g0 + ind.genome.size] = ind.genome
+        proj[g0:g0 + ind.projection.size] = ind.projection
+        fit = ind.fitness
+    return Individual(genome=genome, projection=proj, fitness=fit)
 
 
 class EmulatedShards:
@@ -93,16 +125,29 @@ class EmulatedShards:
 
     Test harness for the sharded protocol: every kernel a real rank runs is
     run by its shard engine; the NCCL all-gather is replaced by device copies
-    of each shard's own slices into the other shards' buffers.
+    of each shard's segment partials into the other shards' buffers.
     """
 
     def __init__(self, objective, algorithm, world: int, **kw):
+        self.D = objective.dimension
         self.engines = [ShardedEngine.create(objective, algorithm, rank=r, world=world, nccl_id=None, **kw)
                         for r in range(world)]
+
+    def _exchange(self, ph):
+        import torch
+
+        torch.cuda.synchronize()
+        for dst in self.engines:
+            for src in self.engines:
+                if src is not dst:
+                    dst.exchange_from(src, ph)
 
     def init(self):
         for e in self.engines:
             e.init()
+        self._exchange(0)
+        for e in self.engines:
+            e.init_finish()
 
     def step(self, n: int):
         import torch
@@ -111,11 +156,7 @@ class EmulatedShards:
         for _ in range(n):
             for ph in range(phases):
                 if ph > 0:
-                    torch.cuda.synchronize()
-                    for dst in self.engines:
-                        for src in self.engines:
-                            if src is not dst:
-                                dst.exchange_from(src, ph)
+                    self._exchange(ph)
                 for e in self.engines:
                     e.run_phase(ph)
         torch.cuda.synchronize()
@@ -123,6 +164,18 @@ class EmulatedShards:
     def finalize(self):
         for e in self.engines:
             e.finalize()
+
+    def best(self) -> Individual:
+        return assemble_best([e.best_columns() for e in self.engines], self.D)
+
+    def population(self):
+        """(genome [NP, D], fitness [NP]) assembled from the shards' columns."""
+        parts = [(e.g0, e.population()) for e in self.engines]
+        NP = self.engines[0].NP
+        genome = np.empty((NP, self.D), dtype=np.float64)
+        for g0, (g, _) in parts:
+            genome[:, g0:g0 + g.shape[1]] = g
+        return genome, parts[0][1][1]
 
 
 def run_sharded(algorithm: str, objective, *, dimension: int, pop_size: int, generations: int, seed: int,
@@ -146,7 +199,13 @@ def run_sharded(algorithm: str, objective, *, dimension: int, pop_size: int, gen
     eng.init()
     eng.step(generations, use_graph=use_graph)
     eng.finalize()
-    return RunResult(best=eng.best(), trace=_trace_rows(eng.trace(0, generations + 1)))
+    part = eng.best_columns()
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, part, group=group)
+    else:
+        parts = [part]
+    return RunResult(best=assemble_best(parts, dimension), trace=_trace_rows(eng.trace(0, generations + 1)))
 
 
 def replicas_trace_equal(traces) -> bool:

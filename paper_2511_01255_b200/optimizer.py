@@ -216,7 +216,7 @@ class Engine:
 
     def __init__(self, objective: GpuPatternObjective, algorithm: str, *, pop_size: int, generations: int,
                  seed: int, de: DEParams, gwo: GWOParams, sch: Schedules, fitness_mode: str | None = None,
-                 bounds: tuple[float, float] = (-1.0, 1.0), stream=None, row_range: tuple[int, int] | None = None):
+                 bounds: tuple[float, float] = (-1.0, 1.0), stream=None, shard: tuple[int, int] = (0, 1)):
         import torch
 
         if not isinstance(objective, GpuPatternObjective):
@@ -251,7 +251,7 @@ class Engine:
         p.conv_window = max(1, int(sch.conv_window))
         p.adaptive_branches = int(bool(sch.adaptive_branches))
         p.gwo_lo, p.gwo_hi, p.gwo_a0 = float(bounds[0]), float(bounds[1]), gwo.a
-        p.row_lo, p.row_hi = row_range if row_range is not None else (0, self.NP)
+        p.shard_rank, p.shard_world = int(shard[0]), int(shard[1])
         self.params = p
         self.sched = np.ascontiguousarray(schedule_table(self.G, de, gwo, sch))
         h = ctypes.c_void_p()
@@ -259,6 +259,10 @@ class Engine:
                                                       self.sched.ctypes.data, self.stream.cuda_stream),
                       "qpm_engine_create")
         self.handle = h
+        g0, dl = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(_native.lib().qpm_engine_columns(h, ctypes.byref(g0), ctypes.byref(dl)), "qpm_engine_columns")
+        # this engine's genes [g0, g0 + Dl): all of them on one GPU, a column shard on several
+        self.g0, self.Dl = int(g0.value), int(dl.value)
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -309,15 +313,17 @@ class Engine:
         return out
 
     def best(self) -> Individual:
-        genome = np.empty(self.D, dtype=np.float64)
-        proj = np.empty(self.D, dtype=np.int8)
+        """The final best individual (a column shard returns its columns [g0, g0 + Dl))."""
+        genome = np.empty(self.Dl, dtype=np.float64)
+        proj = np.empty(self.Dl, dtype=np.int8)
         fit = np.empty(1, dtype=np.float64)
         _native.check(_native.lib().qpm_engine_read_best(self.handle, genome.ctypes.data, proj.ctypes.data,
                                                          fit.ctypes.data), "qpm_engine_read_best")
         return Individual(genome=genome, projection=proj, fitness=float(fit[0]))
 
     def population(self):
-        genome = np.empty((self.NP, self.D), dtype=np.float64)
+        """(genome [NP, Dl], fitness [NP]); a column shard returns its columns."""
+        genome = np.empty((self.NP, self.Dl), dtype=np.float64)
         fit = np.empty(self.NP, dtype=np.float64)
         _native.check(_native.lib().qpm_engine_read_population(self.handle, genome.ctypes.data, fit.ctypes.data),
                       "qpm_engine_read_population")

@@ -1,0 +1,78 @@
+"""Per-rank GPU time of the sharded engine at world W, emulated on one GPU.
+
+    python tools/shard_probe.py [--world 8] [--np-per-rank 1024] [--d 10000] [--gens 10]
+W shard engines of one run (EmulatedShards protocol); after a warm-up, each
+generation's phases of rank 0 are run alone between synchronisations and timed
+with CUDA events on its stream.  The NCCL all-gathers are replaced by device
+copies (not timed), so the result is rank 0's kernel time per generation; the
+exchange adds NP*8 B (+ NP*D/8 B of wolf rows) of all-gather per generation.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--world", type=int, default=8)
+    ap.add_argument("--np-per-rank", type=int, default=1024)
+    ap.add_argument("--d", type=int, default=10_000)
+    ap.add_argument("--warm", type=int, default=30)
+    ap.add_argument("--gens", type=int, default=10)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    import paper_2511_01255_b200 as q
+    from paper_2511_01255_b200.distributed import EmulatedShards
+
+    torch.cuda.set_device(0)
+    NP = args.np_per_rank * args.world
+    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, args.d)
+    kw = dict(pop_size=NP, generations=1000, seed=0, de=q.DEParams(), gwo=q.GWOParams(), sch=q.Schedules())
+    sh = EmulatedShards(obj, "hybrid", args.world, **kw)
+    sh.init()
+    sh.step(args.warm)
+    engines = sh.engines
+    phases = engines[0].phases
+    per_phase = np.zeros(phases)
+    for _ in range(args.gens):
+        for ph in range(phases):
+            if ph > 0:
+                torch.cuda.synchronize()
+                for dst in engines:
+                    for src in engines:
+                        if src is not dst:
+                            dst.exchange_from(src, ph)
+            torch.cuda.synchronize()
+            s = engines[0].stream
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            engines[0].run_phase(ph)
+            e1.record(s)
+            torch.cuda.synchronize()
+            per_phase[ph] += e0.elapsed_time(e1) * 1e3
+            for e in engines[1:]:
+                e.run_phase(ph)
+    torch.cuda.synchronize()
+    per_phase /= args.gens
+    single = q.Engine(obj, "hybrid", **kw)
+    single.init()
+    single.step(args.warm)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(single.stream)
+    single.step(args.gens)
+    e1.record(single.stream)
+    torch.cuda.synchronize()
+    one = e0.elapsed_time(e1) * 1e3 / args.gens
+    print(json.dumps({"world": args.world, "NP": NP, "D": args.d, "rank0_us_per_phase": per_phase.round(2).tolist(),
+                      "rank0_us_per_gen": float(per_phase.sum()), "single_gpu_us_per_gen_same_NP": one,
+                      "note": "eager phases (no graph, no PDL), exchanges untimed"}))
+
+
+if __name__ == "__main__":
+    main()

@@ -87,6 +87,8 @@ def main():
               f"{(rel[:, 2] - rel[:, 1]).mean():8.2f}")
     print("fit_fast CTA 0 stamps (us from start): bits, first table, loop end, stored =",
           [round(float(x), 2) for x in stamps(L)[1:5]])
+    print("select_stats stamps (us from start): selected, synced, max/min, mean, var, tail =",
+          [round(float(x), 2) for x in stamps(L, "qpm_dev_trace_engine", 5, 7)[1:7]])
 
 
 
