@@ -564,8 +564,14 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
     r.t = a.gthr[g];
 }
 
-template <bool BIN, bool FULL, int K>
-__device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int jc) {
+constexpr int kDeSteps = 2;  // 64-gene warp steps per k_de_trial batch (registers)
+
+// One warp's share of a row: nb batches of kDeSteps 64-gene steps, step st of
+// batch bt at genes j0 + (bt kDeSteps + st) SPAN (SPAN = 512: the eight warps of
+// a CTA interleave over a chunk; SPAN = 64: one warp walks a whole row).
+template <bool BIN, bool FULL, int K, int SPAN>
+__device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int j0,
+                                               int nb) {
     // A warp covers 64 genes per step: lane l owns genes l and l+32, so every
     // load/store is one coalesced 256-byte warp access and the two sign words
     // are plain ballots.
@@ -585,21 +591,18 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
     const uint64_t gnon = (uint64_t)(uint32_t)(early ? 2 * c.Dg : 5 * c.Dg) * kGold;
     const uint32_t Hcr = top_thr(c.thr_cr);
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    constexpr int kSteps = 2;               // 64-gene warp steps per batch (registers)
-    constexpr int kSpan = kRowThreads * 2;  // genes per CTA step
-    constexpr int kBatches = kDeChunk / (kSpan * kSteps);
+    constexpr int kSpan = SPAN;
 #pragma unroll 1
-    for (int bt = 0; bt < kBatches; ++bt) {
-        const int jb = jc + bt * kSpan * kSteps + warp * 64;
+    for (int bt = 0; bt < nb; ++bt) {
+        const int jb = j0 + bt * kSpan * kDeSteps;
         if (!FULL && jb >= (int)c.Dp) break;
         // mask bits, then every genome load of the batch, the math and the
         // stores, then the wolf draws (other warps' loads are in flight)
-        uint32_t mb[kSteps];
+        uint32_t mb[kDeSteps];
         bool tie = false;
         const uint64_t zb = key + (uint64_t)(p_mask + (uint32_t)(jb + lane)) * kGold;  // mask draw of gene jb + lane
 #pragma unroll
-        for (int st = 0; st < kSteps; ++st) {
+        for (int st = 0; st < kDeSteps; ++st) {
             mb[st] = 0u;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -615,7 +618,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
         }
         if (__any_sync(0xffffffffu, tie) && tie) {  // a high-word tie (p = 2^-32): exact compares
 #pragma unroll
-            for (int st = 0; st < kSteps; ++st) {
+            for (int st = 0; st < kDeSteps; ++st) {
                 mb[st] = 0u;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -625,9 +628,9 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 }
             }
         }
-        double y[kSteps][2], p1[kSteps][2], p2[kSteps][2], p3[kSteps][2];
+        double y[kDeSteps][2], p1[kDeSteps][2], p2[kDeSteps][2], p3[kDeSteps][2];
 #pragma unroll
-        for (int st = 0; st < kSteps; ++st) {
+        for (int st = 0; st < kDeSteps; ++st) {
             const int j64 = jb + st * kSpan;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -651,7 +654,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             }
         }
 #pragma unroll
-        for (int st = 0; st < kSteps; ++st) {
+        for (int st = 0; st < kDeSteps; ++st) {
             const int j64 = jb + st * kSpan;  // this warp's 64-gene span
             if (!FULL && j64 >= (int)c.Dp) break;
             bool neg[2];
@@ -675,10 +678,10 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             }
         }
         if (K > 0) {  // after the stores: the load registers are free again
-            uint32_t code[kSteps][2];
+            uint32_t code[kDeSteps][2];
             bool wtie = false;
 #pragma unroll
-            for (int st = 0; st < kSteps; ++st) {
+            for (int st = 0; st < kDeSteps; ++st) {
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const int jj = jb + st * kSpan + lane + 32 * q;
@@ -691,7 +694,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             }
             if (__any_sync(0xffffffffu, wtie) && wtie) {
 #pragma unroll
-                for (int st = 0; st < kSteps; ++st) {
+                for (int st = 0; st < kDeSteps; ++st) {
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const int jj = jb + st * kSpan + lane + 32 * q;
@@ -703,7 +706,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 }
             }
 #pragma unroll
-            for (int st = 0; st < kSteps; ++st) {
+            for (int st = 0; st < kDeSteps; ++st) {
                 const int j64 = jb + st * kSpan;
                 if (!FULL && j64 >= (int)c.Dp) break;
 #pragma unroll
@@ -712,23 +715,57 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
             }
         }
     }
-    if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
 }
 
 template <int K>
 __device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const TrialArgs &a, const TrialRow &r, int jc) {
+    constexpr int kSpan = kRowThreads * 2;  // genes per CTA step
+    constexpr int kBatches = kDeChunk / (kSpan * kDeSteps);
     const bool full = jc + kDeChunk <= (int)c.D;
+    const int j0 = jc + (int)(threadIdx.x >> 5) * 64;
     if (r.bin) {
         if (full)
-            de_trial_chunk<true, true, K>(c, a, r, jc);
+            de_trial_chunk<true, true, K, kSpan>(c, a, r, j0, kBatches);
         else
-            de_trial_chunk<true, false, K>(c, a, r, jc);
+            de_trial_chunk<true, false, K, kSpan>(c, a, r, j0, kBatches);
     } else {
         if (full)
-            de_trial_chunk<false, true, K>(c, a, r, jc);
+            de_trial_chunk<false, true, K, kSpan>(c, a, r, j0, kBatches);
         else
-            de_trial_chunk<false, false, K>(c, a, r, jc);
+            de_trial_chunk<false, false, K, kSpan>(c, a, r, j0, kBatches);
     }
+    if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
+}
+
+// Short rows (a column shard of a multi-GPU run; Dp <= kDeRowsMaxDp): one
+// warp per row walks all of its genes, eight rows per CTA.  Each warp
+// resolves its own row (lane 0, broadcast through shared memory) with no CTA
+// barrier, so a row's setup latency hides under the other warps' work instead
+// of being paid once per 1-2 k-gene CTA.
+constexpr int kDeRowsMaxDp = 4096;
+template <int K>
+__global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_rows(RunConsts c, TrialArgs a) {
+    QTRACE(0);
+    pdl_wait();
+    QTRACE_STARTED();
+    constexpr int kWarps = kRowThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = a.row_lo + (int64_t)blockIdx.x * kWarps + warp;
+    if (i >= a.row_lo + a.n_rows) return;  // warp-uniform
+    __shared__ TrialRow s_rows[kWarps];
+    if (lane == 0) trial_row_setup(c, a, a.st->g, i, s_rows[warp]);
+    __syncwarp();
+    const TrialRow &r = s_rows[warp];
+    constexpr int kB = 64 * kDeSteps;  // genes per warp batch
+    const int nfull = (int)c.D / kB, ntot = (int)((c.Dp + kB - 1) / kB);
+    if (r.bin) {
+        de_trial_chunk<true, true, K, 64>(c, a, r, 0, nfull);
+        de_trial_chunk<true, false, K, 64>(c, a, r, nfull * kB, ntot - nfull);
+    } else {
+        de_trial_chunk<false, true, K, 64>(c, a, r, 0, nfull);
+        de_trial_chunk<false, false, K, 64>(c, a, r, nfull * kB, ntot - nfull);
+    }
+    if (lane == 0) a.slot_bin[r.out_slot] = 0;
 }
 
 // one CTA per (row, kDeChunk genes).  K = leader count when the CTA also
@@ -783,9 +820,12 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
     QTRACE(4);
     pdl_wait();
     QTRACE_STARTED();
-    // one CTA row per individual: the row-level decisions are CTA-uniform
-    const int64_t i = a.row_lo + blockIdx.y;
-    const int w = (int)(blockIdx.x * kApplyThreads + threadIdx.x);
+    // one thread per (individual, 32-gene word), flattened: short rows (a
+    // column shard of a multi-GPU run) leave no idle lanes
+    const int64_t idx = (int64_t)blockIdx.x * kApplyThreads + threadIdx.x;
+    if (idx >= a.n_rows * c.W) return;
+    const int64_t i = a.row_lo + idx / c.W;
+    const int w = (int)(idx % c.W);
     int32_t lead[K];
 #pragma unroll
     for (int t = 0; t < K; ++t) lead[t] = a.st->leaders[t];
@@ -1396,6 +1436,7 @@ struct Engine {
     bool wolf_side = false;         // this generation's planes on the side stream during the DE fitness (QPM_WOLF=side)
     cudaEvent_t ev_wfork = nullptr, ev_wjoin = nullptr;
     int topk_threads = kCtaThreads;   // k_select_topk block (QPM_TOPK_THREADS)
+    int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-per-row trial kernel up to this row length (QPM_DE_ROWS)
     int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
     int64_t g_done = 0;
@@ -1696,7 +1737,13 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         // tail, including its planner branch
         const unsigned items = (unsigned)(NP * de_chunks);
         const bool wolf_side = hybrid && e->wolf_side;
-        if (!hybrid || e->wolf_in_planner || wolf_side)
+        const bool rows_mode = c.Dp <= e->de_rows_max_dp && !e->wolf_mixed;
+        const unsigned row_ctas = (unsigned)((NP + kRowThreads / 32 - 1) / (kRowThreads / 32));
+        if (rows_mode) {
+            const bool k0 = !hybrid || e->wolf_in_planner || wolf_side;
+            QPM_CUDA_TRY(launch_k(false, k0 ? k_de_trial_rows<0> : (c.k == 4 ? k_de_trial_rows<4> : k_de_trial_rows<3>),
+                                  dim3(row_ctas), dim3(kRowThreads), 0, s, c, all));
+        } else if (!hybrid || e->wolf_in_planner || wolf_side)
             QPM_CUDA_TRY(launch_k(false, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, all));
         else if (e->wolf_mixed)
             QPM_CUDA_TRY(launch_k(false, c.k == 4 ? k_de_trial_mixed<4> : k_de_trial_mixed<3>, dim3(2 * items),
@@ -1736,8 +1783,8 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         if (e->wolf_side) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
         QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
-                              dim3((unsigned)((c.W + kApplyThreads - 1) / kApplyThreads), (unsigned)NP),
-                              dim3(kApplyThreads), 0, s, c, all));
+                              dim3((unsigned)((NP * c.W + kApplyThreads - 1) / kApplyThreads)), dim3(kApplyThreads),
+                              0, s, c, all));
         QPM_LAUNCH_CHECK();
         *n += 2;
         mark("fitness_gwo");
@@ -1918,6 +1965,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         // they never did
         if (e->wolf_in_planner) e->plan_after_trial = true;
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
+        if (const char *v = getenv("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
         auto cta_knob = [](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
             if (const char *v = getenv(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
         };

@@ -2,6 +2,7 @@
 
     python tools/gen_sweep.py 'QPM_PDL=0' 'QPM_PDL=1' 'QPM_WOLF=planner,QPM_PLAN_FORK=trial,QPM_PLAN_CTAS=296'
 Each argument is a comma-separated env assignment list applied before the engine is created
+(QPM_SWEEP_SHAPE="NP,D" in the environment changes the shape from C2)
 (the QPM_* knobs are read at engine / problem creation).  Every setting times the same
 generations (warm-up 50, then 3 x 300), reported as the median us per generation.
 """
@@ -29,8 +30,9 @@ def main():
         for kv in filter(None, cfg.split(",")):
             k, v = kv.split("=")
             os.environ[k] = v
-        obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, 10_000)
-        eng = q.Engine(obj, "hybrid", pop_size=1024, generations=1000, seed=0, de=q.DEParams(), gwo=q.GWOParams(),
+        NPs, Ds = (int(x) for x in os.environ.get("QPM_SWEEP_SHAPE", "1024,10000").split(","))
+        obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, Ds)
+        eng = q.Engine(obj, "hybrid", pop_size=NPs, generations=1000, seed=0, de=q.DEParams(), gwo=q.GWOParams(),
                        sch=q.Schedules())
         eng.init()
         eng.step(50)
