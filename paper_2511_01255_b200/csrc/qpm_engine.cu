@@ -737,35 +737,39 @@ __device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const Tria
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
 }
 
-// Short rows (a column shard of a multi-GPU run; Dp <= kDeRowsMaxDp): one
-// warp per row walks all of its genes, eight rows per CTA.  Each warp
-// resolves its own row (lane 0, broadcast through shared memory) with no CTA
-// barrier, so a row's setup latency hides under the other warps' work instead
-// of being paid once per 1-2 k-gene CTA.
+// Warp items (short rows -- a column shard of a multi-GPU run, Dp <=
+// kDeRowsMaxDp -- or QPM_DE_ROWS): each warp walks the genes [ch k, ch (k+1))
+// of one row (ch = whole row for short rows), eight items per CTA.  Each
+// warp resolves its own row (lane 0, broadcast through shared memory) with no
+// CTA barrier, so a row's setup latency hides under the other warps' work.
 constexpr int kDeRowsMaxDp = 4096;
 template <int K>
-__global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_rows(RunConsts c, TrialArgs a) {
+__global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_rows(RunConsts c, TrialArgs a, int ch) {
     QTRACE(0);
     pdl_wait();
     QTRACE_STARTED();
     constexpr int kWarps = kRowThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t i = a.row_lo + (int64_t)blockIdx.x * kWarps + warp;
-    if (i >= a.row_lo + a.n_rows) return;  // warp-uniform
+    const int nch = (int)((c.Dp + ch - 1) / ch);
+    const int64_t item = (int64_t)blockIdx.x * kWarps + warp;
+    if (item >= a.n_rows * nch) return;  // warp-uniform
+    const int64_t i = a.row_lo + item / nch;
+    const int j0 = (int)(item % nch) * ch, j1 = min(j0 + ch, (int)c.Dp);
     __shared__ TrialRow s_rows[kWarps];
     if (lane == 0) trial_row_setup(c, a, a.st->g, i, s_rows[warp]);
     __syncwarp();
     const TrialRow &r = s_rows[warp];
-    constexpr int kB = 64 * kDeSteps;  // genes per warp batch
-    const int nfull = (int)c.D / kB, ntot = (int)((c.Dp + kB - 1) / kB);
+    constexpr int kB = 64 * kDeSteps;  // genes per warp batch (ch is a multiple)
+    const int jf = max(j0, min(j1, (int)c.D / kB * kB));  // batches below jf lie inside D
+    const int nfull = (jf - j0) / kB, ntail = (j1 - jf + kB - 1) / kB;
     if (r.bin) {
-        de_trial_chunk<true, true, K, 64>(c, a, r, 0, nfull);
-        de_trial_chunk<true, false, K, 64>(c, a, r, nfull * kB, ntot - nfull);
+        de_trial_chunk<true, true, K, 64>(c, a, r, j0, nfull);
+        de_trial_chunk<true, false, K, 64>(c, a, r, jf, ntail);
     } else {
-        de_trial_chunk<false, true, K, 64>(c, a, r, 0, nfull);
-        de_trial_chunk<false, false, K, 64>(c, a, r, nfull * kB, ntot - nfull);
+        de_trial_chunk<false, true, K, 64>(c, a, r, j0, nfull);
+        de_trial_chunk<false, false, K, 64>(c, a, r, jf, ntail);
     }
-    if (lane == 0) a.slot_bin[r.out_slot] = 0;
+    if (lane == 0 && j0 == 0) a.slot_bin[r.out_slot] = 0;
 }
 
 // one CTA per (row, kDeChunk genes).  K = leader count when the CTA also
@@ -1436,7 +1440,8 @@ struct Engine {
     bool wolf_side = false;         // this generation's planes on the side stream during the DE fitness (QPM_WOLF=side)
     cudaEvent_t ev_wfork = nullptr, ev_wjoin = nullptr;
     int topk_threads = kCtaThreads;   // k_select_topk block (QPM_TOPK_THREADS)
-    int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-per-row trial kernel up to this row length (QPM_DE_ROWS)
+    int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
+    int de_item = 1024;                      // genes per warp item on longer rows (QPM_DE_ITEM, multiple of 128)
     int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
     int64_t g_done = 0;
@@ -1738,11 +1743,13 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         const unsigned items = (unsigned)(NP * de_chunks);
         const bool wolf_side = hybrid && e->wolf_side;
         const bool rows_mode = c.Dp <= e->de_rows_max_dp && !e->wolf_mixed;
-        const unsigned row_ctas = (unsigned)((NP + kRowThreads / 32 - 1) / (kRowThreads / 32));
+        const int ch = c.Dp <= kDeRowsMaxDp ? (int)c.Dp : e->de_item;  // genes per warp item
+        const int64_t n_items = NP * ((c.Dp + ch - 1) / ch);
+        const unsigned row_ctas = (unsigned)((n_items + kRowThreads / 32 - 1) / (kRowThreads / 32));
         if (rows_mode) {
             const bool k0 = !hybrid || e->wolf_in_planner || wolf_side;
             QPM_CUDA_TRY(launch_k(false, k0 ? k_de_trial_rows<0> : (c.k == 4 ? k_de_trial_rows<4> : k_de_trial_rows<3>),
-                                  dim3(row_ctas), dim3(kRowThreads), 0, s, c, all));
+                                  dim3(row_ctas), dim3(kRowThreads), 0, s, c, all, ch));
         } else if (!hybrid || e->wolf_in_planner || wolf_side)
             QPM_CUDA_TRY(launch_k(false, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, all));
         else if (e->wolf_mixed)
@@ -1966,6 +1973,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (e->wolf_in_planner) e->plan_after_trial = true;
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
         if (const char *v = getenv("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
+        if (const char *v = getenv("QPM_DE_ITEM")) e->de_item = std::max(128, atoi(v) / 128 * 128);
         auto cta_knob = [](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
             if (const char *v = getenv(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
         };
