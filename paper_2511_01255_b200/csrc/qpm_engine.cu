@@ -1147,17 +1147,30 @@ __device__ double block_pairwise(const double *v, const RunConsts &c, const Tree
 // ---------------------------------------------------------------- select + top-k
 // de_select over all individuals (strict >, ties keep the target), then
 // rank_leaders (optimizer.py:437-444).  One CTA.
+// Large populations use several CTAs (kTopkMaxCtas at most): each selects a
+// contiguous slice and publishes its top-k indices; the last CTA to finish
+// (arrival counter, reset by it for the next launch) merges the lists by
+// argmax rounds over the lists' heads, values re-read from fit.  (-value,
+// index) is a strict total order, so the leaders are the same for any split.
+constexpr int kTopkMaxCtas = 32;
+struct TopkScratch {
+    int32_t *idx;   // [kTopkMaxCtas][kTopSlots]
+    unsigned *cnt;  // arrival counter, zero between launches
+};
+
 __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, EngineState *__restrict__ st,
                                                              const double *cand,
                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
-                                                             int32_t *__restrict__ spare_of) {
+                                                             int32_t *__restrict__ spare_of, TopkScratch ts) {
     QTRACE(3);
     pdl_wait();
     QTRACE_STARTED();
     Cand L[kTopSlots];
 #pragma unroll
     for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
-    for (int64_t i = threadIdx.x; i < c.NP; i += blockDim.x) {
+    const int64_t per = (c.NP + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * per, hi = min(c.NP, lo + per);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         // the slot ids are loaded with the fitness values (one L2 round trip,
         // not two) and written back only on acceptance
         const double f = cand[i];
@@ -1171,7 +1184,32 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, Engine
         }
         topk_insert(L, Cand{v, (int32_t)i});  // the selected value, straight from registers
     }
-    block_topk_lists(L, c.k, st->leaders);
+    if (gridDim.x == 1) {
+        block_topk_lists(L, c.k, st->leaders);
+        return;
+    }
+    block_topk_lists(L, c.k, ts.idx + blockIdx.x * kTopSlots);
+    __shared__ unsigned s_last;
+    __threadfence();  // this CTA's selection writes and list, before its arrival
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ts.cnt, 1u) + 1u == gridDim.x;
+    __syncthreads();
+    if (!s_last || threadIdx.x >= 32) return;
+    __threadfence();
+    const int lane = threadIdx.x;
+#pragma unroll
+    for (int t = 0; t < kTopSlots; ++t) {
+        const int32_t id = lane < (int)gridDim.x && t < c.k ? __ldcg(ts.idx + lane * kTopSlots + t) : -1;
+        L[t] = Cand{id >= 0 ? __ldcg(fit + id) : 0.0, id};
+    }
+    Cand R[kTopSlots];
+    topk_warp_rounds(L, c.k, R);
+    if (lane == 0) {
+#pragma unroll
+        for (int t = 0; t < kTopSlots; ++t)
+            if (t < c.k) st->leaders[t] = R[t].i;
+        *ts.cnt = 0u;
+    }
 }
 
 __global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, EngineState *__restrict__ st,
@@ -1440,6 +1478,9 @@ struct Engine {
     bool wolf_side = false;         // this generation's planes on the side stream during the DE fitness (QPM_WOLF=side)
     cudaEvent_t ev_wfork = nullptr, ev_wjoin = nullptr;
     int topk_threads = kCtaThreads;   // k_select_topk block (QPM_TOPK_THREADS)
+    int topk_ctas = 1;                 // k_select_topk CTAs (NP / 2048, at most kTopkMaxCtas; QPM_TOPK_CTAS)
+    int32_t *topk_idx = nullptr;       // [kTopkMaxCtas][kTopSlots] per-CTA lists
+    unsigned *topk_cnt = nullptr;      // arrival counter
     int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
     int de_item = 1024;                      // genes per warp item on longer rows (QPM_DE_ITEM, multiple of 128)
     int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)
@@ -1785,8 +1826,9 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             return QPM_OK;
         }
         mark("select_topk");
-        QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3(1), dim3(e->topk_threads), 0, s, c, e->st,
-                              (const double *)e->cand, e->fit, e->slot_of, e->spare_of));
+        QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3((unsigned)e->topk_ctas), dim3(e->topk_threads), 0, s, c,
+                              e->st, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
+                              TopkScratch{e->topk_idx, e->topk_cnt}));
         if (e->wolf_side) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
         QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
@@ -1973,6 +2015,8 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (e->wolf_in_planner) e->plan_after_trial = true;
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
         if (const char *v = getenv("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
+        e->topk_ctas = (int)std::min<int64_t>(kTopkMaxCtas, std::max<int64_t>(1, c.NP / 2048));
+        if (const char *v = getenv("QPM_TOPK_CTAS")) e->topk_ctas = std::min(kTopkMaxCtas, std::max(1, atoi(v)));
         if (const char *v = getenv("QPM_DE_ITEM")) e->de_item = std::max(128, atoi(v) / 128 * 128);
         auto cta_knob = [](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
             if (const char *v = getenv(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
@@ -2029,6 +2073,8 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->st, 1);
     QPM_ALLOC(e->best_genome, c.Dp);
     QPM_ALLOC(e->best_bits, c.W);
+    QPM_ALLOC(e->topk_idx, (size_t)kTopkMaxCtas * kTopSlots);
+    QPM_ALLOC(e->topk_cnt, 1);
     if (e->world > 1) {
         QPM_ALLOC(e->gpart, (size_t)e->world * gpart_slot(e));
         QPM_ALLOC(e->ggains, (size_t)NP * gp.n_wl);
@@ -2089,6 +2135,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     if (err == cudaSuccess) err = cudaMemsetAsync(e->genome, 0, sizeof(double) * 2 * NP * c.Dp, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->bits, 0, sizeof(uint32_t) * 2 * NP * c.W, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->slot_bin, 0, 2 * NP, e->stream);
+    if (err == cudaSuccess) err = cudaMemsetAsync(e->topk_cnt, 0, sizeof(unsigned), e->stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
     if (err != cudaSuccess) {
         set_error("engine upload: %s", cudaGetErrorString(err));

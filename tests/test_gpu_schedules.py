@@ -10,7 +10,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL", "QPM_TOPK_THREADS", "QPM_STATS_THREADS")
+KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL", "QPM_TOPK_THREADS", "QPM_STATS_THREADS",
+         "QPM_TOPK_CTAS", "QPM_DE_ROWS", "QPM_DE_ITEM")
 
 
 @pytest.fixture(scope="module")
@@ -41,7 +42,10 @@ VARIANTS = [
     {"QPM_PDL": "0"},
     {"QPM_WOLF": "mixed"},
     {"QPM_WOLF": "side"},
+    {"QPM_TOPK_CTAS": "3"},
+    {"QPM_TOPK_CTAS": "32"},
     {"QPM_WOLF": "side", "QPM_PDL": "0", "QPM_PLAN_CTAS": "7"},
+    {"QPM_DE_ROWS": "100000", "QPM_DE_ITEM": "384"},
     {"QPM_WOLF": "planner"},
     {"QPM_WOLF": "planner", "QPM_PDL": "0"},
     {"QPM_WOLF": "planner", "QPM_PLAN_FORK": "trial"},
@@ -96,3 +100,11 @@ def test_c2_shape_runs_match_default(q, monkeypatch, env):
     for _ in range(2):
         got = _trace(q, monkeypatch, env, D=10_000, NP=1024, G=600)[0]
         assert np.array_equal(got, base)
+
+
+def test_large_population_multi_cta_selection(q, monkeypatch):
+    """NP = 8192 selects the leaders with several CTAs (last-CTA merge) and
+    short rows take the warp-per-row trial: same trace as one CTA / chunked CTAs."""
+    want = _trace(q, monkeypatch, {"QPM_TOPK_CTAS": "1", "QPM_DE_ROWS": "0"}, D=1300, NP=8192, G=6)[0]
+    got = _trace(q, monkeypatch, {}, D=1300, NP=8192, G=6)[0]
+    assert np.array_equal(got, want)
