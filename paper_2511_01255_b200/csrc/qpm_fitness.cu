@@ -892,8 +892,15 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
     p.nchunks = p.W / 4;
     // segment length (in 128-domain chunks) depends only on D and the
     // wavelength count, never on the batch, so fitness stays a pure function
-    // of the row bits; longer segments when wavelengths supply parallelism
-    p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, n_wl > 1 ? 4 * std::min(n_wl, 8) : 4));
+    // of the row bits; longer segments when wavelengths supply parallelism.
+    // One wavelength: 4 chunks, or 2 when that leaves fewer than 32 segments
+    // (C2, D = 10^4: 40 segments, which split evenly over 2, 4 and 8 GPUs;
+    // same single-GPU speed, measured)
+    if (n_wl > 1)
+        p.seg_chunks = 4 * std::min(n_wl, 8);
+    else
+        p.seg_chunks = (p.nchunks + 3) / 4 < 32 ? 2 : 4;
+    p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, p.seg_chunks));
     if (const char *env = getenv("QPM_SEG_CHUNKS")) {  // tuning override (changes fitness rounding only)
         const int v = atoi(env);
         if (v >= 1) p.seg_chunks = (int)std::min<int64_t>(p.nchunks, v);

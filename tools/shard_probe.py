@@ -38,7 +38,8 @@ def main():
     sh.step(args.warm)
     engines = sh.engines
     phases = engines[0].phases
-    per_phase = np.zeros(phases)
+    W = len(engines)
+    per = np.zeros((W, phases))
     for _ in range(args.gens):
         for ph in range(phases):
             if ph > 0:
@@ -47,18 +48,18 @@ def main():
                     for src in engines:
                         if src is not dst:
                             dst.exchange_from(src, ph)
-            torch.cuda.synchronize()
-            s = engines[0].stream
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            engines[0].run_phase(ph)
-            e1.record(s)
-            torch.cuda.synchronize()
-            per_phase[ph] += e0.elapsed_time(e1) * 1e3
-            for e in engines[1:]:
+            for r, e in enumerate(engines):  # each rank's phase alone on the GPU
+                torch.cuda.synchronize()
+                s = e.stream
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
                 e.run_phase(ph)
+                e1.record(s)
+                torch.cuda.synchronize()
+                per[r, ph] += e0.elapsed_time(e1) * 1e3
     torch.cuda.synchronize()
-    per_phase /= args.gens
+    per /= args.gens
+    per_phase = per.max(axis=0)  # the slowest rank of each phase sets the pace
     single = q.Engine(obj, "hybrid", **kw)
     single.init()
     single.step(args.warm)
@@ -69,9 +70,11 @@ def main():
     e1.record(single.stream)
     torch.cuda.synchronize()
     one = e0.elapsed_time(e1) * 1e3 / args.gens
-    print(json.dumps({"world": args.world, "NP": NP, "D": args.d, "rank0_us_per_phase": per_phase.round(2).tolist(),
-                      "rank0_us_per_gen": float(per_phase.sum()), "single_gpu_us_per_gen_same_NP": one,
-                      "note": "eager phases (no graph, no PDL), exchanges untimed"}))
+    print(json.dumps({"world": args.world, "NP": NP, "D": args.d, "seg_chunks": os.environ.get("QPM_SEG_CHUNKS", "default"),
+                      "columns": [e.Dl for e in engines], "max_rank_us_per_phase": per_phase.round(2).tolist(),
+                      "max_rank_us_per_gen": float(per_phase.sum()),
+                      "rank_us_per_gen": per.sum(axis=1).round(1).tolist(), "single_gpu_us_per_gen_same_NP": one,
+                      "note": "eager phases (no graph, no PDL), exchanges untimed; per phase the slowest rank"}))
 
 
 if __name__ == "__main__":
