@@ -566,6 +566,34 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
 
 constexpr int kDeSteps = 2;  // 64-gene warp steps per k_de_trial batch (registers)
 
+// L2 policy of the trial's genome traffic (QPM_L2_HINTS): the current
+// population (NP rows, 82 MB at C2) is read ~4 times per generation as
+// donors / targets and fits the 126 MB L2; the trial rows written to the
+// spare slots are not read again this generation.  Donor loads ask L2 to
+// keep their lines (evict_last), trial stores to drop theirs first
+// (st.global.cs), so the written stream does not push the donors out.
+#ifndef QPM_L2_HINTS
+#define QPM_L2_HINTS 1
+#endif
+__device__ __forceinline__ double ld_keep(const double *p) {
+#if QPM_L2_HINTS
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    return *p;
+#endif
+}
+__device__ __forceinline__ void st_stream(double *p, double v) {
+#if QPM_L2_HINTS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 // One warp's share of a row: nb batches of kDeSteps 64-gene steps, step st of
 // batch bt at genes j0 + (bt kDeSteps + st) SPAN (SPAN = 512: the eight warps of
 // a CTA interleave over a chunk; SPAN = 64: one warp walks a whole row).
@@ -645,11 +673,11 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                     p2[st][q] = x2.f ? x2.f[j] : (((x2.b[w] >> lane) & 1u) ? -1.0 : 1.0);
                     p3[st][q] = x3.f ? x3.f[j] : (((x3.b[w] >> lane) & 1u) ? -1.0 : 1.0);
                 } else if ((mb[st] >> q) & 1u) {
-                    p1[st][q] = x1.f[j];
-                    p2[st][q] = x2.f[j];
-                    p3[st][q] = x3.f[j];
+                    p1[st][q] = ld_keep(x1.f + j);
+                    p2[st][q] = ld_keep(x2.f + j);
+                    p3[st][q] = ld_keep(x3.f + j);
                 } else {
-                    y[st][q] = xi.f[j];
+                    y[st][q] = ld_keep(xi.f + j);
                 }
             }
         }
@@ -664,7 +692,7 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
                 neg[q] = false;
                 if (FULL || j < D) {
                     const double v = ((mb[st] >> q) & 1u) ? p1[st][q] + F * (p2[st][q] - p3[st][q]) : y[st][q];
-                    out[j] = v;
+                    st_stream(out + j, v);
                     neg[q] = !(v >= 0.0);
                 } else if (j < (int)c.Dp) {
                     out[j] = 0.0;
