@@ -11,7 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL", "QPM_TOPK_THREADS", "QPM_STATS_THREADS",
-         "QPM_TOPK_CTAS", "QPM_DE_ROWS", "QPM_DE_ITEM")
+         "QPM_TOPK_CTAS", "QPM_DE_ROWS", "QPM_DE_ITEM", "QPM_GRAPH_GENS")
 
 
 @pytest.fixture(scope="module")
@@ -43,6 +43,8 @@ VARIANTS = [
     {"QPM_WOLF": "mixed"},
     {"QPM_WOLF": "side"},
     {"QPM_TOPK_CTAS": "3"},
+    {"QPM_GRAPH_GENS": "1"},
+    {"QPM_GRAPH_GENS": "7", "QPM_PDL": "0"},
     {"QPM_TOPK_CTAS": "32"},
     {"QPM_WOLF": "side", "QPM_PDL": "0", "QPM_PLAN_CTAS": "7"},
     {"QPM_DE_ROWS": "100000", "QPM_DE_ITEM": "384"},
