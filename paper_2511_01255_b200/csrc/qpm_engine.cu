@@ -587,7 +587,7 @@ __device__ __forceinline__ double ld_keep(const double *p) {
 #endif
 }
 __device__ __forceinline__ void st_stream(double *p, double v) {
-#if QPM_L2_HINTS
+#if QPM_L2_HINTS && !defined(QPM_NO_STCS)
     __stcs(p, v);
 #else
     *p = v;

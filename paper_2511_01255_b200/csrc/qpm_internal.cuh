@@ -44,7 +44,10 @@ void set_error(const char *fmt, ...);
         }                                                      \
     } while (0)
 
-constexpr int kFitThreads = 128;      // rows per fast-fitness CTA (one lane per row)
+#ifndef QPM_FIT_THREADS
+#define QPM_FIT_THREADS 128
+#endif
+constexpr int kFitThreads = QPM_FIT_THREADS;  // rows per fast-fitness CTA (one lane per row)
 constexpr int kQuadsPerChunk = 32;    // 128 domains = 4 u32 words per chunk
 constexpr int kQuadEntries = 24;      // B[8], E[8], I[8] complex entries per quad (by relative signs)
 constexpr int kPartDoubles = 6;       // acc, P, T (complex) per (row, wavelength, segment)
