@@ -1,36 +1,45 @@
 // qpm_engine.cu -- device-resident HWSDA generation loop (run_hybrid /
-// run_de / run_gwo, optimizer.py:400-592) for one B200.
+// run_de / run_gwo, optimizer.py:400-592) on one B200, or on one column
+// shard of a multi-GPU run.
 //
-// HBM layout (one engine):
+// HBM layout (one engine; D, W, Dp are this engine's genes):
 //   genome  f64 [2 NP][Dp]   slot pool; individual i lives in slot_of[i], its
 //                            trial / candidate goes to spare_of[i] and
 //                            acceptance swaps the two ids (no row copies)
 //   bits    u32 [2 NP][W]    sign bits of each slot (bit 1 <=> gene < 0)
+//   cbits   u32 [NP][W]      the generation's candidate sign rows, dense by
+//                            individual (what the fitness scans)
 //   slot_bin u8 [2 NP]       1 = the slot holds a wolf candidate whose genome is
 //                            exactly +/-1 (optimizer.py:376): its f64 row is
 //                            never written, readers expand the bits instead
-//   planes  u32 [NP][W][8]   per-gene wolf draw outcomes as bit-planes (k_de_trial)
-//   fit, cand f64 [NP]; keys u64 [NP]; picks int4 [NP] (r1, r2, r3, m)
+//   planes  u32 [2][NP][W][8] per-gene wolf draw outcomes as bit-planes
+//   fit, cand f64 [NP]; keys u64 [2][NP]; picks int4 [2][NP] (r1, r2, r3, m)
 //   sched   f64 [G+1][8]     per-generation scalars, host-computed
 //   trace   f64 [G+1][5]     (g, best, mean, F|a, pop_std)
 //   state   EngineState      g, F, window, leaders, best-ever bookkeeping
+//   gpart   f64 [W][n_wl][NP][S_slot][6]  all-gathered fitness segment
+//                            partials (multi-GPU)
 // Dp = W * 32 with W a multiple of 4, so rows start on 512-byte boundaries.
 //
-// One hybrid generation is 8 launches, all reading g and F from device
-// memory so a single CUDA graph replays every generation:
+// One hybrid generation (ten per CUDA graph, everything reading g and F from
+// device memory):
 //   k_plan_rows     (side stream, one generation ahead) keys + DE indices
-//   k_de_trial      crossover mask, trial genome + bits, AND the wolf
-//                   phase's three random draws per gene folded into 8
-//                   bit-planes.  The kernel is HBM-bound; the splitmix64
-//                   integer work rides in its shadow.
-//   fitness x2      segmented quad-table scan + warp-parallel stitch
-//   k_select_topk   greedy selection + top-k leaders (one CTA)
-//   k_gwo_apply     leader vote per gene from the codes -> candidate bits
-//   fitness x2
+//   k_de_trial      crossover mask, trial genome + bits, and the first two
+//                   wolf draws of every gene as bit-planes (integer-issue
+//                   bound, HBM traffic in its shadow); k_de_trial_rows for
+//                   short rows (column shards)
+//   fitness         segmented quad-table scan + warp-parallel stitch
+//   k_select_topk   greedy selection + top-k leaders
+//   k_gwo_apply     leader vote per gene from the planes (+ the third draw
+//                   where the outcome depends on it) -> candidate bits
+//   fitness
 //   k_select_stats  wolf selection + np.max/mean/std replica + F update
+// Multi-GPU (column shards): the fitness scans write segment partials, which
+// are all-gathered (NCCL, in the graph) and stitched on every rank.
 // Decisions reproduce the reference bit-for-bit given the same fitness:
 //   - stream positions follow SURVEY.md Appendix A (de_mutate rejection
-//     draws 0..m-1, j_rand at m, mask m+1..m+D, wolf block from m+1+D);
+//     draws 0..m-1, j_rand at m, mask m+1..m+D, wolf block from m+1+D), with
+//     the global gene index on a shard;
 //   - DE arithmetic x_r1 + F (x_r2 - x_r3) is unfused (-fmad=false);
 //   - u < p comparisons are exact integer compares on the 53-bit mantissa;
 //   - np.mean / np.std use a replica of numpy's pairwise summation.
@@ -511,7 +520,7 @@ struct TrialArgs {
     const int4 *picks;       // [2][NP]
     const uint64_t *keys;    // [2][NP]
     const int32_t *jrand;    // [2][NP]
-    uint32_t *planes;        // [2][NP][W][8] wolf planes (own rows)
+    uint32_t *planes;        // [2][NP][W][8] wolf planes
     const int32_t *slot_of, *spare_of;
     uint8_t *slot_bin;
     double *genome;
@@ -521,7 +530,7 @@ struct TrialArgs {
 };
 
 // The trial of row i over genes [jc, jc + kDeChunk) with the crossover mask
-// drawn inline (one splitmix64 per gene).  For K > 0 (run_hybrid, own rows)
+// drawn inline (one splitmix64 per gene).  For K > 0 (run_hybrid)
 // the same pass draws the row's wolf planes for this generation (three
 // draws per gene): the trial is HBM-bound (~30 B per gene) and the integer
 // work of the draws runs while the genome loads are in flight.
@@ -801,8 +810,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_rows(RunC
 }
 
 // one CTA per (row, kDeChunk genes).  K = leader count when the CTA also
-// draws the wolf planes (run_hybrid own rows), 0 otherwise; filter mode
-// recomputes the trials of foreign rows that won (multi-GPU)
+// draws the wolf planes (run_hybrid), 0 otherwise
 template <int K>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts c, TrialArgs a) {
     QTRACE(0);
