@@ -10,7 +10,7 @@ timeout 600 python bench.py > $E/bench.jsonl 2> $E/bench.err; echo RC=$? >> $E/b
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $E/bench_reference.jsonl 2>&1
 for a in "c1 hybrid" "c2 hybrid" "c3 hybrid" "c4 hybrid" "c4 de" "c4 gwo" "c5 hybrid"; do
   set -- $a
-  timeout 300 python tools/run_config.py --config $1 --algo $2 --gens 20 --warm 5 --profile 0 >> $E/configs.jsonl 2>> $E/configs.err
+  timeout 300 python tools/run_config.py --config $1 --algo $2 --gens 20 --warm 20 --profile 0 >> $E/configs.jsonl 2>> $E/configs.err
 done
 timeout 300 python tools/measure_extras.py > $E/extras.log 2>&1
 [ -f build/ab/libqpm_trace.so ] && timeout 300 python tools/timeline.py > $E/timeline.log 2>&1

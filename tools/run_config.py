@@ -23,7 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--gens", type=int, default=20)
-    ap.add_argument("--warm", type=int, default=5)
+    ap.add_argument("--warm", type=int, default=20)  # >= QPM_GRAPH_GENS: the multi-generation graph is built before timing
     ap.add_argument("--algo", default="hybrid")
     ap.add_argument("--profile", type=int, default=3)
     args = ap.parse_args()
