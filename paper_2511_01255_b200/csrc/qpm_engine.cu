@@ -145,6 +145,17 @@ struct SumTree {
     const int32_t *lvl;
     double *val;  // [2 n_leaf - 1]
 };
+// The same tree by value (leaf_off, kid, lvl concatenated) when it fits: a
+// kernel parameter sits in the constant bank at launch, so staging it costs no
+// global round trip on the critical path (NP <= 8192 -> at most 64 leaves)
+#ifndef QPM_TREE_INLINE
+#define QPM_TREE_INLINE 1
+#endif
+constexpr int kTreeInline = 256;
+struct SumTreeInline {
+    int32_t n;  // 0: use the global copy
+    int32_t v[kTreeInline];
+};
 
 // ---------------------------------------------------------------- helpers
 // draw at counter position p1 = pos + 1 (< 2^32): mix(key + p1 * GOLD).  The
@@ -1268,7 +1279,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
                                                               int32_t *__restrict__ spare_of,
                                                               uint8_t *__restrict__ slot_bin,
                                                               double *__restrict__ scratch, SumTree tr,
-                                                              double *__restrict__ trace) {
+                                                              double *__restrict__ trace, SumTreeInline tri) {
     QTRACE(5);
     const int64_t n = c.NP;
     // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
@@ -1283,9 +1294,22 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     ts.kid = ts.leaf_off + c.n_leaf + 1;
     ts.lvl = ts.kid + 2 * c.n_leaf;
     // the tree is the engine's constant: staged before waiting on the predecessor
-    for (int t = threadIdx.x; t <= c.n_leaf; t += blockDim.x) ts.leaf_off[t] = tr.leaf_off[t];
-    for (int t = threadIdx.x; t < 2 * (c.n_leaf - 1); t += blockDim.x) ts.kid[t] = tr.kid[t];
-    for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
+    if (tri.n) {
+        const int nl = c.n_leaf + 1, nk = 2 * (c.n_leaf - 1);
+        for (int t = threadIdx.x; t < tri.n; t += blockDim.x) {
+            const int32_t v = tri.v[t];
+            if (t < nl)
+                ts.leaf_off[t] = v;
+            else if (t < nl + nk)
+                ts.kid[t - nl] = v;
+            else
+                ts.lvl[t - nl - nk] = v;
+        }
+    } else {
+        for (int t = threadIdx.x; t <= c.n_leaf; t += blockDim.x) ts.leaf_off[t] = tr.leaf_off[t];
+        for (int t = threadIdx.x; t < 2 * (c.n_leaf - 1); t += blockDim.x) ts.kid[t] = tr.kid[t];
+        for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
+    }
     pdl_wait();
     QTRACE_STARTED();
     QSTAMP(0);
@@ -1498,6 +1522,7 @@ struct Engine {
     int32_t *tree_i = nullptr;
     double *tree_v = nullptr;
     SumTree tree{};
+    SumTreeInline tree_inline{};
     uint64_t *keys = nullptr;
     int4 *picks = nullptr;
     double *sched = nullptr, *trace = nullptr;
@@ -1634,7 +1659,7 @@ static size_t stats_smem_bytes(const RunConsts &c) {
 static int launch_select_stats(Engine *e, int mode, cudaStream_t s) {
     QPM_CUDA_TRY(launch_k(e->pdl, k_select_stats, dim3(1), dim3(e->stats_threads), stats_smem_bytes(e->c), s, e->c, mode,
                           e->st, (const double *)e->sched, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
-                          e->slot_bin, e->scratch, e->tree, e->trace));
+                          e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline));
     return QPM_OK;
 }
 
@@ -2140,6 +2165,17 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     e->tree.kid = e->tree_i + ht.leaf_off.size();
     e->tree.lvl = e->tree_i + ht.leaf_off.size() + ht.kid.size();
     e->tree.val = e->tree_v;
+    {
+        const size_t nt = ht.leaf_off.size() + ht.kid.size() + ht.lvl.size();
+        e->tree_inline.n = 0;
+        if (QPM_TREE_INLINE && nt <= (size_t)kTreeInline && ht.kid.size() == 2 * (ht.leaf_off.size() - 2)) {
+            size_t k = 0;
+            for (int32_t v : ht.leaf_off) e->tree_inline.v[k++] = v;
+            for (int32_t v : ht.kid) e->tree_inline.v[k++] = v;
+            for (int32_t v : ht.lvl) e->tree_inline.v[k++] = v;
+            e->tree_inline.n = (int32_t)nt;
+        }
+    }
     // host-side constants of the state: p_plus thresholds (optimizer.py:362-365)
     EngineState hs;
     memset(&hs, 0, sizeof(hs));
