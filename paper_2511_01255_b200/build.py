@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqpm_b200.so")
 SOURCES = ["qpm_fitness.cu", "qpm_engine.cu"]
-HEADERS = ["qpm_common.cuh", "qpm_internal.cuh", os.path.join("..", "..", "include", "qpm_b200.h")]
+HEADERS = ["qpm_common.cuh", "qpm_internal.cuh", "qpm_finish.cuh", os.path.join("..", "..", "include", "qpm_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-shared",
               "-cudart", "static", "-Xptxas", "-v"]

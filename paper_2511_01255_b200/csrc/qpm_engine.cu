@@ -52,6 +52,7 @@
 
 #include "qpm_common.cuh"
 #include "qpm_internal.cuh"
+#include "qpm_finish.cuh"
 
 namespace qpm {
 
@@ -1122,7 +1123,7 @@ __device__ void block_topk_k(const double *vals, int64_t n, int k, int32_t *out)
     Cand L[kTopSlots];
 #pragma unroll
     for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) topk_insert(L, Cand{vals[i], (int32_t)i});
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) topk_insert(L, Cand{__ldcg(vals + i), (int32_t)i});
     block_topk_lists(L, k, out);
 }
 
@@ -1272,15 +1273,12 @@ __global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, Engin
 // np.mean / np.std, the convergence window and adaptive_f_update
 // (optimizer.py:277-299, 469-485), or run_gwo's a-row and best-ever tracking
 // (optimizer.py:586-589), and the trace row.  One CTA.
-__global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int mode, EngineState *__restrict__ st,
-                                                              const double *__restrict__ sched,
-                                                              const double *cand,
-                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
-                                                              int32_t *__restrict__ spare_of,
-                                                              uint8_t *__restrict__ slot_bin,
-                                                              double *__restrict__ scratch, SumTree tr,
-                                                              double *__restrict__ trace, SumTreeInline tri) {
-    QTRACE(5);
+__device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, EngineState *__restrict__ st,
+                                                  const double *__restrict__ sched, const double *cand,
+                                                  double *__restrict__ fit, int32_t *__restrict__ slot_of,
+                                                  int32_t *__restrict__ spare_of, uint8_t *__restrict__ slot_bin,
+                                                  double *__restrict__ scratch, const SumTree &tr,
+                                                  double *__restrict__ trace, const SumTreeInline &tri, bool wait) {
     const int64_t n = c.NP;
     // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
     // then the pairwise-sum tree (values, leaf offsets, children, levels)
@@ -1310,9 +1308,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
         for (int t = threadIdx.x; t < 2 * (c.n_leaf - 1); t += blockDim.x) ts.kid[t] = tr.kid[t];
         for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
     }
-    pdl_wait();
-    QTRACE_STARTED();
-    QSTAMP(0);
+    if (wait) pdl_wait();
     __shared__ EngineState s_state;
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(st);
@@ -1326,7 +1322,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     double mx = -INFINITY, mn = INFINITY;
     int64_t amx = n;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        double v = fit[i];
+        double v = __ldcg(fit + i);  // (coherent: a fused caller's other CTAs wrote it)
         if (mode != 3) {
             bool is_leader = false;
 #pragma unroll
@@ -1366,9 +1362,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
         s_mn[threadIdx.x >> 5] = mn;
         s_am[threadIdx.x >> 5] = amx;
     }
-    QSTAMP(1);
     __syncthreads();  // also publishes fv (and, without on-chip staging, fit)
-    QSTAMP(2);
     mx = lane < nw ? s_mx[lane] : -INFINITY;
     mn = lane < nw ? s_mn[lane] : INFINITY;
     amx = lane < nw ? s_am[lane] : n;
@@ -1385,16 +1379,13 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
     mx = __shfl_sync(0xffffffffu, mx, 0);
     mn = __shfl_sync(0xffffffffu, mn, 0);
     amx = __shfl_sync(0xffffffffu, amx, 0);
-    QSTAMP(3);
     const double mean = block_pairwise(fv, c, ts) / (double)n;
-    QSTAMP(4);
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = fv[i] - mean;
         sq[i] = d * d;
     }
     __syncthreads();
     const double var = block_pairwise(sq, c, ts) / (double)n;
-    QSTAMP(5);
     if (threadIdx.x != 0) return;
     // serial tail on the shared-memory copy of the state (fetched at entry);
     // only the fields this kernel owns are written back (g_plan belongs to
@@ -1459,8 +1450,77 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
         st->F = f;
         row[3] = f;
     }
-    QSTAMP(6);
     st->g = g + 1;
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int mode, EngineState *__restrict__ st,
+                                                              const double *__restrict__ sched,
+                                                              const double *cand,
+                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
+                                                              int32_t *__restrict__ spare_of,
+                                                              uint8_t *__restrict__ slot_bin,
+                                                              double *__restrict__ scratch, SumTree tr,
+                                                              double *__restrict__ trace, SumTreeInline tri) {
+    QTRACE(5);
+    select_stats_body(c, mode, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, true);
+}
+
+// Fused fitness finish + selection (run_hybrid): one warp per row stitches its
+// segment partials (finish_row, the k_fit_finish arithmetic), lane 0 selects
+// the row (strict >, ties keep the target; MODE 1: leaders stay), and the
+// last CTA to finish (arrival counter, reset by it) runs the whole-population
+// part: MODE 0 the top-k leaders, MODE 1 np.max/mean/std, window, F and the
+// trace row (select_stats_body with the selection already done).  Saves the
+// separate finish launch and moves the selection onto every SM.
+#ifndef QPM_FS_THREADS
+#define QPM_FS_THREADS 256
+#endif
+constexpr int kFsThreads = QPM_FS_THREADS;  // fused finish + selection CTA
+constexpr int kFsRows = kFsThreads / 32;
+template <int MODE>
+__global__ void __launch_bounds__(kFsThreads) k_finish_select(RunConsts c, FinishArgs f, EngineState *__restrict__ st,
+                                                               const double *__restrict__ sched, double *cand,
+                                                               double *__restrict__ fit, int32_t *__restrict__ slot_of,
+                                                               int32_t *__restrict__ spare_of,
+                                                               uint8_t *__restrict__ slot_bin,
+                                                               double *__restrict__ scratch, SumTree tr,
+                                                               double *__restrict__ trace, SumTreeInline tri,
+                                                               unsigned *cnt) {
+    QTRACE(MODE == 0 ? 3 : 5);
+    pdl_wait();
+    QTRACE_STARTED();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * kFsRows + warp;
+    if (r < c.NP) {  // warp-uniform
+        const double g = finish_row(f, r, lane);
+        if (lane == 0) {
+            cand[r] = g;
+            bool take = g > __ldcg(fit + r);
+            if (MODE == 1) {
+#pragma unroll
+                for (int t = 0; t < kMaxLeaders; ++t) take &= !(t < c.k && st->leaders[t] == r);
+            }
+            if (take) {
+                const int32_t a = slot_of[r], b = spare_of[r];
+                slot_of[r] = b;
+                spare_of[r] = a;
+                fit[r] = g;
+                if (MODE == 1) slot_bin[b] = 1;
+            }
+        }
+    }
+    __shared__ unsigned s_last;
+    __threadfence();  // this CTA's selections, before its arrival
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1u) + 1u == gridDim.x;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (MODE == 0)
+        block_topk_k(fit, c.NP, c.k, st->leaders);
+    else
+        select_stats_body(c, 3, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, false);
+    if (threadIdx.x == 0) *cnt = 0u;  // ready for the next launch (stream-ordered)
 }
 
 // best row -> result buffer (when flagged), expanding +/-1 slots from bits
@@ -1546,6 +1606,9 @@ struct Engine {
     cudaEvent_t ev_wfork = nullptr, ev_wjoin = nullptr;
     int topk_threads = kCtaThreads;   // k_select_topk block (QPM_TOPK_THREADS)
     int topk_ctas = 1;                 // k_select_topk CTAs (NP / 2048, at most kTopkMaxCtas; QPM_TOPK_CTAS)
+    bool fused_select = true;          // run_hybrid, NP <= 2048: fused finish + selection kernels (QPM_FUSED_SELECT)
+    unsigned *fs_cnt = nullptr;        // their arrival counters [2]
+    int S_cur = 1;                     // segments of the last one-GPU scan
     int32_t *topk_idx = nullptr;       // [kTopkMaxCtas][kTopSlots] per-CTA lists
     unsigned *topk_cnt = nullptr;      // arrival counter
     int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
@@ -1769,12 +1832,36 @@ static int enqueue_exchange(Engine *e, int phase) {
 // the candidates' fitness into out[NP]: one GPU scores them now; a column
 // shard scans its segments into its gpart slot and fit_finish scores them
 // after the exchange
+// run_hybrid on one GPU with the fused finish + selection kernels: the scans
+// only write partials (QPM_FUSED_SELECT=0 restores finish + select kernels)
+static bool fused_select(const Engine *e) { return e->c.algorithm == QPM_ALGO_HYBRID && e->fused_select; }
 static int fit_scan(Engine *e, const uint32_t *bits, const int32_t *row_index, double *out, cudaStream_t s, int *n) {
     const RunConsts &c = e->c;
+    if (!e->sharded() && fused_select(e))
+        return launch_fitness_partials(e->prob, &e->fs, bits, c.W, row_index, c.NP, e->P.fitness_mode, s, n, e->pdl,
+                                       &e->S_cur);
     if (!e->sharded())
         return launch_fitness(e->prob, &e->fs, bits, c.W, row_index, c.NP, out, e->P.fitness_mode, s, n, e->pdl);
     return launch_fitness_scan(e->lprob ? &e->lprob->p : e->prob, bits, c.W, row_index, c.NP,
                                e->gpart + e->rank * gpart_slot(e), e->S_slot, s, n, e->pdl);
+}
+static FinishArgs fused_finish_args(const Engine *e) {
+    if (e->sharded())
+        return finish_args(e->prob, e->gpart, e->prob->S, e->world, e->S_slot, e->c.NP, e->ggains);
+    return finish_args(e->prob, e->fs.part, e->S_cur, 1, e->S_cur, e->c.NP, e->fs.gains);
+}
+static int launch_finish_select(Engine *e, int mode, cudaStream_t s) {
+    const RunConsts &c = e->c;
+    const unsigned grid = (unsigned)((c.NP + kFsRows - 1) / kFsRows);
+    if (mode == 0)
+        QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<0>, dim3(grid), dim3(kFsThreads), 0, s, c, fused_finish_args(e),
+                              e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of, e->spare_of, e->slot_bin,
+                              e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt));
+    else
+        QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<1>, dim3(grid), dim3(kFsThreads), stats_smem_bytes(c), s, c,
+                              fused_finish_args(e), e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of,
+                              e->spare_of, e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt + 1));
+    return QPM_OK;
 }
 static int fit_finish(Engine *e, double *out, cudaStream_t s, int *n) {
     if (!e->sharded()) return QPM_OK;
@@ -1802,7 +1889,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     const int64_t NP = c.NP;
     const bool sharded = e->sharded();
     const int64_t de_chunks = (c.Dp + kDeChunk - 1) / kDeChunk;
-    if (phase > 0 && sharded) {
+    if (phase > 0 && sharded && !fused_select(e)) {
         mark("fitness_finish");
         if ((rc = fit_finish(e, e->cand, s, n))) return rc;
     }
@@ -1894,10 +1981,15 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
             return QPM_OK;
         }
-        mark("select_topk");
-        QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3((unsigned)e->topk_ctas), dim3(e->topk_threads), 0, s, c,
-                              e->st, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
-                              TopkScratch{e->topk_idx, e->topk_cnt}));
+        if (fused_select(e)) {
+            mark("finish_select_topk");
+            if ((rc = launch_finish_select(e, 0, s))) return rc;
+        } else {
+            mark("select_topk");
+            QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3((unsigned)e->topk_ctas), dim3(e->topk_threads), 0, s, c,
+                                  e->st, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
+                                  TopkScratch{e->topk_idx, e->topk_cnt}));
+        }
         if (e->wolf_side) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
         QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
@@ -1909,8 +2001,13 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         return fit_scan(e, e->cbits, nullptr, e->cand, s, n);
     }
     // phase 2 (hybrid)
-    mark("select_stats");
-    if ((rc = launch_select_stats(e, 1, s))) return rc;
+    if (fused_select(e)) {
+        mark("finish_select_stats");
+        if ((rc = launch_finish_select(e, 1, s))) return rc;
+    } else {
+        mark("select_stats");
+        if ((rc = launch_select_stats(e, 1, s))) return rc;
+    }
     *n += 1;
     QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
     return QPM_OK;
@@ -2089,6 +2186,11 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (const char *v = getenv("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
         e->topk_ctas = (int)std::min<int64_t>(kTopkMaxCtas, std::max<int64_t>(1, c.NP / 2048));
         if (const char *v = getenv("QPM_TOPK_CTAS")) e->topk_ctas = std::min(kTopkMaxCtas, std::max(1, atoi(v)));
+        // fused finish + selection: its last CTA runs the whole-population part
+        // alone, which pays up to ~2k rows (C2: 116.0 -> 113.8 us per
+        // generation; NP 8192: 133 -> 149 us, alternating A/B)
+        e->fused_select = c.NP <= 2048;
+        if (const char *v = getenv("QPM_FUSED_SELECT")) e->fused_select = atoi(v) != 0;
         if (const char *v = getenv("QPM_DE_ITEM")) e->de_item = std::max(128, atoi(v) / 128 * 128);
         auto cta_knob = [](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
             if (const char *v = getenv(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
@@ -2115,6 +2217,12 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
             engine_free(e);
             return QPM_ERR_CUDA;
         }
+        cudaFuncAttributes fb{};
+        cudaFuncGetAttributes(&fb, k_finish_select<1>);
+        if ((size_t)max_optin < stats_smem_bytes(c) + fb.sharedSizeBytes ||
+            cudaFuncSetAttribute(k_finish_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_optin - (int)fb.sharedSizeBytes) != cudaSuccess)
+            e->fused_select = false;  // (the statistics then run in k_select_stats)
     }
 
     const int64_t NP = c.NP;
@@ -2147,6 +2255,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->best_bits, c.W);
     QPM_ALLOC(e->topk_idx, (size_t)kTopkMaxCtas * kTopSlots);
     QPM_ALLOC(e->topk_cnt, 1);
+    QPM_ALLOC(e->fs_cnt, 2);
     if (e->world > 1) {
         QPM_ALLOC(e->gpart, (size_t)e->world * gpart_slot(e));
         QPM_ALLOC(e->ggains, (size_t)NP * gp.n_wl);
@@ -2219,6 +2328,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     if (err == cudaSuccess) err = cudaMemsetAsync(e->bits, 0, sizeof(uint32_t) * 2 * NP * c.W, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->slot_bin, 0, 2 * NP, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->topk_cnt, 0, sizeof(unsigned), e->stream);
+    if (err == cudaSuccess) err = cudaMemsetAsync(e->fs_cnt, 0, 2 * sizeof(unsigned), e->stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
     if (err != cudaSuccess) {
         set_error("engine upload: %s", cudaGetErrorString(err));

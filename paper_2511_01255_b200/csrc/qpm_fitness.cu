@@ -41,6 +41,7 @@
 
 #include "qpm_common.cuh"
 #include "qpm_internal.cuh"
+#include "qpm_finish.cuh"
 
 namespace qpm {
 
@@ -280,21 +281,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-// Segment concatenation: (a1, P1, T1) . (a2, P2, T2) = (a1 + a2 + P1 T2, P1 + P2, T1 + T2).
-struct Seg {
-    double ar, ai, pr, pi, tr, ti;
-};
-
-__device__ __forceinline__ Seg seg_cat(const Seg &x, const Seg &y) {
-    Seg z;
-    z.ar = (x.ar + y.ar) + fma(x.pr, y.tr, -x.pi * y.ti);
-    z.ai = (x.ai + y.ai) + fma(x.pr, y.ti, x.pi * y.tr);
-    z.pr = x.pr + y.pr;
-    z.pi = x.pi + y.pi;
-    z.tr = x.tr + y.tr;
-    z.ti = x.ti + y.ti;
-    return z;
-}
 
 // |d_eff| of pattern p at wavelength m: one CTA per (m, p), threads own
 // contiguous domain ranges, partial (acc, P, T) per thread stitched in
@@ -521,86 +507,16 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_fast(const double2 *__restr
 // 32 runs are stitched by a fixed shuffle tree (deterministic).
 constexpr int kFinishWarps = 4;
 
-// Column-sharded runs (multi-GPU): rank k scored the global segments
-// [floor(k S / world), floor((k+1) S / world)) into its slot of the
-// all-gathered partials, laid out [world][n_wl][rows][S_slot][6]; segment s
-// lives in rank (world (s+1) - 1) / S.  One GPU: world = 1, S_slot = S.
-__device__ __forceinline__ const double *seg_ptr(const double *part, int s, int lam, int64_t r, int64_t rows, int n_wl,
-                                                 int S, int world, int S_slot) {
-    int rk = 0, loc = s;
-    if (world > 1) {
-        rk = (world * (s + 1) - 1) / S;
-        loc = s - (rk * S) / world;
-    }
-    return part + ((((int64_t)rk * n_wl + lam) * rows + r) * S_slot + loc) * kPartDoubles;
-}
 
-__global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(
-    const double *part, int S, int world, int S_slot, int64_t rows, int n_wl, const double2 *__restrict__ w,
-    const double2 *__restrict__ h, int thg, double scale, int multi, double g0, double beta,
-    double *__restrict__ gains, double *__restrict__ out) {
+__global__ void __launch_bounds__(32 * kFinishWarps) k_fit_finish(FinishArgs f, double *__restrict__ out) {
     QTRACE(2);
     pdl_wait();
     QTRACE_STARTED();
     const int64_t r = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (r >= rows) return;
-    const int per = (S + 31) / 32;
-    const int s0 = lane * per;
-    const int s1 = s0 + per < S ? s0 + per : S;
-    double gmax = 0.0, gmin = 0.0;
-    for (int lam = 0; lam < n_wl; ++lam) {
-        double ar, ai;
-        if (S == 1) {
-            const double *p = part + ((int64_t)lam * rows + r) * kPartDoubles;
-            ar = __ldcg(p);  // exact mode: the row's sum, untouched
-            ai = __ldcg(p + 1);
-        } else {
-            Seg acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int s = s0; s < s1; ++s) {
-                const double *q = seg_ptr(part, s, lam, r, rows, n_wl, S, world, S_slot);
-                const Seg y = {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5)};
-                acc = s == s0 ? y : seg_cat(acc, y);
-            }
-            for (int off = 1; off < 32; off <<= 1) {
-                Seg o;
-                o.ar = __shfl_down_sync(0xffffffffu, acc.ar, off);
-                o.ai = __shfl_down_sync(0xffffffffu, acc.ai, off);
-                o.pr = __shfl_down_sync(0xffffffffu, acc.pr, off);
-                o.pi = __shfl_down_sync(0xffffffffu, acc.pi, off);
-                o.tr = __shfl_down_sync(0xffffffffu, acc.tr, off);
-                o.ti = __shfl_down_sync(0xffffffffu, acc.ti, off);
-                const bool has_other = lane + off < 32 && (lane + off) * per < S;
-                if ((lane & (2 * off - 1)) == 0 && has_other) acc = seg_cat(acc, o);
-            }
-            ar = acc.ar;
-            ai = acc.ai;
-        }
-        if (lane != 0) continue;
-        const double2 ww = w[lam];
-        double zr = ww.x * ar - ww.y * ai;
-        double zi = ww.x * ai + ww.y * ar;
-        if (thg) {
-            const double2 hh = h[lam];
-            zr += hh.x;
-            zi += hh.y;
-        }
-        double g = hypot_glibc(zr, zi);
-        if (scale != 1.0) g /= scale;
-        if (!multi) {
-            out[r] = g;
-            return;
-        }
-        if (lam == 0 || g > gmax) gmax = g;
-        if (lam == 0 || g < gmin) gmin = g;
-        gains[r * n_wl + lam] = g;
-    }
-    if (lane != 0) return;
-    double *dv = gains + r * n_wl;
-    for (int lam = 0; lam < n_wl; ++lam) dv[lam] = fabs(g0 - dv[lam]);
-    double f = pairwise_sum_seq(dv, n_wl);
-    f += beta * (gmax - gmin);
-    out[r] = -f;
+    if (r >= f.rows) return;
+    const double g = finish_row(f, r, lane);
+    if (lane == 0) out[r] = g;
 }
 
 // ------------------------------------------------------------ top-k
@@ -710,16 +626,53 @@ int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_word
     return QPM_OK;
 }
 
+FinishArgs finish_args(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
+                       double *gains) {
+    FinishArgs f;
+    f.part = part;
+    f.S = S;
+    f.world = world;
+    f.S_slot = S_slot;
+    f.rows = rows;
+    f.n_wl = p->n_wl;
+    f.w = (const double2 *)p->w;
+    f.h = (const double2 *)p->h;
+    f.thg = p->process == QPM_PROCESS_THG;
+    f.scale = p->scale;
+    f.multi = p->multi;
+    f.g0 = p->g0;
+    f.beta = p->beta;
+    f.gains = gains;
+    return f;
+}
+
 int launch_fitness_finish(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
                           double *gains, double *out, cudaStream_t stream, int *launches, bool pdl) {
     if (rows == 0) return QPM_OK;
-    const int thg = p->process == QPM_PROCESS_THG;
     QPM_CUDA_TRY(launch_k(pdl, k_fit_finish, dim3((unsigned)((rows + kFinishWarps - 1) / kFinishWarps)),
-                          dim3(32 * kFinishWarps), 0, stream, part, S, world, S_slot, rows, p->n_wl,
-                          (const double2 *)p->w, (const double2 *)p->h, thg, p->scale, p->multi, p->g0, p->beta,
-                          gains, out));
+                          dim3(32 * kFinishWarps), 0, stream, finish_args(p, part, S, world, S_slot, rows, gains), out));
     if (launches) *launches += 1;
     return QPM_OK;
+}
+
+// the segment partials of `rows` bit rows into fs->part (fast: p->S segments;
+// exact: the whole row as one partial), for a caller that finishes them
+int launch_fitness_partials(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
+                            const int32_t *row_index, int64_t rows, int mode, cudaStream_t stream, int *launches,
+                            bool pdl, int *S_out) {
+    QPM_ARG_CHECK(row_words == p->W, "row_words must equal qpm_problem_row_words()");
+    QPM_ARG_CHECK(rows >= 0 && rows <= fs->rows, "rows exceed the reserved fitness scratch");
+    if (mode == QPM_MODE_EXACT) {
+        *S_out = 1;
+        if (rows == 0) return QPM_OK;
+        const dim3 grid((unsigned)((rows + 127) / 128), (unsigned)p->n_wl);
+        QPM_CUDA_TRY(launch_k(pdl, k_fit_exact, grid, dim3(128), 0, stream, (const double2 *)p->e1, (const double2 *)p->b,
+                              p->D, p->process == QPM_PROCESS_THG, bits, p->W, row_index, rows, fs->part));
+        if (launches) *launches += 1;
+        return QPM_OK;
+    }
+    *S_out = p->S;
+    return launch_fitness_scan(p, bits, row_words, row_index, rows, fs->part, p->S, stream, launches, pdl);
 }
 
 int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,

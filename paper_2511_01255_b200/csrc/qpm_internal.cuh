@@ -221,6 +221,9 @@ int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_word
 // all-gathered column-shard slots [world][n_wl][rows][S_slot][6])
 int launch_fitness_finish(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
                           double *gains, double *out, cudaStream_t stream, int *launches, bool pdl);
+int launch_fitness_partials(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
+                            const int32_t *row_index, int64_t rows, int mode, cudaStream_t stream, int *launches,
+                            bool pdl, int *S_out);
 }  // namespace qpm
 struct qpm_problem;
 namespace qpm {

@@ -11,7 +11,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL", "QPM_TOPK_THREADS", "QPM_STATS_THREADS",
-         "QPM_TOPK_CTAS", "QPM_DE_ROWS", "QPM_DE_ITEM", "QPM_GRAPH_GENS")
+         "QPM_TOPK_CTAS", "QPM_DE_ROWS", "QPM_DE_ITEM", "QPM_GRAPH_GENS",
+         "QPM_FUSED_SELECT")
 
 
 @pytest.fixture(scope="module")
@@ -44,6 +45,8 @@ VARIANTS = [
     {"QPM_WOLF": "side"},
     {"QPM_TOPK_CTAS": "3"},
     {"QPM_GRAPH_GENS": "1"},
+    {"QPM_FUSED_SELECT": "0"},
+    {"QPM_FUSED_SELECT": "0", "QPM_TOPK_CTAS": "2"},
     {"QPM_GRAPH_GENS": "7", "QPM_PDL": "0"},
     {"QPM_TOPK_CTAS": "32"},
     {"QPM_WOLF": "side", "QPM_PDL": "0", "QPM_PLAN_CTAS": "7"},
@@ -91,7 +94,7 @@ def test_repeated_runs_are_identical(q, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{}, {"QPM_WOLF": "planner"}, {"QPM_WOLF": "planner", "QPM_PDL": "0"},
-                                 {"QPM_WOLF": "mixed"}, {"QPM_WOLF": "side"}],
+                                 {"QPM_WOLF": "mixed"}, {"QPM_WOLF": "side"}, {"QPM_FUSED_SELECT": "0"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_c2_shape_runs_match_default(q, monkeypatch, env):
     """The C2 shape (NP 1024, D 10^4) for 600 generations, twice per schedule:
@@ -110,3 +113,5 @@ def test_large_population_multi_cta_selection(q, monkeypatch):
     want = _trace(q, monkeypatch, {"QPM_TOPK_CTAS": "1", "QPM_DE_ROWS": "0"}, D=1300, NP=8192, G=6)[0]
     got = _trace(q, monkeypatch, {}, D=1300, NP=8192, G=6)[0]
     assert np.array_equal(got, want)
+    fused = _trace(q, monkeypatch, {"QPM_FUSED_SELECT": "1"}, D=1300, NP=8192, G=6)[0]  # 8 stats elements per thread
+    assert np.array_equal(fused, want)
