@@ -846,13 +846,15 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
     // segment length (in 128-domain chunks) depends only on D and the
     // wavelength count, never on the batch, so fitness stays a pure function
     // of the row bits; longer segments when wavelengths supply parallelism.
-    // One wavelength: 4 chunks, or 2 when that leaves fewer than 32 segments
-    // (C2, D = 10^4: 40 segments, which split evenly over 2, 4 and 8 GPUs;
-    // same single-GPU speed, measured)
+    // One wavelength: 3 chunks (C2, D = 10^4: 27 segments; alternating A/B
+    // on one B200: 112.1 / 114.0 / 116.5 us per generation for 3 / 2 / 1
+    // chunks, 4 was slower still), or 2 when 3 leaves fewer than 16 segments.
+    // Multi-GPU runs choose their own (bench.py: 2, an even split of C2 over
+    // 2, 4 and 8 GPUs) through QPM_SEG_CHUNKS.
     if (n_wl > 1)
         p.seg_chunks = 4 * std::min(n_wl, 8);
     else
-        p.seg_chunks = (p.nchunks + 3) / 4 < 32 ? 2 : 4;
+        p.seg_chunks = (p.nchunks + 2) / 3 < 16 ? 2 : 3;
     p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, p.seg_chunks));
     if (const char *env = getenv("QPM_SEG_CHUNKS")) {  // tuning override (changes fitness rounding only)
         const int v = atoi(env);

@@ -40,14 +40,15 @@ def shard_columns(D: int, world: int, rank: int, n_wl: int = 1, seg_chunks: int 
     """Gene columns [g0, g1) of `rank` (the engine's split, qpm_engine_create):
     rank k owns the fitness segments [floor(k S / W), floor((k+1) S / W)) of
     the problem and the genes under them; a segment is seg_chunks 128-domain
-    chunks (one wavelength: 4, or 2 when that leaves fewer than 32 segments;
-    4 min(n_wl, 8) with several wavelengths)."""
+    chunks (one wavelength: 3, or 2 when that leaves fewer than 16 segments;
+    4 min(n_wl, 8) with several wavelengths; QPM_SEG_CHUNKS overrides it in
+    the library, pass seg_chunks here to match)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside [0, {world})")
     words = -(-(-(-D // 32)) // 4) * 4
     nchunks = words // 4
     if seg_chunks is None:  # qpm_problem_create's default
-        seg_chunks = 4 * min(n_wl, 8) if n_wl > 1 else (2 if -(-nchunks // 4) < 32 else 4)
+        seg_chunks = 4 * min(n_wl, 8) if n_wl > 1 else (2 if -(-nchunks // 3) < 16 else 3)
         seg_chunks = max(1, min(nchunks, seg_chunks))
     S = -(-nchunks // seg_chunks)
     if S < world:

@@ -222,10 +222,11 @@ def test_shard_columns_partition():
         spans = [shard_columns(D, world, r) for r in range(world)]
         assert spans[0][0] == 0 and spans[-1][1] == D
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
-        assert all(g0 % 256 == 0 and g1 > g0 for g0, g1 in spans)  # whole segments (2 or 4 chunks)
+        assert all(g0 % 128 == 0 and g1 > g0 for g0, g1 in spans)  # whole segments (2 or 3 chunks)
         widths = [g1 - g0 for g0, g1 in spans]
-        assert max(widths[:-1] or [0]) - min(widths[:-1] or [0]) <= 512
-    assert [shard_columns(10_000, 8, r)[1] - shard_columns(10_000, 8, r)[0] for r in range(7)] == [1280] * 7
+        assert max(widths[:-1] or [0]) - min(widths[:-1] or [0]) <= 384
+    assert [shard_columns(10_000, 8, r, seg_chunks=2)[1] - shard_columns(10_000, 8, r, seg_chunks=2)[0]
+            for r in range(7)] == [1280] * 7
     with pytest.raises(ValueError, match="segments"):
         shard_columns(40, 2, 0)
     with pytest.raises(ValueError):
