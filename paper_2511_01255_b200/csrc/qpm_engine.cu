@@ -66,7 +66,10 @@ constexpr int kCtaThreads = 1024;   // single-CTA select / top-k / stats kernels
 #define QPM_DE_CHUNK 4096
 #endif
 constexpr int kDeChunk = QPM_DE_CHUNK;  // genes per DE-trial CTA (multiple of 1024)
-constexpr int kApplyThreads = 128;  // k_gwo_apply: 32-gene words per CTA
+#ifndef QPM_APPLY_THREADS
+#define QPM_APPLY_THREADS 128
+#endif
+constexpr int kApplyThreads = QPM_APPLY_THREADS;  // k_gwo_apply: 32-gene words per CTA
 #ifndef QPM_DE_MINB
 #define QPM_DE_MINB 4  // k_de_trial CTAs per SM the register budget is sized for
 #endif      // genes per DE-trial CTA (amortizes the per-row setup)

@@ -373,7 +373,10 @@ __global__ void __launch_bounds__(kSpecThreads) k_spectrum(int thg, double t, in
 
 constexpr int kChunkEntries = kQuadsPerChunk * kQuadEntries;  // 768 double2 = 12 KB
 constexpr uint32_t kChunkBytes = kChunkEntries * sizeof(double2);
-constexpr int kFitBufs = 4;  // table chunks in flight: a C2 segment (4 chunks) is staged at once
+#ifndef QPM_FIT_BUFS
+#define QPM_FIT_BUFS 3  // (4: C2 110.1, C5 fitness 2040 us; 3: 109.1, 2029 us -- alternating A/B)
+#endif
+constexpr int kFitBufs = QPM_FIT_BUFS;  // table chunks in flight (a whole C2 segment is staged at once)
 constexpr int kFitSmem = kFitBufs * kChunkBytes;  // dynamic shared memory (48 KB)
 
 template <bool THG>
