@@ -1478,10 +1478,14 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
 #ifndef QPM_FS_THREADS
 #define QPM_FS_THREADS 256
 #endif
-constexpr int kFsThreads = QPM_FS_THREADS;  // fused finish + selection CTA
-constexpr int kFsRows = kFsThreads / 32;
+#ifndef QPM_FS_THREADS1
+#define QPM_FS_THREADS1 QPM_FS_THREADS
+#endif
+// fused finish + selection CTA: <0> (leaders) and <1> (statistics)
 template <int MODE>
-__global__ void __launch_bounds__(kFsThreads) k_finish_select(RunConsts c, FinishArgs f, EngineState *__restrict__ st,
+__host__ __device__ constexpr int fs_threads() { return MODE == 0 ? QPM_FS_THREADS : QPM_FS_THREADS1; }
+template <int MODE>
+__global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts c, FinishArgs f, EngineState *__restrict__ st,
                                                                const double *__restrict__ sched, double *cand,
                                                                double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                                int32_t *__restrict__ spare_of,
@@ -1493,7 +1497,7 @@ __global__ void __launch_bounds__(kFsThreads) k_finish_select(RunConsts c, Finis
     pdl_wait();
     QTRACE_STARTED();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t r = (int64_t)blockIdx.x * kFsRows + warp;
+    const int64_t r = (int64_t)blockIdx.x * (fs_threads<MODE>() / 32) + warp;
     if (r < c.NP) {  // warp-uniform
         const double g = finish_row(f, r, lane);
         if (lane == 0) {
@@ -1855,13 +1859,15 @@ static FinishArgs fused_finish_args(const Engine *e) {
 }
 static int launch_finish_select(Engine *e, int mode, cudaStream_t s) {
     const RunConsts &c = e->c;
-    const unsigned grid = (unsigned)((c.NP + kFsRows - 1) / kFsRows);
+    constexpr int r0 = fs_threads<0>() / 32, r1 = fs_threads<1>() / 32;
     if (mode == 0)
-        QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<0>, dim3(grid), dim3(kFsThreads), 0, s, c, fused_finish_args(e),
+        QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<0>, dim3((unsigned)((c.NP + r0 - 1) / r0)), dim3(fs_threads<0>()), 0,
+                              s, c, fused_finish_args(e),
                               e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of, e->spare_of, e->slot_bin,
                               e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt));
     else
-        QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<1>, dim3(grid), dim3(kFsThreads), stats_smem_bytes(c), s, c,
+        QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<1>, dim3((unsigned)((c.NP + r1 - 1) / r1)), dim3(fs_threads<1>()),
+                              stats_smem_bytes(c), s, c,
                               fused_finish_args(e), e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of,
                               e->spare_of, e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt + 1));
     return QPM_OK;
