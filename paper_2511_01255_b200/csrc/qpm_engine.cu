@@ -197,6 +197,25 @@ __device__ __forceinline__ RowRef row_ref(const RunConsts &c, int64_t slot, cons
     return r;
 }
 
+// the same from a slot tag (slot | bin << 31)
+constexpr uint32_t kBinTag = 0x80000000u;
+#ifndef QPM_SLOT_TAG
+#define QPM_SLOT_TAG 1
+#endif
+__device__ __forceinline__ RowRef row_ref_tag(const RunConsts &c, uint32_t tag, const double *genome,
+                                              const uint32_t *bits) {
+    const int64_t slot = (int64_t)(tag & ~kBinTag);
+    RowRef r;
+    if (tag & kBinTag) {
+        r.f = nullptr;
+        r.b = bits + slot * c.W;
+    } else {
+        r.f = genome + slot * c.Dp;
+        r.b = nullptr;
+    }
+    return r;
+}
+
 // de_mutate index draws (optimizer.py:229-247) and j_rand (optimizer.py:258)
 __device__ void de_row_draws(const RunConsts &c, uint64_t key, int64_t i, int4 &pk, int32_t &jr) {
     int64_t r[3];
@@ -498,7 +517,8 @@ __global__ void k_plan_bump(EngineState *st) {
 __global__ void __launch_bounds__(kRowThreads) k_init_population(RunConsts c, double *__restrict__ genome,
                                                                  uint32_t *__restrict__ bits,
                                                                  int32_t *__restrict__ slot_of,
-                                                                 int32_t *__restrict__ spare_of) {
+                                                                 int32_t *__restrict__ spare_of,
+                                                                 uint32_t *__restrict__ slot_tag) {
     const int64_t i = blockIdx.y;
     const uint64_t key = fold_key3(c.seed, 0, (uint64_t)i);  // stream (seed, 0, i), optimizer.py:223
     double *row = genome + i * c.Dp;
@@ -518,6 +538,7 @@ __global__ void __launch_bounds__(kRowThreads) k_init_population(RunConsts c, do
         }
     if (threadIdx.x == 0) {
         slot_of[i] = (int32_t)i;
+        if (slot_tag) slot_tag[i] = (uint32_t)i;
         spare_of[i] = (int32_t)(c.NP + i);
     }
 }
@@ -537,6 +558,7 @@ struct TrialArgs {
     const int32_t *jrand;    // [2][NP]
     uint32_t *planes;        // [2][NP][W][8] wolf planes
     const int32_t *slot_of, *spare_of;
+    const uint32_t *slot_tag;  // [NP] slot_of[i] | slot_bin[slot_of[i]] << 31 (QPM_SLOT_TAG)
     uint8_t *slot_bin;
     double *genome;
     uint32_t *bits;
@@ -572,10 +594,17 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
     const int4 pk = a.picks[b * c.NP + i];
     r.key = a.keys[b * c.NP + i];
     r.jr = a.jrand[b * c.NP + i];
-    r.xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
-    r.x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
-    r.x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
-    r.x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
+    if (a.slot_tag) {  // slot and +/-1 flag in one load: picks -> tag, no slot_bin level
+        r.xi = row_ref_tag(c, a.slot_tag[i], a.genome, a.bits);
+        r.x1 = row_ref_tag(c, a.slot_tag[pk.x], a.genome, a.bits);
+        r.x2 = row_ref_tag(c, a.slot_tag[pk.y], a.genome, a.bits);
+        r.x3 = row_ref_tag(c, a.slot_tag[pk.z], a.genome, a.bits);
+    } else {
+        r.xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
+        r.x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
+        r.x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
+        r.x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
+    }
     r.bin = !r.xi.f || !r.x1.f || !r.x2.f || !r.x3.f;
     r.out_slot = a.spare_of[i];
     r.out = a.genome + r.out_slot * c.Dp;
@@ -1212,7 +1241,8 @@ struct TopkScratch {
 __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, EngineState *__restrict__ st,
                                                              const double *cand,
                                                              double *__restrict__ fit, int32_t *__restrict__ slot_of,
-                                                             int32_t *__restrict__ spare_of, TopkScratch ts) {
+                                                             int32_t *__restrict__ spare_of, TopkScratch ts,
+                                                             uint32_t *__restrict__ slot_tag) {
     QTRACE(3);
     pdl_wait();
     QTRACE_STARTED();
@@ -1230,6 +1260,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_topk(RunConsts c, Engine
         if (f > v) {
             slot_of[i] = b;
             spare_of[i] = a;
+            if (slot_tag) slot_tag[i] = (uint32_t)b;  // a DE trial: an f64 row
             fit[i] = f;
             v = f;
         }
@@ -1281,7 +1312,8 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
                                                   double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                   int32_t *__restrict__ spare_of, uint8_t *__restrict__ slot_bin,
                                                   double *__restrict__ scratch, const SumTree &tr,
-                                                  double *__restrict__ trace, const SumTreeInline &tri, bool wait) {
+                                                  double *__restrict__ trace, const SumTreeInline &tri, bool wait,
+                                                  uint32_t *__restrict__ slot_tag) {
     const int64_t n = c.NP;
     // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
     // then the pairwise-sum tree (values, leaf offsets, children, levels)
@@ -1337,6 +1369,7 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
                 spare_of[i] = a;
                 fit[i] = f;
                 if (mode == 1) slot_bin[b] = 1;
+                if (slot_tag) slot_tag[i] = (uint32_t)b | (mode == 1 ? kBinTag : 0u);
                 v = f;
             }
         }
@@ -1463,9 +1496,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
                                                               int32_t *__restrict__ spare_of,
                                                               uint8_t *__restrict__ slot_bin,
                                                               double *__restrict__ scratch, SumTree tr,
-                                                              double *__restrict__ trace, SumTreeInline tri) {
+                                                              double *__restrict__ trace, SumTreeInline tri,
+                                                              uint32_t *__restrict__ slot_tag) {
     QTRACE(5);
-    select_stats_body(c, mode, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, true);
+    select_stats_body(c, mode, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, true,
+                      slot_tag);
 }
 
 // Fused fitness finish + selection (run_hybrid): one warp per row stitches its
@@ -1492,7 +1527,7 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
                                                                uint8_t *__restrict__ slot_bin,
                                                                double *__restrict__ scratch, SumTree tr,
                                                                double *__restrict__ trace, SumTreeInline tri,
-                                                               unsigned *cnt) {
+                                                               unsigned *cnt, uint32_t *__restrict__ slot_tag) {
     QTRACE(MODE == 0 ? 3 : 5);
     pdl_wait();
     QTRACE_STARTED();
@@ -1513,6 +1548,7 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
                 spare_of[r] = a;
                 fit[r] = g;
                 if (MODE == 1) slot_bin[b] = 1;
+                if (slot_tag) slot_tag[r] = (uint32_t)b | (MODE == 1 ? kBinTag : 0u);
             }
         }
     }
@@ -1526,7 +1562,8 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
     if (MODE == 0)
         block_topk_k(fit, c.NP, c.k, st->leaders);
     else
-        select_stats_body(c, 3, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, false);
+        select_stats_body(c, 3, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, false,
+                          nullptr);
     if (threadIdx.x == 0) *cnt = 0u;  // ready for the next launch (stream-ordered)
 }
 
@@ -1615,6 +1652,7 @@ struct Engine {
     int topk_ctas = 1;                 // k_select_topk CTAs (NP / 2048, at most kTopkMaxCtas; QPM_TOPK_CTAS)
     bool fused_select = true;          // run_hybrid, NP <= 2048: fused finish + selection kernels (QPM_FUSED_SELECT)
     unsigned *fs_cnt = nullptr;        // their arrival counters [2]
+    uint32_t *slot_tag = nullptr;      // [NP] slot | +/-1 flag per individual (trial setup in one load; QPM_SLOT_TAG)
     int S_cur = 1;                     // segments of the last one-GPU scan
     int32_t *topk_idx = nullptr;       // [kTopkMaxCtas][kTopSlots] per-CTA lists
     unsigned *topk_cnt = nullptr;      // arrival counter
@@ -1729,7 +1767,7 @@ static size_t stats_smem_bytes(const RunConsts &c) {
 static int launch_select_stats(Engine *e, int mode, cudaStream_t s) {
     QPM_CUDA_TRY(launch_k(e->pdl, k_select_stats, dim3(1), dim3(e->stats_threads), stats_smem_bytes(e->c), s, e->c, mode,
                           e->st, (const double *)e->sched, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
-                          e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline));
+                          e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline, e->slot_tag));
     return QPM_OK;
 }
 
@@ -1745,6 +1783,7 @@ static TrialArgs trial_args(const Engine *e, int64_t row_lo, int64_t n_rows) {
     a.planes = e->planes;
     a.cbits = e->cbits;
     a.slot_of = e->slot_of;
+    a.slot_tag = e->slot_tag;
     a.spare_of = e->spare_of;
     a.slot_bin = e->slot_bin;
     a.genome = e->genome;
@@ -1864,12 +1903,13 @@ static int launch_finish_select(Engine *e, int mode, cudaStream_t s) {
         QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<0>, dim3((unsigned)((c.NP + r0 - 1) / r0)), dim3(fs_threads<0>()), 0,
                               s, c, fused_finish_args(e),
                               e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of, e->spare_of, e->slot_bin,
-                              e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt));
+                              e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt, e->slot_tag));
     else
         QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<1>, dim3((unsigned)((c.NP + r1 - 1) / r1)), dim3(fs_threads<1>()),
                               stats_smem_bytes(c), s, c,
                               fused_finish_args(e), e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of,
-                              e->spare_of, e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt + 1));
+                              e->spare_of, e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt + 1,
+                              e->slot_tag));
     return QPM_OK;
 }
 static int fit_finish(Engine *e, double *out, cudaStream_t s, int *n) {
@@ -1997,7 +2037,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             mark("select_topk");
             QPM_CUDA_TRY(launch_k(e->pdl, k_select_topk, dim3((unsigned)e->topk_ctas), dim3(e->topk_threads), 0, s, c,
                                   e->st, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
-                                  TopkScratch{e->topk_idx, e->topk_cnt}));
+                                  TopkScratch{e->topk_idx, e->topk_cnt}, e->slot_tag));
         }
         if (e->wolf_side) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
@@ -2265,6 +2305,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->topk_idx, (size_t)kTopkMaxCtas * kTopSlots);
     QPM_ALLOC(e->topk_cnt, 1);
     QPM_ALLOC(e->fs_cnt, 2);
+    if (QPM_SLOT_TAG) QPM_ALLOC(e->slot_tag, NP);
     if (e->world > 1) {
         QPM_ALLOC(e->gpart, (size_t)e->world * gpart_slot(e));
         QPM_ALLOC(e->ggains, (size_t)NP * gp.n_wl);
@@ -2385,7 +2426,8 @@ int qpm_engine_init(qpm_engine *h) {
     Engine *e = h->e;
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
-    k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of);
+    k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of,
+                                                                 e->slot_tag);
     QPM_LAUNCH_CHECK();
     int rc;
     if (e->sharded()) {
