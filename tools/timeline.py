@@ -13,7 +13,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-NAMES = ["de_trial", "fit_fast", "fit_finish", "select_topk", "gwo_apply", "select_stats", "plan_rows", "plan_bump", "plan_wolf"]
+NAMES = ["de_trial", "fit_fast", "fit_finish", "topk|fs<0>", "gwo_apply", "stats|fs<1>", "plan_rows", "plan_bump",
+         "plan_wolf"]  # ids 3 / 5: k_select_topk / k_select_stats or the fused k_finish_select<0> / <1>
 IDS, LEN = 9, 4096
 
 
@@ -87,8 +88,7 @@ def main():
               f"{(rel[:, 2] - rel[:, 1]).mean():8.2f}")
     print("fit_fast CTA 0 stamps (us from start): bits, first table, loop end, stored =",
           [round(float(x), 2) for x in stamps(L)[1:5]])
-    print("select_stats stamps (us from start): selected, synced, max/min, mean, var, tail =",
-          [round(float(x), 2) for x in stamps(L, "qpm_dev_trace_engine", 5, 7)[1:7]])
+
 
 
 
@@ -100,6 +100,8 @@ def stamps(L, fn_name="qpm_dev_trace_fitness", kid=1, n=8):
     assert getattr(L, fn_name)(2, buf.ctypes.data_as(ctypes.c_void_p), None) == 0
     s = buf[kid].astype(np.int64)
     s = s[s[:, 0] > 0]
+    if len(s) == 0:
+        return np.zeros(n)
     rel = (s[:, :n] - s[:, :1]) / 1e3
     return rel.mean(axis=0)
 
