@@ -1011,7 +1011,7 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, con
     const double a = sched[g * QPM_SCHED_COLS + QPM_SCHED_A_NOW];
     const double two_a = 2.0 * a;
     const uint64_t key = fold_key3(c.seed, (uint64_t)g, (uint64_t)i);
-    const uint64_t D = (uint64_t)c.Dg;  // stream layout; genes j of this shard sit at g0 + j
+    const uint64_t gD = (uint64_t)c.Dg * kGold;  // stream layout (Dg genes; this shard's gene j is g0 + j)
     const RowRef x = row_ref(c, slot_of[i], slot_bin, genome, bits);
     const RowRef L0 = row_ref(c, slot_of[st->leaders[0]], slot_bin, genome, bits);
     const RowRef L1 = row_ref(c, slot_of[st->leaders[1]], slot_bin, genome, bits);
@@ -1029,10 +1029,13 @@ __global__ void __launch_bounds__(kRowThreads) k_gwo_continuous(RunConsts c, con
             const double xj = x.at(j);
             const double Lm[3] = {L0.at(j), L1.at(j), L2.at(j)};
             double moved[3];
+            // counter states: position p sits at key + (p + 1) GOLD, so the six
+            // draws of gene jj are one product plus constant offsets k D GOLD
+            const uint64_t zj = key + (jj + 1) * kGold;
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
-                const double r1 = draw_u(key, 2 * m * D + jj);
-                const double r2 = draw_u(key, 2 * m * D + D + jj);
+                const double r1 = (double)(mix64(zj + (uint64_t)(2 * m) * gD) >> 11) * kTwoM53;
+                const double r2 = (double)(mix64(zj + (uint64_t)(2 * m + 1) * gD) >> 11) * kTwoM53;
                 const double av = two_a * r1 - a;
                 const double cv = 2.0 * r2;
                 const double dist = fabs(cv * Lm[m] - xj);

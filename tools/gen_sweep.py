@@ -2,7 +2,7 @@
 
     python tools/gen_sweep.py 'QPM_PDL=0' 'QPM_PDL=1' 'QPM_WOLF=planner,QPM_PLAN_FORK=trial,QPM_PLAN_CTAS=296'
 Each argument is a comma-separated env assignment list applied before the engine is created
-(QPM_SWEEP_SHAPE="NP,D" in the environment changes the shape from C2)
+(QPM_SWEEP_SHAPE="NP,D" and QPM_SWEEP_ALGO=hybrid|de|gwo in the environment change the run from C2 hybrid)
 (the QPM_* knobs are read at engine / problem creation).  Every setting times the same
 generations (warm-up 50, then 3 x 300), reported as the median us per generation.
 """
@@ -32,7 +32,9 @@ def main():
             os.environ[k] = v
         NPs, Ds = (int(x) for x in os.environ.get("QPM_SWEEP_SHAPE", "1024,10000").split(","))
         obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, Ds)
-        eng = q.Engine(obj, "hybrid", pop_size=NPs, generations=1000, seed=0, de=q.DEParams(), gwo=q.GWOParams(),
+        algo = os.environ.get("QPM_SWEEP_ALGO", "hybrid")
+        gwo = q.GWOParams(a=0.1, a_final=0.01) if algo == "gwo" else q.GWOParams()
+        eng = q.Engine(obj, algo, pop_size=NPs, generations=1000, seed=0, de=q.DEParams(), gwo=gwo,
                        sch=q.Schedules())
         eng.init()
         eng.step(50)
