@@ -12,7 +12,7 @@
 //   slot_bin u8 [2 NP]       1 = the slot holds a wolf candidate whose genome is
 //                            exactly +/-1 (optimizer.py:376): its f64 row is
 //                            never written, readers expand the bits instead
-//   planes  u32 [2][NP][W][8] per-gene wolf draw outcomes as bit-planes
+//   planes  u32 [2][NP][W][4] per-gene wolf draw outcomes as bit-planes
 //   fit, cand f64 [NP]; keys u64 [2][NP]; picks int4 [2][NP] (r1, r2, r3, m)
 //   sched   f64 [G+1][8]     per-generation scalars, host-computed
 //   trace   f64 [G+1][5]     (g, best, mean, F|a, pop_std)
@@ -248,7 +248,12 @@ __device__ void de_row_draws(const RunConsts &c, uint64_t key, int64_t i, int4 &
 //      u_plus < p_plus(count) <=> count >= L)
 // so a late generation writes 3 planes and an early one 5.  The leader vote
 // is then evaluated 32 genes at a time with bit-sliced logic.
-constexpr int kPlanes = 8;  // plane slots per word (P0..P4 used)
+#ifndef QPM_PLANES
+#define QPM_PLANES 4
+#endif
+// stored plane slots per 32-gene word: P0..P2 (P3, P4 live in k_gwo_apply's
+// registers only), one 16-byte store / load per word
+constexpr int kPlanes = QPM_PLANES;
 
 // bit-sliced leader vote of one 32-gene word.  ld[t]: leader t's sign bits
 // (1 = -1); pl: the word's planes.  Returns the candidate's sign bits.
