@@ -47,7 +47,11 @@ void set_error(const char *fmt, ...);
 #ifndef QPM_FIT_THREADS
 #define QPM_FIT_THREADS 128
 #endif
-constexpr int kFitThreads = QPM_FIT_THREADS;  // rows per fast-fitness CTA (one lane per row)
+constexpr int kFitThreads = QPM_FIT_THREADS;  // rows per fast-fitness CTA (one lane per row), several wavelengths
+#ifndef QPM_FIT_THREADS1
+#define QPM_FIT_THREADS1 256
+#endif
+constexpr int kFitThreadsMax = QPM_FIT_THREADS1;  // ... one wavelength (and the launch bound)
 constexpr int kQuadsPerChunk = 32;    // 128 domains = 4 u32 words per chunk
 constexpr int kQuadEntries = 24;      // B[8], E[8], I[8] complex entries per quad (by relative signs)
 constexpr int kPartDoubles = 6;       // acc, P, T (complex) per (row, wavelength, segment)
