@@ -66,3 +66,24 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(_native.QpmError, match="no CUDA device"):
         q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)),
                          q.MismatchTable({1404.0: q.PhaseMismatchPair(0.3, 0.7)}), 1.0, 16)
+
+
+def test_run_params_layout_matches_header(tmp_path):
+    """ctypes' RunParams mirrors qpm_run_params field for field (size and offsets
+    from the C compiler), so the Python side cannot drift from the ABI."""
+    import ctypes
+
+    fields = [name for name, _ in _native.RunParams._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "qpm_b200.h"\nint main(void) {\n'
+                   '  printf("%zu\\n", sizeof(qpm_run_params));\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(qpm_run_params, {f}));\n' for f in fields)
+                   + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    res = subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        pytest.skip(f"gcc unavailable: {res.stderr[:200]}")
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert vals[0] == ctypes.sizeof(_native.RunParams)
+    assert vals[1:] == [getattr(_native.RunParams, f).offset for f in fields]
