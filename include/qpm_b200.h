@@ -183,10 +183,21 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
 int qpm_engine_destroy(qpm_engine *e);
 /* device bytes held by the engine */
 int64_t qpm_engine_device_bytes(const qpm_engine *e);
-/* init_population + generation-0 evaluation and trace row (async) */
+/* init_population + generation-0 evaluation and trace row (async); once per
+ * engine (a second call returns QPM_ERR_STATE) */
 int qpm_engine_init(qpm_engine *e);
-/* run n generations (async; CUDA-graph replays when use_graph != 0) */
+/* run n generations (async).  use_graph != 0: CUDA-graph replays (one
+ * graph of 10 generations plus a one-generation graph for the remainder),
+ * captured on first use -- except that an engine without graphs runs a step
+ * of fewer than 256 generations with eager launches, which is cheaper than
+ * capturing for so short a run (same kernels, bit-identical results);
+ * qpm_engine_prepare forces the capture. */
 int qpm_engine_step(qpm_engine *e, int64_t n, int use_graph);
+/* capture, instantiate and upload every graph a graph-mode step of n
+ * generations replays, without running a generation (synchronous); a later
+ * qpm_engine_step then only launches.  Lets a caller keep the one-time
+ * capture cost out of a timed region. */
+int qpm_engine_prepare(qpm_engine *e, int64_t n);
 /* select the final best (top-1 of the current population, or best-ever for
  * run_gwo) into the result buffer (async) */
 int qpm_engine_finalize(qpm_engine *e);

@@ -23,7 +23,7 @@ EXPORTS = (
     "qpm_problem_create", "qpm_problem_destroy", "qpm_problem_row_words", "qpm_pack_signs",
     "qpm_fitness_bits", "qpm_evaluate_block_host", "qpm_sum_block_host", "qpm_reduce_best", "qpm_brute_force", "qpm_sweep_spectrum",
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
-    "qpm_engine_step", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
+    "qpm_engine_step", "qpm_engine_prepare", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
     "qpm_engine_read_best", "qpm_engine_read_population", "qpm_engine_profile", "qpm_engine_launches_per_generation",
     "qpm_engine_fitness_ptr", "qpm_nccl_unique_id", "qpm_engine_set_comm", "qpm_engine_columns",
     "qpm_engine_init_finish",
@@ -105,6 +105,7 @@ def lib():
         "qpm_engine_device_bytes": (I64, [P]),
         "qpm_engine_init": (I32, [P]),
         "qpm_engine_step": (I32, [P, I64, I32]),
+        "qpm_engine_prepare": (I32, [P, I64]),
         "qpm_engine_finalize": (I32, [P]),
         "qpm_engine_generation": (I32, [P, P]),
         "qpm_engine_read_trace": (I32, [P, I64, I64, P]),

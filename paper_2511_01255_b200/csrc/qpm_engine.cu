@@ -2432,6 +2432,12 @@ static int init_tail(Engine *e) {
 int qpm_engine_init(qpm_engine *h) {
     QPM_ARG_CHECK(h, "engine");
     Engine *e = h->e;
+    if (e->initialized || e->init_pending) {
+        // a second init would rerun init_population with st->g past 0, and the
+        // statistics kernel would then write trace row g instead of row 0
+        set_error("qpm_engine_init called twice: create a new engine for a new run");
+        return QPM_ERR_STATE;
+    }
     const RunConsts &c = e->c;
     cudaStream_t s = e->stream;
     k_init_population<<<row_grid(e, c.NP), kRowThreads, 0, s>>>(c, e->genome, e->bits, e->slot_of, e->spare_of,
@@ -2461,58 +2467,91 @@ int qpm_engine_init_finish(qpm_engine *h) {
     return init_tail(h->e);
 }
 
-int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
-    QPM_ARG_CHECK(h, "engine");
-    Engine *e = h->e;
+constexpr int64_t kGraphMinGens = 256;  // fresh engines capture graphs from this run length on
+
+// capture `gens` generations into one executable graph (uploaded to the
+// device, so its first launch costs no more than a replay)
+static int capture_graph(Engine *e, int gens, cudaGraph_t *graph, cudaGraphExec_t *exec) {
+    QPM_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    int launches = 0, rc = QPM_OK;
+    for (int t = 0; t < gens && rc == QPM_OK; ++t) {
+        e->pdl_trial = t > 0;
+        int l = 0;
+        rc = enqueue_generation(e, &l);
+        launches += l;
+    }
+    e->pdl_trial = false;
+    cudaGraph_t g = nullptr;
+    cudaError_t err = cudaStreamEndCapture(e->stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (err != cudaSuccess) {
+        set_error("graph capture: %s", cudaGetErrorString(err));
+        return QPM_ERR_CUDA;
+    }
+    *graph = g;
+    QPM_CUDA_TRY(cudaGraphInstantiateWithFlags(exec, g, cudaGraphInstantiateFlagUseNodePriority));
+    QPM_CUDA_TRY(cudaGraphUpload(*exec, e->stream));
+    e->launches = launches / gens;
+    return QPM_OK;
+}
+
+// every graph a graph-mode step of n generations replays: the one-generation
+// graph, and the graph_gens-generation graph when n reaches it
+static int ensure_graphs(Engine *e, int64_t n) {
+    int rc;
+    const bool use_k = e->graph_gens > 1 && n >= e->graph_gens;
+    const bool need_1 = !use_k || n % e->graph_gens != 0;
+    if (need_1 && !e->exec && (rc = capture_graph(e, 1, &e->graph, &e->exec))) return rc;
+    if (use_k && !e->exec_k && (rc = capture_graph(e, e->graph_gens, &e->graph_k, &e->exec_k))) return rc;
+    return QPM_OK;
+}
+
+static int step_ready(Engine *e, const char *what) {
     if (!e->initialized) {
-        set_error("qpm_engine_step before qpm_engine_init");
+        set_error("%s before qpm_engine_init", what);
         return QPM_ERR_STATE;
     }
-    QPM_ARG_CHECK(n >= 0 && e->g_done + n <= e->c.G, "generation count exceeds G");
     if (e->world > 1 && !e->comm) {
         set_error("sharded engine without a communicator: drive it with qpm_engine_run_phase");
         return QPM_ERR_STATE;
     }
+    return QPM_OK;
+}
+
+int qpm_engine_prepare(qpm_engine *h, int64_t n) {
+    QPM_ARG_CHECK(h, "engine");
+    Engine *e = h->e;
+    int rc;
+    if ((rc = step_ready(e, "qpm_engine_prepare"))) return rc;
+    QPM_ARG_CHECK(n >= 0, "n >= 0");
     if (n == 0) return QPM_OK;
+    if ((rc = ensure_graphs(e, n))) return rc;
+    QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return QPM_OK;
+}
+
+int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
+    QPM_ARG_CHECK(h, "engine");
+    Engine *e = h->e;
+    int rc0;
+    if ((rc0 = step_ready(e, "qpm_engine_step"))) return rc0;
+    QPM_ARG_CHECK(n >= 0 && e->g_done + n <= e->c.G, "generation count exceeds G");
+    if (n == 0) return QPM_OK;
+    // A short run on an engine without graphs launches eagerly: PDL already
+    // overlaps the launches, so a replayed generation saves only ~3 us
+    // against ~0.9 ms of capture, instantiation and teardown (C2, B200,
+    // tools/e2e_probe.py: 20 generations 3.0 ms eager vs 3.9 ms with graphs).
+    // Both paths run the same kernels in the same order (bit-identical).
+    const bool have = e->exec || e->exec_k;
+    if (use_graph && !have && n < kGraphMinGens) use_graph = 0;
     if (use_graph) {
-        // capture `gens` generations into one executable graph
-        auto capture = [&](int gens, cudaGraph_t *graph, cudaGraphExec_t *exec) -> int {
-            QPM_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-            int launches = 0, rc = QPM_OK;
-            for (int t = 0; t < gens && rc == QPM_OK; ++t) {
-                e->pdl_trial = t > 0;
-                int l = 0;
-                rc = enqueue_generation(e, &l);
-                launches += l;
-            }
-            e->pdl_trial = false;
-            cudaGraph_t g = nullptr;
-            cudaError_t err = cudaStreamEndCapture(e->stream, &g);
-            if (rc) {
-                if (g) cudaGraphDestroy(g);
-                return rc;
-            }
-            if (err != cudaSuccess) {
-                set_error("graph capture: %s", cudaGetErrorString(err));
-                return QPM_ERR_CUDA;
-            }
-            *graph = g;
-            QPM_CUDA_TRY(cudaGraphInstantiateWithFlags(exec, g, cudaGraphInstantiateFlagUseNodePriority));
-            e->launches = launches / gens;
-            return QPM_OK;
-        };
-        if (!e->exec) {
-            const int rc = capture(1, &e->graph, &e->exec);
-            if (rc) return rc;
-        }
+        if ((rc0 = ensure_graphs(e, n))) return rc0;
         int64_t t = 0;
-        if (e->graph_gens > 1 && n >= e->graph_gens) {
-            if (!e->exec_k) {
-                const int rc = capture(e->graph_gens, &e->graph_k, &e->exec_k);
-                if (rc) return rc;
-            }
+        if (e->graph_gens > 1 && n >= e->graph_gens)
             for (; t + e->graph_gens <= n; t += e->graph_gens) QPM_CUDA_TRY(cudaGraphLaunch(e->exec_k, e->stream));
-        }
         for (; t < n; ++t) QPM_CUDA_TRY(cudaGraphLaunch(e->exec, e->stream));
     } else {
         for (int64_t t = 0; t < n; ++t) {

@@ -578,6 +578,43 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const double *__restrict_
     }
 }
 
+// k in (8, 64]: k rounds of a block-wide argmax, round t over the elements
+// strictly worse than round t-1's winner in the (-value, index) order (a
+// strict total order, so the rounds enumerate the top-k exactly); each
+// round rescans the thread's elements (off the per-generation path)
+constexpr int kTopkRoundsMax = 64;
+__global__ void __launch_bounds__(kTopkThreads) k_topk_rounds(const double *__restrict__ vals, int64_t n, int k,
+                                                              int32_t *__restrict__ idx_out) {
+    __shared__ Cand red[kTopkThreads / 32];
+    __shared__ Cand win;
+    Cand last = {0.0, -1};  // nothing excluded yet
+    for (int t = 0; t < k; ++t) {
+        Cand c = {0.0, -1};
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const Cand e = {vals[i], (int32_t)i};
+            if ((last.i < 0 || better(last, e)) && better(e, c)) c = e;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            Cand o;
+            o.v = __shfl_down_sync(0xffffffffu, c.v, off);
+            o.i = __shfl_down_sync(0xffffffffu, c.i, off);
+            if (better(o, c)) c = o;
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Cand best = red[0];
+            for (int wv = 1; wv < (int)(blockDim.x >> 5); ++wv)
+                if (better(red[wv], best)) best = red[wv];
+            win = best;
+            idx_out[t] = best.i;
+        }
+        __syncthreads();
+        last = win;
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------ launchers
 int scratch_reserve(const Problem *p, FitScratch *fs, int64_t rows) {
     if (rows <= fs->rows) return QPM_OK;
@@ -605,8 +642,28 @@ void scratch_free(FitScratch *fs) {
     *fs = FitScratch{};
 }
 
+// Callers of the problem's own scratch hold p->mu while they enqueue.
+static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+// order this use of p->own after the previous one (any stream)
+static int own_acquire(Problem *p, cudaStream_t s) {
+    if (p->own_ev && !capturing(s)) QPM_CUDA_TRY(cudaStreamWaitEvent(s, p->own_ev, 0));
+    return QPM_OK;
+}
+static int own_release(Problem *p, cudaStream_t s) {
+    if (capturing(s)) return QPM_OK;
+    if (!p->own_ev) QPM_CUDA_TRY(cudaEventCreateWithFlags(&p->own_ev, cudaEventDisableTiming));
+    QPM_CUDA_TRY(cudaEventRecord(p->own_ev, s));
+    return QPM_OK;
+}
+
 static int problem_reserve(Problem *p, int64_t rows) {
     if (!p->own) p->own = new FitScratch;
+    // growing frees the old blocks into the device cache, where another
+    // allocation may pick them up: the last queued user must be done first
+    if (rows > p->own->rows && p->own_ev) QPM_CUDA_TRY(cudaEventSynchronize(p->own_ev));
     const int64_t before = p->own->bytes;
     const int rc = scratch_reserve(p, p->own, rows);
     p->device_bytes += p->own->bytes - before;
@@ -756,8 +813,12 @@ int problem_slice(const Problem *p, int64_t g0, int64_t Dl, qpm_problem **out) {
 
 int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out, cudaStream_t stream) {
     QPM_ARG_CHECK(n >= 1, "cannot reduce an empty list");
-    QPM_ARG_CHECK(k >= 1 && k <= n && k <= kTopkMax, "k must be in [1, min(n, 8)]");
-    k_topk<<<1, kTopkThreads, 0, stream>>>(values, n, k, idx_out);
+    QPM_ARG_CHECK(k >= 1 && k <= n && k <= kTopkRoundsMax, "k must be in [1, min(n, 64)]");
+    QPM_ARG_CHECK(n < (1LL << 31), "n < 2^31");
+    if (k <= kTopkMax)
+        k_topk<<<1, kTopkThreads, 0, stream>>>(values, n, k, idx_out);
+    else
+        k_topk_rounds<<<1, kTopkThreads, 0, stream>>>(values, n, k, idx_out);
     QPM_LAUNCH_CHECK();
     return QPM_OK;
 }
@@ -912,6 +973,10 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
 int qpm_problem_destroy(qpm_problem *h) {
     if (!h) return QPM_OK;
     Problem &p = h->p;
+    if (p.own_ev) {  // the scratch goes back to the block cache: its last user must be done
+        cudaEventSynchronize(p.own_ev);
+        cudaEventDestroy(p.own_ev);
+    }
     delete p.mu;
     p.mu = nullptr;
     cudaFree(p.e1);
@@ -942,10 +1007,15 @@ int qpm_pack_signs(const int8_t *signs_dev, int64_t rows, int64_t D, uint32_t *b
 int qpm_fitness_bits(qpm_problem *h, const uint32_t *bits_dev, int64_t row_words, const int32_t *row_index_dev,
                      int64_t rows, double *out_dev, int mode, void *stream) {
     QPM_ARG_CHECK(h, "problem");
-    int rc = problem_reserve(&h->p, rows);
+    Problem &p = h->p;
+    const cudaStream_t s = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lock(*p.mu);
+    int rc = problem_reserve(&p, rows);
     if (rc) return rc;
-    return launch_fitness(&h->p, h->p.own, bits_dev, row_words, row_index_dev, rows, out_dev, mode,
-                          (cudaStream_t)stream, nullptr);
+    if ((rc = own_acquire(&p, s))) return rc;
+    if ((rc = launch_fitness(&p, p.own, bits_dev, row_words, row_index_dev, rows, out_dev, mode, s, nullptr)))
+        return rc;
+    return own_release(&p, s);
 }
 
 int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, double *out, int mode) {
@@ -958,8 +1028,10 @@ int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, d
     QPM_CUDA_TRY(cudaMemcpyAsync(p.hp_signs, signs, (size_t)rows * p.D, cudaMemcpyHostToDevice, p.hp_stream));
     rc = launch_pack(p.hp_signs, rows, p.D, p.hp_bits, p.W, p.hp_stream);
     if (rc) return rc;
+    if ((rc = own_acquire(&p, p.hp_stream))) return rc;
     rc = launch_fitness(&p, p.own, p.hp_bits, p.W, nullptr, rows, p.hp_out, mode, p.hp_stream, nullptr);
     if (rc) return rc;
+    if ((rc = own_release(&p, p.hp_stream))) return rc;
     QPM_CUDA_TRY(cudaMemcpyAsync(out, p.hp_out, (size_t)rows * sizeof(double), cudaMemcpyDeviceToHost, p.hp_stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
     return QPM_OK;
@@ -1024,11 +1096,13 @@ int qpm_brute_force(qpm_problem *h, int n, int mode, int64_t chunk_rows, int64_t
     const int64_t chunk = (int64_t)std::min<uint64_t>(total, (uint64_t)chunk_rows);
     int rc = problem_reserve(&p, chunk);
     if (rc) return rc;
+    if ((rc = own_acquire(&p, s))) return rc;
     const size_t bits_bytes = (size_t)chunk * p.W * sizeof(uint32_t);
     uint32_t *bits = (uint32_t *)dev_cache_alloc(bits_bytes);
     double *vals = (double *)dev_cache_alloc((size_t)chunk * sizeof(double));
     int32_t *idx = (int32_t *)dev_cache_alloc(sizeof(int32_t) * 4);
     auto done = [&](int code) {
+        own_release(&p, s);
         if (s) cudaStreamSynchronize(s); else cudaDeviceSynchronize();
         dev_cache_release(bits, bits_bytes);
         dev_cache_release(vals, (size_t)chunk * sizeof(double));
@@ -1073,6 +1147,7 @@ int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows
     rc = launch_pack(p.hp_signs, rows, p.D, p.hp_bits, p.W, p.hp_stream);
     if (rc) return rc;
     const int thg = p.process == QPM_PROCESS_THG;
+    if ((rc = own_acquire(&p, p.hp_stream))) return rc;
     k_fit_exact<<<(unsigned)((rows + 127) / 128), 128, 0, p.hp_stream>>>(
         p.e1 + (int64_t)wl * p.D, thg ? p.b + (int64_t)wl * p.D : nullptr, p.D, thg, p.hp_bits, p.W, nullptr, rows,
         p.own->part);
@@ -1080,6 +1155,7 @@ int qpm_sum_block_host(qpm_problem *h, int wl, const int8_t *signs, int64_t rows
     // part rows are [acc.r, acc.i, 0, 0, 0, 0]; gather the first two doubles
     QPM_CUDA_TRY(cudaMemcpy2DAsync(out, 2 * sizeof(double), p.own->part, kPartDoubles * sizeof(double),
                                    2 * sizeof(double), (size_t)rows, cudaMemcpyDeviceToHost, p.hp_stream));
+    if ((rc = own_release(&p, p.hp_stream))) return rc;
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
     return QPM_OK;
 }

@@ -76,6 +76,11 @@ struct Problem {
     // scratch of the problem's own entry points (qpm_fitness_bits, host path);
     // every engine owns its scratch, so engines sharing a problem never race
     struct FitScratch *own = nullptr;
+    // recorded after every use of `own` on whatever stream made it; the next
+    // user's stream waits on it, so qpm_fitness_bits on a caller's stream and
+    // the host paths on hp_stream never overlap in the shared scratch, and
+    // the scratch is only regrown or released once its last user is done
+    cudaEvent_t own_ev = nullptr;
     // host plugin path buffers
     int8_t *hp_signs = nullptr;
     uint32_t *hp_bits = nullptr;

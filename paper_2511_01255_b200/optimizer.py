@@ -279,6 +279,10 @@ class Engine:
     def step(self, n: int, use_graph: bool = True):
         _native.check(_native.lib().qpm_engine_step(self.handle, int(n), int(use_graph)), "qpm_engine_step")
 
+    def prepare(self, n: int):
+        """Capture and upload the CUDA graphs a step(n) replays (keeps capture out of timed regions)."""
+        _native.check(_native.lib().qpm_engine_prepare(self.handle, int(n)), "qpm_engine_prepare")
+
     def finalize(self):
         _native.check(_native.lib().qpm_engine_finalize(self.handle), "qpm_engine_finalize")
 
@@ -334,10 +338,27 @@ def _trace_rows(arr: np.ndarray) -> list:
     return [make_trace_row(*row) for row in arr]
 
 
+def _check_wolf_rates(sch: Schedules, generations: int) -> None:
+    """The reference re-validates GWOParams with each generation's rates
+    (replace(gwo, p_dist=..., p_sl=..., p_flip=...), optimizer.py:447-452) and
+    so raises GWOParams' ValueError at the first generation whose scheduled
+    rate leaves [0, 1]; the device takes the rates from a precomputed table, so
+    the same check runs here, before generation 0, with the same message."""
+    G = int(generations)
+    for g in range(1, G + 1):
+        for name, v in (("p_dist", sch.p_dist(g, G)), ("p_sl", sch.p_sl(g, G)), ("p_flip", sch.p_flip(g, G))):
+            if not (0.0 <= v <= 1.0):
+                raise ValueError(f"{name} must be in [0, 1], got {v}")
+
+
 def _run(algorithm, objective, *, dimension, pop_size, generations, seed, de, gwo, sch, workers, bounds,
-         fitness_mode, use_graph=True) -> RunResult:
+         fitness_mode, use_graph=True, chunk_size=None) -> RunResult:
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
+    if chunk_size is not None and chunk_size < 1:  # parexec.BatchJob (parexec.py:69-70)
+        raise ValueError(f"chunk_size must be >= 1, got {chunk_size}")
+    if algorithm == "hybrid":
+        _check_wolf_rates(sch, generations)
     if pop_size < 4:
         raise ValueError(f"population size must be >= 4, got {pop_size}")
     if dimension < 1:
@@ -365,7 +386,8 @@ def run_hybrid(objective, *, dimension: int, pop_size: int, generations: int, se
     gwo = replace(gwo_params) if gwo_params else GWOParams()
     sch = replace(schedules) if schedules else Schedules()
     return _run("hybrid", objective, dimension=dimension, pop_size=pop_size, generations=generations, seed=seed,
-                de=de, gwo=gwo, sch=sch, workers=workers, bounds=(de.x_min, de.x_max), fitness_mode=fitness_mode)
+                de=de, gwo=gwo, sch=sch, workers=workers, bounds=(de.x_min, de.x_max), fitness_mode=fitness_mode,
+                chunk_size=chunk_size)
 
 
 def run_de(objective, *, dimension: int, pop_size: int, generations: int, seed: int,
@@ -375,7 +397,7 @@ def run_de(objective, *, dimension: int, pop_size: int, generations: int, seed: 
     sch = replace(schedules) if schedules else Schedules()
     return _run("de", objective, dimension=dimension, pop_size=pop_size, generations=generations, seed=seed,
                 de=de, gwo=GWOParams(), sch=sch, workers=workers, bounds=(de.x_min, de.x_max),
-                fitness_mode=fitness_mode)
+                fitness_mode=fitness_mode, chunk_size=chunk_size)
 
 
 def run_gwo(objective, *, dimension: int, pop_size: int, generations: int, seed: int,
@@ -384,7 +406,7 @@ def run_gwo(objective, *, dimension: int, pop_size: int, generations: int, seed:
     gwo = replace(gwo_params) if gwo_params else GWOParams()
     return _run("gwo", objective, dimension=dimension, pop_size=pop_size, generations=generations, seed=seed,
                 de=DEParams(), gwo=gwo, sch=Schedules(), workers=workers, bounds=bounds,
-                fitness_mode=fitness_mode)
+                fitness_mode=fitness_mode, chunk_size=chunk_size)
 
 
 def run(algorithm: str, objective, *, dimension: int, pop_size: int, generations: int, seed: int,
