@@ -235,6 +235,8 @@ def test_graph_and_eager_identical(q):
     for use_graph in (True, False):
         eng = q.Engine(obj, "hybrid", pop_size=37, generations=30, seed=3, de=de, gwo=gwo, sch=sch)
         eng.init()
+        if use_graph:
+            eng.prepare(13)
         eng.step(13, use_graph=use_graph)
         eng.step(17, use_graph=use_graph)
         eng.finalize()

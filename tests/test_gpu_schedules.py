@@ -25,7 +25,7 @@ def q():
     return pkg
 
 
-def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders=4, mode="fast"):
+def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders=4, mode="fast", graph=True):
     for k in KNOBS:
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
@@ -34,6 +34,8 @@ def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders
     eng = q.Engine(obj, algorithm, pop_size=NP, generations=G, seed=3, de=q.DEParams(),
                    gwo=q.GWOParams(leader_count=leaders), sch=q.Schedules(phase_split=0.5))
     eng.init()
+    if graph:  # short runs launch eagerly unless the graphs are prepared
+        eng.prepare(G)
     eng.step(G)
     eng.finalize()
     return eng.trace(), eng.population()[0]
@@ -68,6 +70,15 @@ def test_schedule_knobs_do_not_change_the_trace(q, monkeypatch, env, leaders):
     assert np.array_equal(got_p, want_p)
 
 
+@pytest.mark.parametrize("algorithm", ["hybrid", "de", "gwo"])
+def test_eager_launches_equal_graph_replays(q, monkeypatch, algorithm):
+    """A fresh engine runs short steps with eager launches: same trace as the graphs."""
+    want_t, want_p = _trace(q, monkeypatch, {}, algorithm=algorithm, graph=True)
+    got_t, got_p = _trace(q, monkeypatch, {}, algorithm=algorithm, graph=False)
+    assert np.array_equal(got_t, want_t)
+    assert np.array_equal(got_p, want_p)
+
+
 def test_schedule_knobs_exact_mode_de(q, monkeypatch):
     want_t, _ = _trace(q, monkeypatch, {}, algorithm="de", mode="exact")
     got_t, _ = _trace(q, monkeypatch, {"QPM_PDL": "0", "QPM_PLAN_FORK": "trial"}, algorithm="de", mode="exact")
@@ -86,6 +97,7 @@ def test_repeated_runs_are_identical(q, monkeypatch):
         eng = q.Engine(obj, "hybrid", pop_size=512, generations=200, seed=9, de=q.DEParams(), gwo=q.GWOParams(),
                        sch=q.Schedules())
         eng.init()
+        eng.prepare(200)
         eng.step(200)
         traces.append(eng.trace())
         del eng

@@ -116,5 +116,6 @@ def test_one_rank_nccl_communicator_in_graph(q, algorithm):
     ref.step(12)
     eng = ShardedEngine.create(obj, algorithm, rank=0, world=1, nccl_id=nccl_unique_id(), **kw)
     eng.init()
+    eng.prepare(12)  # the allgather captured in the generation graphs
     eng.step(12, use_graph=True)
     assert np.array_equal(eng.trace(), ref.trace())
