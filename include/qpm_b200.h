@@ -232,6 +232,24 @@ int qpm_engine_init_finish(qpm_engine *e);
 /* emulated exchange before a phase (or before qpm_engine_init_finish): copy
  * src's segment partials into dst (synchronous) */
 int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase);
+/* Host-staged exchange (the sharded protocol across a process boundary
+ * without NCCL, e.g. over a torch.distributed gloo group; tests use it to
+ * run real shard engines in separate processes on one GPU): after a phase,
+ * read this rank's partial slot to the host, all-gather the slots, write
+ * every peer's slot back, then run the next phase (or qpm_engine_init_finish).
+ * slot_doubles: doubles per rank slot.  All three are synchronous. */
+int qpm_engine_partials_info(const qpm_engine *e, int64_t *slot_doubles, int *world, int *rank);
+int qpm_engine_partials_read(qpm_engine *e, double *host_out);
+int qpm_engine_partials_write(qpm_engine *e, int rank, const double *host_in);
+/* Wait for the engine's queued work with failure detection: polls the stream
+ * and ncclCommGetAsyncError; an asynchronous NCCL error, or no progress
+ * within timeout_ms (< 0: no limit), aborts the communicator
+ * (ncclCommAbort) and returns QPM_ERR_NCCL -- a peer that died or hangs
+ * cannot block this rank forever.  qpm_engine_step also polls the error
+ * state between graph launches.  After QPM_ERR_NCCL the engine refuses
+ * further steps.  Replaces the reference's BatchEvaluationError failure
+ * contract (parexec.py:27-33) on the multi-GPU path. */
+int qpm_engine_wait(qpm_engine *e, int64_t timeout_ms);
 int qpm_engine_cand_ptr(qpm_engine *e, double **cand_dev);
 int qpm_engine_stream(qpm_engine *e, void **stream);
 

@@ -28,7 +28,8 @@ EXPORTS = (
     "qpm_engine_fitness_ptr", "qpm_nccl_unique_id", "qpm_engine_set_comm", "qpm_engine_columns",
     "qpm_engine_init_finish",
     "qpm_engine_phases", "qpm_engine_run_phase", "qpm_engine_exchange_from", "qpm_engine_cand_ptr",
-    "qpm_engine_stream",
+    "qpm_engine_stream", "qpm_engine_partials_info", "qpm_engine_partials_read", "qpm_engine_partials_write",
+    "qpm_engine_wait",
 )
 
 
@@ -123,6 +124,10 @@ def lib():
         "qpm_engine_exchange_from": (I32, [P, P, I32]),
         "qpm_engine_cand_ptr": (I32, [P, P]),
         "qpm_engine_stream": (I32, [P, P]),
+        "qpm_engine_partials_info": (I32, [P, P, P, P]),
+        "qpm_engine_partials_read": (I32, [P, P]),
+        "qpm_engine_partials_write": (I32, [P, I32, P]),
+        "qpm_engine_wait": (I32, [P, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -46,8 +46,10 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "qpm_common.cuh"
@@ -1672,6 +1674,7 @@ struct Engine {
     bool initialized = false;
     bool init_pending = false;  // emulated shard: fitness scan of generation 0 done, exchange pending
     bool owns_stream = false;
+    bool failed = false;  // a collective failed or timed out: the communicator was aborted
     int64_t device_bytes = 0;
     std::vector<std::pair<void *, size_t>> allocs;
 };
@@ -1836,6 +1839,8 @@ typedef int (*nccl_init_rank_fn)(void **, int, ncclUniqueIdPod, int);
 typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
 typedef int (*nccl_destroy_fn)(void *);
 typedef const char *(*nccl_err_fn)(int);
+typedef int (*nccl_async_err_fn)(void *, int *);
+typedef int (*nccl_abort_fn)(void *);
 struct NcclApi {
     bool loaded = false;
     nccl_get_id_fn get_id = nullptr;
@@ -1843,7 +1848,10 @@ struct NcclApi {
     nccl_allgather_fn allgather = nullptr;
     nccl_destroy_fn destroy = nullptr;
     nccl_err_fn err = nullptr;
+    nccl_async_err_fn async_err = nullptr;  // ncclCommGetAsyncError
+    nccl_abort_fn abort = nullptr;          // ncclCommAbort
 };
+constexpr int kNcclSuccess = 0, kNcclInProgress = 7;  // ncclResult_t (nccl.h)
 static NcclApi g_nccl;
 constexpr int kNcclFloat64 = 8;  // ncclFloat64 in nccl.h
 constexpr int kNcclUint8 = 1;    // ncclUint8
@@ -1860,7 +1868,10 @@ static int nccl_load() {
     g_nccl.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
     g_nccl.destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
     g_nccl.err = (nccl_err_fn)dlsym(h, "ncclGetErrorString");
-    if (!g_nccl.get_id || !g_nccl.init_rank || !g_nccl.allgather || !g_nccl.destroy || !g_nccl.err) {
+    g_nccl.async_err = (nccl_async_err_fn)dlsym(h, "ncclCommGetAsyncError");
+    g_nccl.abort = (nccl_abort_fn)dlsym(h, "ncclCommAbort");
+    if (!g_nccl.get_id || !g_nccl.init_rank || !g_nccl.allgather || !g_nccl.destroy || !g_nccl.err ||
+        !g_nccl.async_err || !g_nccl.abort) {
         set_error("libnccl.so.2 lacks a required symbol");
         return QPM_ERR_NCCL;
     }
@@ -1878,6 +1889,27 @@ static int enqueue_exchange(Engine *e, int phase) {
     const int r = g_nccl.allgather(e->gpart + e->rank * n, e->gpart, n, kNcclFloat64, e->comm, e->stream);
     if (r != 0) {
         set_error("ncclAllGather: %s", g_nccl.err(r));
+        return QPM_ERR_NCCL;
+    }
+    return QPM_OK;
+}
+
+// Failure detection for the collective path (the reference's failure
+// contract is an exception, parexec.py:27-33; a hung or failed collective
+// inside a replayed graph would otherwise block every later synchronize).
+// An asynchronous NCCL error aborts the communicator and surfaces as
+// QPM_ERR_NCCL; the engine is unusable afterwards.
+static int nccl_poll(Engine *e) {
+    if (!e->comm) return QPM_OK;
+    int aerr = kNcclSuccess;
+    const int r = g_nccl.async_err(e->comm, &aerr);
+    if (r != kNcclSuccess || (aerr != kNcclSuccess && aerr != kNcclInProgress)) {
+        const int code = r != kNcclSuccess ? r : aerr;
+        set_error("NCCL asynchronous error on rank %d of %d: %s (communicator aborted)", e->rank, e->world,
+                  g_nccl.err(code));
+        g_nccl.abort(e->comm);
+        e->comm = nullptr;
+        e->failed = true;
         return QPM_ERR_NCCL;
     }
     return QPM_OK;
@@ -2510,6 +2542,10 @@ static int ensure_graphs(Engine *e, int64_t n) {
 }
 
 static int step_ready(Engine *e, const char *what) {
+    if (e->failed) {
+        set_error("%s: the engine's collective failed earlier (communicator aborted); create a new engine", what);
+        return QPM_ERR_NCCL;
+    }
     if (!e->initialized) {
         set_error("%s before qpm_engine_init", what);
         return QPM_ERR_STATE;
@@ -2551,14 +2587,21 @@ int qpm_engine_step(qpm_engine *h, int64_t n, int use_graph) {
         if ((rc0 = ensure_graphs(e, n))) return rc0;
         int64_t t = 0;
         if (e->graph_gens > 1 && n >= e->graph_gens)
-            for (; t + e->graph_gens <= n; t += e->graph_gens) QPM_CUDA_TRY(cudaGraphLaunch(e->exec_k, e->stream));
-        for (; t < n; ++t) QPM_CUDA_TRY(cudaGraphLaunch(e->exec, e->stream));
+            for (; t + e->graph_gens <= n; t += e->graph_gens) {
+                QPM_CUDA_TRY(cudaGraphLaunch(e->exec_k, e->stream));
+                if ((rc0 = nccl_poll(e))) return rc0;
+            }
+        for (; t < n; ++t) {
+            QPM_CUDA_TRY(cudaGraphLaunch(e->exec, e->stream));
+            if ((rc0 = nccl_poll(e))) return rc0;
+        }
     } else {
         for (int64_t t = 0; t < n; ++t) {
             int launches = 0;
             int rc = enqueue_generation(e, &launches);
             if (rc) return rc;
             e->launches = launches;
+            if ((rc = nccl_poll(e))) return rc;
         }
     }
     e->g_done += n;
@@ -2771,6 +2814,77 @@ int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase) {
     QPM_CUDA_TRY(cudaMemcpyAsync(d->gpart + s->rank * n, s->gpart + s->rank * n, sizeof(double) * n,
                                  cudaMemcpyDeviceToDevice, d->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(d->stream));
+    return QPM_OK;
+}
+
+int qpm_engine_wait(qpm_engine *h, int64_t timeout_ms) {
+    QPM_ARG_CHECK(h, "engine");
+    Engine *e = h->e;
+    if (e->failed) {
+        set_error("qpm_engine_wait: the engine's collective failed earlier (communicator aborted)");
+        return QPM_ERR_NCCL;
+    }
+    // poll the stream and, on the collective path, NCCL's asynchronous error
+    // state; on timeout abort the communicator so the stuck kernels exit
+    // instead of hanging every later synchronize
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(e->stream);
+        if (q == cudaSuccess) return nccl_poll(e);
+        if (q != cudaErrorNotReady) {
+            set_error("qpm_engine_wait: %s", cudaGetErrorString(q));
+            return QPM_ERR_CUDA;
+        }
+        int rc;
+        if ((rc = nccl_poll(e))) return rc;
+        const auto ms =
+            std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (timeout_ms >= 0 && ms > timeout_ms) {
+            if (e->comm) {
+                g_nccl.abort(e->comm);
+                e->comm = nullptr;
+                e->failed = true;
+                set_error("qpm_engine_wait: rank %d of %d timed out after %lld ms waiting for the generation "
+                          "(a peer stopped participating in the collective); communicator aborted",
+                          e->rank, e->world, (long long)ms);
+                return QPM_ERR_NCCL;
+            }
+            set_error("qpm_engine_wait: timed out after %lld ms", (long long)ms);
+            return QPM_ERR_STATE;
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+}
+
+int qpm_engine_partials_info(const qpm_engine *h, int64_t *slot_doubles, int *world, int *rank) {
+    QPM_ARG_CHECK(h, "engine");
+    const Engine *e = h->e;
+    if (slot_doubles) *slot_doubles = e->gpart ? (int64_t)gpart_slot(e) : 0;
+    if (world) *world = e->world;
+    if (rank) *rank = e->rank;
+    return QPM_OK;
+}
+
+int qpm_engine_partials_read(qpm_engine *h, double *host_out) {
+    QPM_ARG_CHECK(h && host_out, "engine, out");
+    Engine *e = h->e;
+    QPM_ARG_CHECK(e->gpart != nullptr, "not a sharded engine");
+    const size_t n = gpart_slot(e);
+    QPM_CUDA_TRY(cudaMemcpyAsync(host_out, e->gpart + e->rank * n, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                 e->stream));
+    QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return QPM_OK;
+}
+
+int qpm_engine_partials_write(qpm_engine *h, int rank, const double *host_in) {
+    QPM_ARG_CHECK(h && host_in, "engine, in");
+    Engine *e = h->e;
+    QPM_ARG_CHECK(e->gpart != nullptr, "not a sharded engine");
+    QPM_ARG_CHECK(rank >= 0 && rank < e->world && rank != e->rank, "a peer rank of this engine's run");
+    const size_t n = gpart_slot(e);
+    QPM_CUDA_TRY(cudaMemcpyAsync(e->gpart + rank * n, host_in, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                 e->stream));
+    QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
     return QPM_OK;
 }
 

@@ -106,6 +106,31 @@ class ShardedEngine(Engine):
         _native.check(_native.lib().qpm_engine_exchange_from(self.handle, other.handle, int(phase)),
                       "qpm_engine_exchange_from")
 
+    def wait(self, timeout_s: float | None = None):
+        """Block until the queued generations finish, with failure detection
+        (qpm_engine_wait): an NCCL asynchronous error, or no completion within
+        timeout_s, aborts the communicator and raises QpmError."""
+        ms = -1 if timeout_s is None else int(timeout_s * 1e3)
+        _native.check(_native.lib().qpm_engine_wait(self.handle, ms), "qpm_engine_wait")
+
+    def partials_slot(self) -> int:
+        n = ctypes.c_int64()
+        _native.check(_native.lib().qpm_engine_partials_info(self.handle, ctypes.byref(n), None, None),
+                      "qpm_engine_partials_info")
+        return int(n.value)
+
+    def partials_read(self) -> np.ndarray:
+        out = np.empty(self.partials_slot(), dtype=np.float64)
+        _native.check(_native.lib().qpm_engine_partials_read(self.handle, out.ctypes.data), "qpm_engine_partials_read")
+        return out
+
+    def partials_write(self, rank: int, slot: np.ndarray):
+        slot = np.ascontiguousarray(slot, dtype=np.float64)
+        if slot.size != self.partials_slot():
+            raise ValueError(f"slot has {slot.size} doubles, the engine's is {self.partials_slot()}")
+        _native.check(_native.lib().qpm_engine_partials_write(self.handle, int(rank), slot.ctypes.data),
+                      "qpm_engine_partials_write")
+
     def best_columns(self) -> tuple[int, Individual]:
         """(g0, this shard's columns of the final best individual)."""
         return self.g0, Engine.best(self)
@@ -181,10 +206,71 @@ class EmulatedShards:
         return genome, parts[0][1][1]
 
 
+class HostExchangeShard:
+    """This process's shard engine of a column-sharded run whose exchanges
+    go through host memory and a torch.distributed group of any backend
+    (gloo on CPU) instead of the in-graph ncclAllGather.
+
+    The kernels are the real shard engine's; only the transport differs: after
+    each phase the rank's partial slot is read to the host, all-gathered over
+    the group and the peers' slots written back (qpm_engine_partials_*).  It
+    is how the sharded protocol is exercised across a process boundary on a
+    single GPU (NCCL cannot place two ranks on one device), and a slow but
+    working path for hosts without NCCL peers.
+    """
+
+    def __init__(self, objective, algorithm, *, group=None, **kw):
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.engine = ShardedEngine.create(objective, algorithm, rank=self.rank, world=self.world, nccl_id=None,
+                                           **kw)
+        self.D = objective.dimension
+        self.exchanged_bytes = 0
+
+    def _exchange(self):
+        import torch
+        import torch.distributed as dist
+
+        mine = torch.from_numpy(self.engine.partials_read())
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(parts, mine, group=self.group)
+        for r, p in enumerate(parts):
+            if r != self.rank:
+                self.engine.partials_write(r, p.numpy())
+        self.exchanged_bytes += mine.numel() * 8 * self.world
+
+    def init(self):
+        self.engine.init()
+        self._exchange()
+        self.engine.init_finish()
+
+    def step(self, n: int):
+        for _ in range(n):
+            for ph in range(self.engine.phases):
+                if ph > 0:
+                    self._exchange()
+                self.engine.run_phase(ph)
+
+    def finalize(self):
+        self.engine.finalize()
+
+    def trace(self):
+        return self.engine.trace()
+
+    def best(self) -> Individual:
+        import torch.distributed as dist
+
+        parts = [None] * self.world
+        dist.all_gather_object(parts, self.engine.best_columns(), group=self.group)
+        return assemble_best(parts, self.D)
+
+
 def run_sharded(algorithm: str, objective, *, dimension: int, pop_size: int, generations: int, seed: int,
                 de_params: DEParams | None = None, gwo_params: GWOParams | None = None,
                 schedules: Schedules | None = None, fitness_mode: str | None = None, group=None,
-                use_graph: bool = True) -> RunResult:
+                use_graph: bool = True, timeout_s: float | None = 600.0) -> RunResult:
     """The run on all ranks of `group` (torch.distributed, NCCL); every rank returns the same result."""
     import torch.distributed as dist
 
@@ -202,6 +288,7 @@ def run_sharded(algorithm: str, objective, *, dimension: int, pop_size: int, gen
     eng.init()
     eng.step(generations, use_graph=use_graph)
     eng.finalize()
+    eng.wait(timeout_s)  # failure detection: a dead or stuck peer raises instead of hanging
     part = eng.best_columns()
     if world > 1:
         parts = [None] * world
