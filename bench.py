@@ -121,16 +121,16 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_objective(q, mode="fast"):
+def build_objective(q, mode="fast", seg_chunks=None):
     spec = q.ObjectiveSpec("single_thg", (PUMP_NM,))
-    return q.make_objective(spec, q.default_dispersion(25.0), THICKNESS_UM, D, mode=mode)
+    return q.make_objective(spec, q.default_dispersion(25.0), THICKNESS_UM, D, mode=mode, seg_chunks=seg_chunks)
 
 
 def evals_per_generation(k=4):
     return (2 * NP - k) * D
 
 
-def cpu_baseline(threads: int = 0, target_s: float = 12.0):
+def cpu_baseline(threads: int = 0, target_s: float = 12.0, with_reference_package: bool = True):
     """The CPU oracle port on this host: bounded sample of C2 generations."""
     from oracle import oracle as O
     from paper_2511_01255_b200 import tables as T
@@ -148,9 +148,49 @@ def cpu_baseline(threads: int = 0, target_s: float = 12.0):
     O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=gens)
     dt = time.perf_counter() - t0 - t_init
     cores = threads if threads > 0 else O.max_threads()
-    return {"value": evals_per_generation() * gens / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle/qpm_oracle.c run_hybrid C2 generations 1..{gens} of a {G_RUN}-generation run "
-                      f"(init excluded), {cores} pthreads", "seconds": dt}
+    out = {"value": evals_per_generation() * gens / dt, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"oracle/qpm_oracle.c run_hybrid C2 generations 1..{gens} of a {G_RUN}-generation run "
+                     f"(init excluded), {cores} pthreads", "seconds": dt}
+    out.update(host_info())
+    if with_reference_package:
+        out["reference_package_context"] = reference_package_timing()
+    return out
+
+
+def host_info():
+    """CPU model and how the oracle port was compiled (context for cpu_baseline)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    flags = "unknown"
+    try:
+        for line in open(os.path.join(ROOT, "oracle", "Makefile")):
+            if line.startswith("CFLAGS"):
+                flags = line.split("=", 1)[1].strip()
+    except OSError:
+        pass
+    try:
+        cc = subprocess.run(["gcc", "--version"], capture_output=True, text=True, timeout=10).stdout.splitlines()[0]
+    except Exception:
+        cc = "gcc (version unknown)"
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "compiler": f"{cc}; CFLAGS {flags}"}
+
+
+def reference_package_timing(gens: int = 2):
+    """The reference package itself (qpmdesign run_hybrid, numba, all host cores)
+    on a truncated C2 window (tools/ref_timing.py): how the port compares with
+    the real reference on this host.  Context only; the port is the arm."""
+    try:
+        res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ref_timing.py"), "--gens", str(gens)],
+                             capture_output=True, text=True, timeout=240)
+        return json.loads(res.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # the context number is optional
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
 
 
 def run_reference(args):
@@ -185,7 +225,7 @@ def run_reference(args):
             "config": {"workload": "C2 run_hybrid NP=1024 D=10000 THG 1404nm t=1um, 1000 generations",
                        "NP": NP, "D": D, "generations": G, "timed_generations": [args.warmup + 1,
                                                                                args.warmup + args.steps]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_baseline": {**host_info(), "value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"oracle/qpm_oracle.c (C restatement of qpmdesign run_hybrid, pinned "
                                        f"bit-exact to the reference) generations {args.warmup + 1}.."
                                        f"{args.warmup + args.steps}, {cores} pthreads"},
@@ -301,15 +341,13 @@ def run_ours(args):
     import paper_2511_01255_b200 as q
     from paper_2511_01255_b200.distributed import ShardedEngine, broadcast_unique_id, run_sharded
 
-    if world > 1:
-        # fitness segments of 2 chunks: C2's 40 segments split evenly over 2, 4
-        # and 8 GPUs (the one-GPU default, 3, leaves 27); set before the
-        # objective is created, on every rank
-        os.environ.setdefault("QPM_SEG_CHUNKS", "2")
     dev = torch.device("cuda", torch.cuda.current_device())
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     peaks, peaks_kind = measured_peaks()
-    obj = build_objective(q)
+    # multi-GPU: fitness segments of 2 chunks, C2's 40 segments = 8 stitch
+    # super-blocks of 5 that split evenly over 2, 4 and 8 GPUs (the one-GPU
+    # default, 3 chunks, gives 27 = super-blocks of 3 or 4)
+    obj = build_objective(q, seg_chunks=2 if world > 1 else None)
     de, gwo, sch = q.DEParams(), q.GWOParams(), q.Schedules()
     G = max(G_RUN, args.warmup + args.steps)
     np_total = NP * world  # weak scaling: 1,024 rows per GPU
@@ -432,9 +470,10 @@ def run_ours(args):
                                        f"(NP={np_total}), {G} generations",
                            "NP": np_total, "D": D, "generations": G, "fitness_mode": "fast",
                            "timed_generations": [args.warmup + 1, args.warmup + args.steps],
-                           "parallelism": (f"column-sharded x{world}: each GPU owns the genes under 1/{world} of "
-                                           f"the fitness segments (2-chunk segments) for all rows; NCCL all-gather "
-                                           f"of the segment partials twice per generation, replicated selection")
+                           "parallelism": (f"column-sharded x{world}: each GPU owns the genes under 8/{world} of the 8 "
+                                           f"fitness stitch super-blocks (2-chunk segments) for all rows; in-graph "
+                                           f"NCCL all-gather of the pre-stitched super-block partials (NP x 8 x 48 B) "
+                                           f"twice per generation, replicated selection")
                            if world > 1 else "1 GPU",
                            "l2": "genome pool 2 x NP x D f64 (164 MB per 1,024 rows) > 126 MB L2; no flush"},
                 "generations_per_s": 1e3 / ms_gen, "best_after_timed": best_after,

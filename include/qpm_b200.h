@@ -98,13 +98,21 @@ typedef struct qpm_problem qpm_problem;
  *   e1[n_wl][D][2], b[n_wl][D][2] (THG only, else NULL),
  *   w[n_wl][2] (w12 for THG, w1 for SHG), hconst[n_wl][2] (THG, else NULL).
  * scale: divisor applied to |d_eff| (L or L^2/2), 1.0 for raw.
- * multi: 1 for the multi-wavelength objective -(sum|g0-g| + beta(max-min)). */
+ * multi: 1 for the multi-wavelength objective -(sum|g0-g| + beta(max-min)).
+ * seg_chunks: fast-scan segment length in 128-domain chunks, 0 = the
+ * default for D and n_wl.  It fixes the fitness stitch tree (S segments in
+ * min(8, S) super-blocks), so fast-mode values depend on it (at the 1e-15
+ * level) and on nothing else -- not the batch, not the GPU count.  A
+ * multi-GPU run of W ranks needs min(8, S) >= W. */
 int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int64_t D, const double *e1,
                        const double *b, const double *w, const double *hconst, double scale, double g0,
-                       double beta);
+                       double beta, int seg_chunks);
 int qpm_problem_destroy(qpm_problem *p);
 /* u32 words per bit-packed row (domains padded to a multiple of 128) */
 int64_t qpm_problem_row_words(const qpm_problem *p);
+/* the fast scan's segment length (chunks), segment count S and stitch
+ * super-block count min(8, S) */
+int qpm_problem_layout(const qpm_problem *p, int *seg_chunks, int *segments, int *super_blocks);
 
 /* pack int8 +/-1 rows [rows][D] into bit rows (bit 1 = -1) of stride row_words */
 int qpm_pack_signs(const int8_t *signs_dev, int64_t rows, int64_t D, uint32_t *bits_dev, int64_t row_words,
@@ -208,15 +216,17 @@ int qpm_engine_read_best(qpm_engine *e, double *genome, int8_t *proj, double *fi
 int qpm_engine_read_population(qpm_engine *e, double *genome, double *fitness);
 /* ------------------------------------------------------------ multi-GPU
  * One process per GPU; the genes are sharded in contiguous column ranges
- * aligned to the fitness segments (qpm_run_params.shard_rank/shard_world).
- * Every rank runs the per-gene work (DE trials, wolf moves, draws, fitness
- * segment scans) on its columns of all NP individuals; after each fitness
- * scan the segment partials (NP x 48 B per segment) are all-gathered over
- * NCCL and every rank stitches and scores all rows, so selection, leaders,
- * statistics and the F update run replicated on identical data.  Fitness
- * segments are the single-GPU ones, so a sharded run is bit-identical to
- * the same run on one GPU (fast mode).  Replaces the reference's in-process
- * thread pool (parexec.py:73-120). */
+ * aligned to the fitness stitch super-blocks (qpm_run_params.shard_rank /
+ * shard_world): rank k of W owns super-blocks [floor(k B / W),
+ * floor((k+1) B / W)), B = min(8, S).  Every rank runs the per-gene work (DE
+ * trials, wolf moves, draws, fitness segment scans) on its columns of all NP
+ * individuals and pre-stitches its super-blocks; those partials (NP x 48 B
+ * per owned super-block and wavelength) are all-gathered over NCCL inside
+ * the generation graph and every rank finishes and scores all rows, so
+ * selection, leaders, statistics and the F update run replicated on
+ * identical data.  The stitch tree is the single-GPU one, so a sharded run
+ * is bit-identical to the same run on one GPU (fast mode).  Replaces the
+ * reference's in-process thread pool (parexec.py:73-120). */
 /* rank 0 creates the NCCL id (128 bytes) and broadcasts it to the others */
 int qpm_nccl_unique_id(uint8_t *id_out);
 /* before qpm_engine_init; rank / world must match the engine's shard */
@@ -230,7 +240,7 @@ int qpm_engine_run_phase(qpm_engine *e, int phase);
  * the generation-0 fitness scan; exchange, then qpm_engine_init_finish */
 int qpm_engine_init_finish(qpm_engine *e);
 /* emulated exchange before a phase (or before qpm_engine_init_finish): copy
- * src's segment partials into dst (synchronous) */
+ * src's super-block partial slot into dst (synchronous) */
 int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase);
 /* Host-staged exchange (the sharded protocol across a process boundary
  * without NCCL, e.g. over a torch.distributed gloo group; tests use it to

@@ -20,7 +20,7 @@ SCHED_COLS = 8
 # every symbol include/qpm_b200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
     "qpm_last_error", "qpm_version", "qpm_device_info", "qpm_release_cached_memory", "qpm_fold_key", "qpm_uniform_fill",
-    "qpm_problem_create", "qpm_problem_destroy", "qpm_problem_row_words", "qpm_pack_signs",
+    "qpm_problem_create", "qpm_problem_destroy", "qpm_problem_row_words", "qpm_problem_layout", "qpm_pack_signs",
     "qpm_fitness_bits", "qpm_evaluate_block_host", "qpm_sum_block_host", "qpm_reduce_best", "qpm_brute_force", "qpm_sweep_spectrum",
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
     "qpm_engine_step", "qpm_engine_prepare", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
@@ -91,7 +91,8 @@ def lib():
         "qpm_device_info": (I32, [P, P, P]),
         "qpm_fold_key": (ctypes.c_uint64, [I64, I32, P]),
         "qpm_uniform_fill": (I32, [ctypes.c_uint64, ctypes.c_uint64, I64, P, P]),
-        "qpm_problem_create": (I32, [P, I32, I32, I32, I64, P, P, P, P, D, D, D]),
+        "qpm_problem_create": (I32, [P, I32, I32, I32, I64, P, P, P, P, D, D, D, I32]),
+        "qpm_problem_layout": (I32, [P, P, P, P]),
         "qpm_problem_destroy": (I32, [P]),
         "qpm_problem_row_words": (I64, [P]),
         "qpm_pack_signs": (I32, [P, I64, I64, P, I64, P]),

@@ -17,7 +17,7 @@
 //   sched   f64 [G+1][8]     per-generation scalars, host-computed
 //   trace   f64 [G+1][5]     (g, best, mean, F|a, pop_std)
 //   state   EngineState      g, F, window, leaders, best-ever bookkeeping
-//   gpart   f64 [W][n_wl][NP][S_slot][6]  all-gathered fitness segment
+//   gpart   f64 [W][n_wl][NP][SB_slot][6]  all-gathered fitness super-block
 //                            partials (multi-GPU)
 // Dp = W * 32 with W a multiple of 4, so rows start on 512-byte boundaries.
 //
@@ -176,26 +176,24 @@ struct GenThr {
     uint32_t pad;
 };
 
-// a genome row that is either f64 or, for wolf candidates, +/-1 bits
+// a genome row that is either f64 or, for wolf candidates, +/-1 bits (one
+// pointer and a flag: the trial kernel keeps four of these in registers)
 struct RowRef {
-    const double *f;
-    const uint32_t *b;
+    const void *p;
+    uint32_t bin;
+    __device__ __forceinline__ const double *f() const { return static_cast<const double *>(p); }
+    __device__ __forceinline__ const uint32_t *b() const { return static_cast<const uint32_t *>(p); }
     __device__ __forceinline__ double at(int j) const {
-        if (f) return f[j];
-        return ((b[j >> 5] >> (j & 31)) & 1u) ? -1.0 : 1.0;
+        if (!bin) return f()[j];
+        return ((b()[j >> 5] >> (j & 31)) & 1u) ? -1.0 : 1.0;
     }
 };
 
 __device__ __forceinline__ RowRef row_ref(const RunConsts &c, int64_t slot, const uint8_t *slot_bin,
                                           const double *genome, const uint32_t *bits) {
     RowRef r;
-    if (slot_bin[slot]) {
-        r.f = nullptr;
-        r.b = bits + slot * c.W;
-    } else {
-        r.f = genome + slot * c.Dp;
-        r.b = nullptr;
-    }
+    r.bin = slot_bin[slot] ? 1u : 0u;
+    r.p = r.bin ? static_cast<const void *>(bits + slot * c.W) : static_cast<const void *>(genome + slot * c.Dp);
     return r;
 }
 
@@ -208,13 +206,8 @@ __device__ __forceinline__ RowRef row_ref_tag(const RunConsts &c, uint32_t tag, 
                                               const uint32_t *bits) {
     const int64_t slot = (int64_t)(tag & ~kBinTag);
     RowRef r;
-    if (tag & kBinTag) {
-        r.f = nullptr;
-        r.b = bits + slot * c.W;
-    } else {
-        r.f = genome + slot * c.Dp;
-        r.b = nullptr;
-    }
+    r.bin = (tag & kBinTag) ? 1u : 0u;
+    r.p = r.bin ? static_cast<const void *>(bits + slot * c.W) : static_cast<const void *>(genome + slot * c.Dp);
     return r;
 }
 
@@ -612,7 +605,7 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
         r.x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
         r.x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
     }
-    r.bin = !r.xi.f || !r.x1.f || !r.x2.f || !r.x3.f;
+    r.bin = r.xi.bin | r.x1.bin | r.x2.bin | r.x3.bin;
     r.out_slot = a.spare_of[i];
     r.out = a.genome + r.out_slot * c.Dp;
     r.bout = a.bits + r.out_slot * c.W;
@@ -625,6 +618,9 @@ __device__ __forceinline__ void trial_row_setup(const RunConsts &c, const TrialA
 }
 
 constexpr int kDeSteps = 2;  // 64-gene warp steps per k_de_trial batch (registers)
+#ifndef QPM_TRIAL_LOADS
+#define QPM_TRIAL_LOADS 1  // f64-row trials: branch-free base-row select (1) or take-branched loads (0)
+#endif
 
 // L2 policy of the trial's genome traffic (QPM_L2_HINTS): the current
 // population (NP rows, 82 MB at C2) is read ~4 times per generation as
@@ -653,6 +649,9 @@ __device__ __forceinline__ void st_stream(double *p, double v) {
     *p = v;
 #endif
 }
+
+// +1.0 / -1.0 from a sign bit (bit 0 of b; 1 = -1): built on the high word
+__device__ __forceinline__ double pm1(uint32_t b) { return __hiloint2double((int)(0x3FF00000u | (b << 31)), 0); }
 
 // One warp's share of a row: nb batches of kDeSteps 64-gene steps, step st of
 // batch bt at genes j0 + (bt kDeSteps + st) SPAN (SPAN = 512: the eight warps of
@@ -723,21 +722,33 @@ __device__ __forceinline__ void de_trial_chunk(const RunConsts &c, const TrialAr
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int j = j64 + lane + 32 * q;
-                y[st][q] = p1[st][q] = p2[st][q] = p3[st][q] = 0.0;
+                if (!FULL || BIN || !QPM_TRIAL_LOADS) y[st][q] = p1[st][q] = p2[st][q] = p3[st][q] = 0.0;
                 if (!FULL && j >= D) continue;
-                if (BIN) {
+                if (!BIN && QPM_TRIAL_LOADS) {
+                    // f64 rows: the base (x_r1 where the mask takes the
+                    // mutant, x_i elsewhere) by a per-lane row select, and
+                    // both difference rows unconditionally -- three loads per
+                    // gene, no divergent branch; the lanes that do not take
+                    // the mutant add no DRAM sectors (their neighbours' loads
+                    // of x_r2, x_r3 already fetch them)
+                    const bool tk = (mb[st] >> q) & 1u;
+                    y[st][q] = ld_keep((tk ? x1.f() : xi.f()) + j);
+                    p1[st][q] = y[st][q];
+                    p2[st][q] = ld_keep(x2.f() + j);
+                    p3[st][q] = ld_keep(x3.f() + j);
+                } else if (BIN) {
                     // +/-1 rows: one broadcast word load per 32 genes
                     const int w = (j64 >> 5) + q;
-                    y[st][q] = xi.f ? xi.f[j] : (((xi.b[w] >> lane) & 1u) ? -1.0 : 1.0);
-                    p1[st][q] = x1.f ? x1.f[j] : (((x1.b[w] >> lane) & 1u) ? -1.0 : 1.0);
-                    p2[st][q] = x2.f ? x2.f[j] : (((x2.b[w] >> lane) & 1u) ? -1.0 : 1.0);
-                    p3[st][q] = x3.f ? x3.f[j] : (((x3.b[w] >> lane) & 1u) ? -1.0 : 1.0);
+                    y[st][q] = !xi.bin ? xi.f()[j] : pm1(xi.b()[w] >> lane);
+                    p1[st][q] = !x1.bin ? x1.f()[j] : pm1(x1.b()[w] >> lane);
+                    p2[st][q] = !x2.bin ? x2.f()[j] : pm1(x2.b()[w] >> lane);
+                    p3[st][q] = !x3.bin ? x3.f()[j] : pm1(x3.b()[w] >> lane);
                 } else if ((mb[st] >> q) & 1u) {
-                    p1[st][q] = ld_keep(x1.f + j);
-                    p2[st][q] = ld_keep(x2.f + j);
-                    p3[st][q] = ld_keep(x3.f + j);
+                    p1[st][q] = ld_keep(x1.f() + j);
+                    p2[st][q] = ld_keep(x2.f() + j);
+                    p3[st][q] = ld_keep(x3.f() + j);
                 } else {
-                    y[st][q] = ld_keep(xi.f + j);
+                    y[st][q] = ld_keep(xi.f() + j);
                 }
             }
         }
@@ -1618,13 +1629,14 @@ struct Engine {
     GenThr *gthr = nullptr;
     cudaStream_t side = nullptr;  // low-priority planner stream
     // column shard of this engine (multi-GPU): genes [c.g0, c.g0 + c.D) of
-    // every individual, the fitness segments [seg_lo, seg_lo + seg_n) of the
-    // problem; one GPU: rank 0 of 1, all of it
+    // every individual = the fitness segments [seg_lo, seg_lo + seg_n) of the
+    // problem = its stitch super-blocks owned by this rank (qpm_finish.cuh);
+    // one GPU: rank 0 of 1, all of it
     int rank = 0, world = 1;
     int seg_lo = 0, seg_n = 0;
     qpm_problem *lprob = nullptr;  // the shard's columns of the problem (world > 1, owned)
-    int S_slot = 1;                // partial slots per rank in gpart
-    double *gpart = nullptr;       // [world][n_wl][NP][S_slot][6] all-gathered segment partials (world > 1)
+    int SB_slot = 1;               // super-block partials per rank slot in gpart
+    double *gpart = nullptr;       // [world][n_wl][NP][SB_slot][6] all-gathered super-block partials (sharded)
     double *ggains = nullptr;      // [NP][n_wl] finish scratch (world > 1)
     void *comm = nullptr;          // ncclComm_t
     // the sharded flow (scan, all-gather, finish): several ranks, or one rank
@@ -1881,7 +1893,7 @@ static int nccl_load() {
 
 // exchange before phase `phase`: every rank's segment partials of the
 // candidates' fitness (its columns of every row), all-gathered into gpart
-static size_t gpart_slot(const Engine *e) { return (size_t)e->prob->n_wl * e->c.NP * e->S_slot * kPartDoubles; }
+static size_t gpart_slot(const Engine *e) { return (size_t)e->prob->n_wl * e->c.NP * e->SB_slot * kPartDoubles; }
 static int enqueue_exchange(Engine *e, int phase) {
     (void)phase;
     if (!e->comm) return QPM_OK;  // one GPU, or emulated ranks (qpm_engine_exchange_from)
@@ -1928,13 +1940,17 @@ static int fit_scan(Engine *e, const uint32_t *bits, const int32_t *row_index, d
                                        &e->S_cur);
     if (!e->sharded())
         return launch_fitness(e->prob, &e->fs, bits, c.W, row_index, c.NP, out, e->P.fitness_mode, s, n, e->pdl);
-    return launch_fitness_scan(e->lprob ? &e->lprob->p : e->prob, bits, c.W, row_index, c.NP,
-                               e->gpart + e->rank * gpart_slot(e), e->S_slot, s, n, e->pdl);
+    // a column shard: scan its segments, then pre-stitch its super-blocks
+    // into its slot of the all-gather buffer
+    const Problem *lp = e->lprob ? &e->lprob->p : e->prob;
+    int rc = launch_fitness_scan(lp, bits, c.W, row_index, c.NP, e->fs.part, lp->S, s, n, e->pdl);
+    if (rc) return rc;
+    return launch_prestitch(e->prob, e->fs.part, lp->S, e->seg_lo, e->rank, e->world, e->SB_slot, c.NP,
+                            e->gpart + e->rank * gpart_slot(e), s, n, e->pdl);
 }
 static FinishArgs fused_finish_args(const Engine *e) {
-    if (e->sharded())
-        return finish_args(e->prob, e->gpart, e->prob->S, e->world, e->S_slot, e->c.NP, e->ggains);
-    return finish_args(e->prob, e->fs.part, e->S_cur, 1, e->S_cur, e->c.NP, e->fs.gains);
+    if (e->sharded()) return finish_args_pre(e->prob, e->gpart, e->world, e->SB_slot, e->c.NP, e->ggains);
+    return finish_args(e->prob, e->fs.part, e->S_cur, e->c.NP, e->fs.gains);
 }
 static int launch_finish_select(Engine *e, int mode, cudaStream_t s) {
     const RunConsts &c = e->c;
@@ -1954,8 +1970,8 @@ static int launch_finish_select(Engine *e, int mode, cudaStream_t s) {
 }
 static int fit_finish(Engine *e, double *out, cudaStream_t s, int *n) {
     if (!e->sharded()) return QPM_OK;
-    return launch_fitness_finish(e->prob, e->gpart, e->prob->S, e->world, e->S_slot, e->c.NP, e->ggains, out, s, n,
-                                 e->pdl);
+    return launch_fitness_finish(finish_args_pre(e->prob, e->gpart, e->world, e->SB_slot, e->c.NP, e->ggains), out, s,
+                                 n, e->pdl);
 }
 
 static int phase_count(const Engine *e) { return e->c.algorithm == QPM_ALGO_HYBRID ? 3 : 2; }
@@ -2165,9 +2181,9 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     if (P->shard_world > 1) {
         QPM_ARG_CHECK(P->fitness_mode == QPM_MODE_FAST,
                       "multi-GPU runs score in fast mode (exact mode is the single-GPU parity tool)");
-        QPM_ARG_CHECK(gp.S >= P->shard_world,
-                      "fewer fitness segments than ranks: D is too small for this many GPUs "
-                      "(QPM_SEG_CHUNKS can shorten the segments)");
+        QPM_ARG_CHECK(gp.nsb >= P->shard_world,
+                      "fewer fitness super-blocks than ranks: D is too small for this many GPUs "
+                      "(a shorter seg_chunks at qpm_problem_create gives more segments)");
     }
     Engine *e = new Engine();
     e->prob = &prob->p;
@@ -2204,12 +2220,14 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     c.NP = P->NP;
     c.Dg = gp.D;
     if (e->world > 1) {
-        // rank k owns the fitness segments [floor(k S / W), floor((k+1) S / W))
-        // and the genes under them (segment boundaries are 128-domain aligned)
-        e->seg_lo = (int)((int64_t)e->rank * gp.S / e->world);
-        const int seg_hi = (int)((int64_t)(e->rank + 1) * gp.S / e->world);
+        // rank k owns the stitch super-blocks [floor(k nsb / W), floor((k+1)
+        // nsb / W)), i.e. a contiguous run of fitness segments, and the genes
+        // under them (segment boundaries are 128-domain aligned)
+        const int sb0 = sb_first(e->rank, gp.nsb, e->world), sb1 = sb_first(e->rank + 1, gp.nsb, e->world);
+        e->seg_lo = sb_lo(sb0, gp.S, gp.nsb);
+        const int seg_hi = sb_lo(sb1, gp.S, gp.nsb);
         e->seg_n = seg_hi - e->seg_lo;
-        e->S_slot = (gp.S + e->world - 1) / e->world;
+        e->SB_slot = (gp.nsb + e->world - 1) / e->world;
         const int64_t seg_len = (int64_t)gp.seg_chunks * 128;
         c.g0 = e->seg_lo * seg_len;
         const int64_t g1 = std::min<int64_t>(gp.D, seg_hi * seg_len);
@@ -2222,7 +2240,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         c.W = e->lprob->p.W;
     } else {
         e->seg_n = gp.S;
-        e->S_slot = gp.S;
+        e->SB_slot = gp.nsb;  // (used when a 1-rank communicator makes the engine take the sharded flow)
         c.g0 = 0;
         c.D = gp.D;
         c.W = gp.W;
@@ -2259,17 +2277,18 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         e->plan_grid = sms * 2;
         if (const char *v = getenv("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
-        if (const char *v = getenv("QPM_PLAN_FORK")) e->plan_after_trial = strcmp(v, "trial") == 0;
+        const char *fork = getenv("QPM_PLAN_FORK");
+        if (fork) e->plan_after_trial = strcmp(fork, "trial") == 0;
         if (const char *v = getenv("QPM_WOLF")) {
             e->wolf_in_planner = strcmp(v, "planner") == 0;
             e->wolf_mixed = strcmp(v, "mixed") == 0;
             e->wolf_side = strcmp(v, "side") == 0;
         }
-        // wolf planes on the side stream are drawn after the trial: forked at
-        // the start of the generation, C2 traces differed from run to run
-        // (tools/gen_sweep.py, B200, with and without PDL), after the trial
-        // they never did
-        if (e->wolf_in_planner) e->plan_after_trial = true;
+        // wolf planes on the side stream are drawn after the trial (round 1:
+        // forked at the start of the generation, C2 traces differed from run
+        // to run); QPM_PLAN_FORK=start keeps the start fork for the
+        // race probe (tools/sanitize.sh)
+        if (e->wolf_in_planner && !(fork && strcmp(fork, "start") == 0)) e->plan_after_trial = true;
         if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
         if (const char *v = getenv("QPM_GRAPH_GENS")) e->graph_gens = std::min(64, std::max(1, atoi(v)));
         if (const char *v = getenv("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
@@ -2351,7 +2370,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         QPM_ALLOC(e->ggains, (size_t)NP * gp.n_wl);
     }  // one rank with a communicator: allocated by qpm_engine_set_comm
 #undef QPM_ALLOC
-    if ((rc = scratch_reserve(e->prob, &e->fs, NP)) != 0) {
+    if ((rc = scratch_reserve(e->lprob ? &e->lprob->p : e->prob, &e->fs, NP)) != 0) {
         engine_free(e);
         return rc;
     }
@@ -2806,7 +2825,7 @@ int qpm_engine_exchange_from(qpm_engine *dst, qpm_engine *src, int phase) {
     QPM_ARG_CHECK(dst && src, "engines");
     (void)phase;  // every exchange moves the same buffer: the scanning rank's partial slot
     Engine *d = dst->e, *s = src->e;
-    QPM_ARG_CHECK(d->world > 1 && d->world == s->world && d->c.NP == s->c.NP && d->S_slot == s->S_slot &&
+    QPM_ARG_CHECK(d->world > 1 && d->world == s->world && d->c.NP == s->c.NP && d->SB_slot == s->SB_slot &&
                       d->rank != s->rank,
                   "engines of one sharded run");
     const size_t n = gpart_slot(s);

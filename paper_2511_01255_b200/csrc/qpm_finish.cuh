@@ -26,23 +26,31 @@ __device__ __forceinline__ Seg seg_cat(const Seg &x, const Seg &y) {
     return z;
 }
 
-// Column-sharded runs (multi-GPU): rank k scored the global segments
-// [floor(k S / world), floor((k+1) S / world)) into its slot of the
-// all-gathered partials, laid out [world][n_wl][rows][S_slot][6]; segment s
-// lives in rank (world (s+1) - 1) / S.  One GPU: world = 1, S_slot = S.
-__device__ __forceinline__ const double *seg_ptr(const double *part, int s, int lam, int64_t r, int64_t rows, int n_wl,
-                                                 int S, int world, int S_slot) {
-    int rk = 0, loc = s;
-    if (world > 1) {
-        rk = (world * (s + 1) - 1) / S;
-        loc = s - (rk * S) / world;
-    }
-    return part + ((((int64_t)rk * n_wl + lam) * rows + r) * S_slot + loc) * kPartDoubles;
-}
+// The stitch tree is fixed by the problem alone (D, wavelengths, segment
+// length), never by the batch or the number of GPUs, so fitness is a pure
+// function of the row bits: the S segments are grouped into nsb = min(8, S)
+// contiguous super-blocks, super-block b = segments [sb_lo(b), sb_lo(b+1)),
+// sb_lo(b) = floor(b S / nsb); a super-block is stitched sequentially, then
+// the nsb super-block partials by a fixed 3-level shuffle tree.
+// Multi-GPU (column shards): rank k of W owns super-blocks
+// [floor(k nsb / W), floor((k+1) nsb / W)) and the genes under them; it
+// pre-stitches its super-blocks (k_prestitch, the same sequential order) and
+// only those partials are all-gathered, [W][n_wl][rows][SB_slot][6] --
+// NP x nsb x 48 B per wavelength in total, whatever the segment count.
+constexpr int kMaxSuperBlocks = 8;
+__host__ __device__ __forceinline__ int super_blocks(int S) { return S < kMaxSuperBlocks ? S : kMaxSuperBlocks; }
+__host__ __device__ __forceinline__ int sb_lo(int b, int S, int nsb) { return (int)((int64_t)b * S / nsb); }
+// first super-block of rank k, and the rank owning super-block b
+__host__ __device__ __forceinline__ int sb_first(int k, int nsb, int world) { return (int)((int64_t)k * nsb / world); }
+__host__ __device__ __forceinline__ int sb_owner(int b, int nsb, int world) { return (world * (b + 1) - 1) / nsb; }
 
 struct FinishArgs {
-    const double *part;  // [n_wl][rows][S_slot][6] (one GPU) or [world][n_wl][rows][S_slot][6]
-    int S, world, S_slot;
+    const double *part;  // segment partials [n_wl][rows][S][6], or (pre) super-block partials
+                         // [world][n_wl][rows][SB_slot][6]
+    int S;               // segments per row (1: one exact sum per row)
+    int nsb;             // super-blocks
+    int pre;             // part holds pre-stitched super-blocks (multi-GPU)
+    int world, SB_slot;
     int64_t rows;
     int n_wl;
     const double2 *w, *h;
@@ -53,14 +61,26 @@ struct FinishArgs {
     double *gains;  // [rows][n_wl] scratch (multi)
 };
 
+__device__ __forceinline__ Seg seg_load(const double *q) {
+    return Seg{__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5)};
+}
+
+// super-block b of row r at wavelength lam from segment partials [n_wl][rows][S_stride][6]
+// whose first entry is global segment s_base: sequential stitch (k_prestitch and finish_row)
+__device__ __forceinline__ Seg stitch_super_block(const double *part, int b, int lam, int64_t r, int64_t rows,
+                                                  int S, int nsb, int S_stride, int s_base) {
+    const int s0 = sb_lo(b, S, nsb), s1 = sb_lo(b + 1, S, nsb);
+    const double *q = part + (((int64_t)lam * rows + r) * S_stride + (s0 - s_base)) * kPartDoubles;
+    Seg acc = seg_load(q);
+    for (int s = s0 + 1; s < s1; ++s) acc = seg_cat(acc, seg_load(q + (s - s0) * kPartDoubles));
+    return acc;
+}
+
 // fitness of row r by one warp (every lane must call it; the value is lane 0's):
-// lane l stitches the run of segments [l per, (l + 1) per), the 32 runs are
-// stitched by a fixed shuffle tree (deterministic), then the objective
+// lane b < nsb forms super-block b, the nsb partials are stitched by a fixed
+// shuffle tree, then the objective
 __device__ __forceinline__ double finish_row(const FinishArgs &f, int64_t r, int lane) {
-    const int S = f.S;
-    const int per = (S + 31) / 32;
-    const int s0 = lane * per;
-    const int s1 = s0 + per < S ? s0 + per : S;
+    const int S = f.S, nsb = f.nsb;
     double gmax = 0.0, gmin = 0.0;
     for (int lam = 0; lam < f.n_wl; ++lam) {
         double ar, ai;
@@ -70,12 +90,18 @@ __device__ __forceinline__ double finish_row(const FinishArgs &f, int64_t r, int
             ai = __ldcg(p + 1);
         } else {
             Seg acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int s = s0; s < s1; ++s) {
-                const double *q = seg_ptr(f.part, s, lam, r, f.rows, f.n_wl, S, f.world, f.S_slot);
-                const Seg y = {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5)};
-                acc = s == s0 ? y : seg_cat(acc, y);
+            if (lane < nsb) {
+                if (f.pre) {
+                    const int rk = sb_owner(lane, nsb, f.world);
+                    const int loc = lane - sb_first(rk, nsb, f.world);
+                    acc = seg_load(f.part + ((((int64_t)rk * f.n_wl + lam) * f.rows + r) * f.SB_slot + loc) *
+                                                kPartDoubles);
+                } else {
+                    acc = stitch_super_block(f.part, lane, lam, r, f.rows, S, nsb, S, 0);
+                }
             }
-            for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int off = 1; off < kMaxSuperBlocks; off <<= 1) {
                 Seg o;
                 o.ar = __shfl_down_sync(0xffffffffu, acc.ar, off);
                 o.ai = __shfl_down_sync(0xffffffffu, acc.ai, off);
@@ -83,8 +109,7 @@ __device__ __forceinline__ double finish_row(const FinishArgs &f, int64_t r, int
                 o.pi = __shfl_down_sync(0xffffffffu, acc.pi, off);
                 o.tr = __shfl_down_sync(0xffffffffu, acc.tr, off);
                 o.ti = __shfl_down_sync(0xffffffffu, acc.ti, off);
-                const bool has_other = lane + off < 32 && (lane + off) * per < S;
-                if ((lane & (2 * off - 1)) == 0 && has_other) acc = seg_cat(acc, o);
+                if ((lane & (2 * off - 1)) == 0 && lane + off < nsb) acc = seg_cat(acc, o);
             }
             ar = acc.ar;
             ai = acc.ai;
@@ -113,7 +138,8 @@ __device__ __forceinline__ double finish_row(const FinishArgs &f, int64_t r, int
     return -fv;
 }
 
-FinishArgs finish_args(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
-                       double *gains);
+// one-GPU layout (segment partials), or the all-gathered super-block slots
+FinishArgs finish_args(const Problem *p, const double *part, int S, int64_t rows, double *gains);
+FinishArgs finish_args_pre(const Problem *p, const double *gpart, int world, int SB_slot, int64_t rows, double *gains);
 
 }  // namespace qpm

@@ -164,7 +164,8 @@ __global__ void k_lex_bits(uint64_t start, int64_t rows, int n, int64_t W, uint3
 }
 
 // quad tables: entry rel (bit k-1 set <=> s_k != s_0) of B, E, I for quad q
-// (the s_0 = +1 values; the scan flips B and E by s_0)
+// (the s_0 = +1 values; the scan flips B and E by s_0: sums with every sign
+// negated are the exact negations, and I depends on products of two signs)
 __global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__restrict__ b, int64_t D,
                               int64_t nquads, int n_wl, int thg, double2 *__restrict__ qt) {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -182,7 +183,7 @@ __global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__r
         bi[k] = bb.y;
     }
     double2 *out = qt + (lam * nquads + q) * kQuadEntries;
-    for (int rel = 0; rel < 8; ++rel) {
+    for (int rel = 0; rel < kQuadIdx; ++rel) {
         double sg[4] = {1.0, (rel & 1) ? -1.0 : 1.0, (rel & 2) ? -1.0 : 1.0, (rel & 4) ? -1.0 : 1.0};
         double Br = 0, Bi = 0, Er = 0, Ei = 0, Ir = 0, Ii = 0;
         for (int k = 0; k < 4; ++k) {
@@ -200,8 +201,8 @@ __global__ void k_build_quads(const double2 *__restrict__ e1, const double2 *__r
                 Ii += s * pi;
             }
         out[rel] = make_double2(Br, Bi);
-        out[8 + rel] = make_double2(Er, Ei);
-        out[16 + rel] = make_double2(Ir, Ii);
+        out[kQuadIdx + rel] = make_double2(Er, Ei);
+        out[2 * kQuadIdx + rel] = make_double2(Ir, Ii);
     }
 }
 
@@ -455,12 +456,12 @@ __global__ void __launch_bounds__(kFitThreadsMax) k_fit_fast(const double2 *__re
                 const uint32_t rel = (xw[h] >> (4 * u + 1)) & 7u;
                 const uint64_t m = (uint64_t)((s0w[h] << (31 - 4 * u)) & 0x80000000u) << 32;  // s0 -> sign bit
                 const double2 *tq = tb + q * kQuadEntries + rel;
-                const double2 Et = tq[8];
+                const double2 Et = tq[kQuadIdx];
                 const double2 E = make_double2(flip_if(Et.x, m), flip_if(Et.y, m));
                 Seg &z = ch[h];
                 if (THG) {
                     const double2 Bt = tq[0];
-                    const double2 I = tq[16];
+                    const double2 I = tq[2 * kQuadIdx];
                     const double2 B = make_double2(flip_if(Bt.x, m), flip_if(Bt.y, m));
                     z.ar = fma(z.pr, B.x, z.ar);
                     z.ar = fma(-z.pi, B.y, z.ar);
@@ -689,13 +690,8 @@ int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_word
     return QPM_OK;
 }
 
-FinishArgs finish_args(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
-                       double *gains) {
+static FinishArgs finish_base(const Problem *p, int64_t rows, double *gains) {
     FinishArgs f;
-    f.part = part;
-    f.S = S;
-    f.world = world;
-    f.S_slot = S_slot;
     f.rows = rows;
     f.n_wl = p->n_wl;
     f.w = (const double2 *)p->w;
@@ -709,11 +705,68 @@ FinishArgs finish_args(const Problem *p, const double *part, int S, int world, i
     return f;
 }
 
-int launch_fitness_finish(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
-                          double *gains, double *out, cudaStream_t stream, int *launches, bool pdl) {
-    if (rows == 0) return QPM_OK;
-    QPM_CUDA_TRY(launch_k(pdl, k_fit_finish, dim3((unsigned)((rows + kFinishWarps - 1) / kFinishWarps)),
-                          dim3(32 * kFinishWarps), 0, stream, finish_args(p, part, S, world, S_slot, rows, gains), out));
+FinishArgs finish_args(const Problem *p, const double *part, int S, int64_t rows, double *gains) {
+    FinishArgs f = finish_base(p, rows, gains);
+    f.part = part;
+    f.S = S;
+    f.nsb = super_blocks(S);
+    f.pre = 0;
+    f.world = 1;
+    f.SB_slot = 0;
+    return f;
+}
+
+FinishArgs finish_args_pre(const Problem *p, const double *gpart, int world, int SB_slot, int64_t rows,
+                           double *gains) {
+    FinishArgs f = finish_base(p, rows, gains);
+    f.part = gpart;
+    f.S = p->S;
+    f.nsb = p->nsb;
+    f.pre = 1;
+    f.world = world;
+    f.SB_slot = SB_slot;
+    return f;
+}
+
+int launch_fitness_finish(const FinishArgs &f, double *out, cudaStream_t stream, int *launches, bool pdl) {
+    if (f.rows == 0) return QPM_OK;
+    QPM_CUDA_TRY(launch_k(pdl, k_fit_finish, dim3((unsigned)((f.rows + kFinishWarps - 1) / kFinishWarps)),
+                          dim3(32 * kFinishWarps), 0, stream, f, out));
+    if (launches) *launches += 1;
+    return QPM_OK;
+}
+
+// A column shard's super-block partials (multi-GPU): one thread per (row,
+// wavelength, owned super-block) stitches the super-block's segments from the
+// shard's scan (part [n_wl][rows][S_loc][6], first entry = global segment
+// seg_lo) into its slot of the all-gathered buffer [n_wl][rows][SB_slot][6],
+// in the order finish_row uses on one GPU (bit-identical fitness).
+__global__ void k_prestitch(const double *part, int S, int nsb, int S_loc, int seg_lo, int sb0, int nown,
+                            int64_t rows, int n_wl, int SB_slot, double *__restrict__ slot) {
+    pdl_wait();
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= rows * n_wl * nown) return;
+    const int k = (int)(t % nown);
+    const int64_t rl = t / nown;
+    const int64_t r = rl % rows;
+    const int lam = (int)(rl / rows);
+    const Seg z = stitch_super_block(part, sb0 + k, lam, r, rows, S, nsb, S_loc, seg_lo);
+    double *o = slot + (((int64_t)lam * rows + r) * SB_slot + k) * kPartDoubles;
+    o[0] = z.ar;
+    o[1] = z.ai;
+    o[2] = z.pr;
+    o[3] = z.pi;
+    o[4] = z.tr;
+    o[5] = z.ti;
+}
+
+int launch_prestitch(const Problem *p, const double *part, int S_loc, int seg_lo, int rank, int world, int SB_slot,
+                     int64_t rows, double *slot, cudaStream_t stream, int *launches, bool pdl) {
+    const int sb0 = sb_first(rank, p->nsb, world), nown = sb_first(rank + 1, p->nsb, world) - sb0;
+    const int64_t n = rows * p->n_wl * nown;
+    if (n == 0) return QPM_OK;
+    QPM_CUDA_TRY(launch_k(pdl, k_prestitch, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, stream, part, p->S,
+                          p->nsb, S_loc, seg_lo, sb0, nown, rows, p->n_wl, SB_slot, slot));
     if (launches) *launches += 1;
     return QPM_OK;
 }
@@ -758,7 +811,7 @@ int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64
         const int rc = launch_fitness_scan(p, bits, row_words, row_index, rows, fs->part, S, stream, launches, pdl);
         if (rc) return rc;
     }
-    return launch_fitness_finish(p, fs->part, S, 1, S, rows, fs->gains, out, stream, launches, pdl);
+    return launch_fitness_finish(finish_args(p, fs->part, S, rows, fs->gains), out, stream, launches, pdl);
 }
 
 // A problem over domains [g0, g0 + Dl) of `p` (column shard of a multi-GPU
@@ -781,6 +834,7 @@ int problem_slice(const Problem *p, int64_t g0, int64_t Dl, qpm_problem **out) {
     q.nchunks = q.W / 4;
     q.seg_chunks = p->seg_chunks;
     q.S = (int)((q.nchunks + q.seg_chunks - 1) / q.seg_chunks);
+    q.nsb = super_blocks(q.S);
     q.scale = p->scale;
     q.g0 = p->g0;
     q.beta = p->beta;
@@ -893,13 +947,14 @@ int qpm_uniform_fill(uint64_t key, uint64_t start, int64_t n, double *out_dev, v
 
 int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int64_t D, const double *e1,
                        const double *b, const double *w, const double *hconst, double scale, double g0,
-                       double beta) {
+                       double beta, int seg_chunks) {
     QPM_ARG_CHECK(out, "out");
     QPM_ARG_CHECK(process == QPM_PROCESS_SHG || process == QPM_PROCESS_THG, "process");
     QPM_ARG_CHECK(n_wl >= 1 && n_wl <= 65535, "n_wl in [1, 65535]");
     QPM_ARG_CHECK(D >= 1, "D >= 1");
     QPM_ARG_CHECK(e1 && w, "e1 and w tables");
     QPM_ARG_CHECK(process == QPM_PROCESS_SHG || (b && hconst), "THG needs b and hconst tables");
+    QPM_ARG_CHECK(seg_chunks >= 0, "seg_chunks >= 0 (0 = the default for D and the wavelength count)");
     auto *h = new qpm_problem();
     Problem &p = h->p;
     p.mu = new std::mutex();
@@ -910,24 +965,24 @@ int qpm_problem_create(qpm_problem **out, int process, int multi, int n_wl, int6
     p.W = round_up((D + 31) / 32, 4);
     p.nquads = p.W * 8;
     p.nchunks = p.W / 4;
-    // segment length (in 128-domain chunks) depends only on D and the
-    // wavelength count, never on the batch, so fitness stays a pure function
-    // of the row bits; longer segments when wavelengths supply parallelism.
-    // One wavelength: 3 chunks (C2, D = 10^4: 27 segments; alternating A/B
-    // on one B200: 112.1 / 114.0 / 116.5 us per generation for 3 / 2 / 1
-    // chunks, 4 was slower still), or 2 when 3 leaves fewer than 16 segments.
-    // Multi-GPU runs choose their own (bench.py: 2, an even split of C2 over
-    // 2, 4 and 8 GPUs) through QPM_SEG_CHUNKS.
-    if (n_wl > 1)
+    // segment length (in 128-domain chunks) depends only on the problem (D,
+    // wavelength count, or the caller's seg_chunks), never on the batch or
+    // the GPU count, so fitness stays a pure function of the row bits;
+    // longer segments when wavelengths supply parallelism.  One wavelength:
+    // 3 chunks (C2, D = 10^4: 27 segments; alternating A/B on one B200:
+    // 112.1 / 114.0 / 116.5 us per generation for 3 / 2 / 1 chunks, 4 was
+    // slower still), or 2 when 3 leaves fewer than 16 segments.  Multi-GPU
+    // runs may pick a length that splits evenly over their ranks (bench.py:
+    // 2 chunks, C2's 40 segments = 8 super-blocks of 5).
+    if (seg_chunks > 0)
+        p.seg_chunks = seg_chunks;
+    else if (n_wl > 1)
         p.seg_chunks = 4 * std::min(n_wl, 8);
     else
         p.seg_chunks = (p.nchunks + 2) / 3 < 16 ? 2 : 3;
     p.seg_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nchunks, p.seg_chunks));
-    if (const char *env = getenv("QPM_SEG_CHUNKS")) {  // tuning override (changes fitness rounding only)
-        const int v = atoi(env);
-        if (v >= 1) p.seg_chunks = (int)std::min<int64_t>(p.nchunks, v);
-    }
     p.S = (int)((p.nchunks + p.seg_chunks - 1) / p.seg_chunks);
+    p.nsb = super_blocks(p.S);
     p.scale = scale;
     p.g0 = g0;
     p.beta = beta;
@@ -997,6 +1052,14 @@ int qpm_problem_destroy(qpm_problem *h) {
 }
 
 int64_t qpm_problem_row_words(const qpm_problem *h) { return h ? h->p.W : -1; }
+
+int qpm_problem_layout(const qpm_problem *h, int *seg_chunks, int *segments, int *super_blocks_out) {
+    QPM_ARG_CHECK(h, "problem");
+    if (seg_chunks) *seg_chunks = h->p.seg_chunks;
+    if (segments) *segments = h->p.S;
+    if (super_blocks_out) *super_blocks_out = h->p.nsb;
+    return QPM_OK;
+}
 
 int qpm_pack_signs(const int8_t *signs_dev, int64_t rows, int64_t D, uint32_t *bits_dev, int64_t row_words,
                    void *stream) {

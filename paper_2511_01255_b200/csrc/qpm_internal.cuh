@@ -53,7 +53,14 @@ constexpr int kFitThreads = QPM_FIT_THREADS;  // rows per fast-fitness CTA (one 
 #endif
 constexpr int kFitThreadsMax = QPM_FIT_THREADS1;  // ... one wavelength (and the launch bound)
 constexpr int kQuadsPerChunk = 32;    // 128 domains = 4 u32 words per chunk
-constexpr int kQuadEntries = 24;      // B[8], E[8], I[8] complex entries per quad (by relative signs)
+// complex entries per quad of the fast scan's tables: B[8], E[8], I[8] by the
+// 3 relative signs (s0 applied by XOR in the scan).  One table is one
+// 128-byte shared-memory row, so a quarter-warp's 16-byte loads never
+// conflict (measured: folding s0 into 16-entry tables cut the scan's
+// instructions by 31 % but made it shared-memory-wavefront bound, C5 fitness
+// 2029 -> 3241 us)
+constexpr int kQuadIdx = 8;
+constexpr int kQuadEntries = 3 * kQuadIdx;
 constexpr int kPartDoubles = 6;       // acc, P, T (complex) per (row, wavelength, segment)
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -67,6 +74,7 @@ struct Problem {
     int64_t nchunks = 0;  // W / 4
     int seg_chunks = 1;   // chunks per fast-scan segment
     int S = 1;            // segments per row
+    int nsb = 1;          // stitch super-blocks, min(8, S) (qpm_finish.cuh)
     double scale = 1.0, g0 = 2.0, beta = 1.0;
     double2 *e1 = nullptr;  // [n_wl][D]
     double2 *b = nullptr;   // [n_wl][D] (thg)
@@ -226,10 +234,11 @@ int launch_reduce_best(const double *values, int64_t n, int k, int32_t *idx_out,
 // fast-mode segment scan into part ([n_wl][rows][S_stride][6], S_stride >= p->S)
 int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_words, const int32_t *row_index,
                         int64_t rows, double *part, int S_stride, cudaStream_t stream, int *launches, bool pdl);
-// stitch + objective of rows whose S segment partials are in part (world > 1:
-// all-gathered column-shard slots [world][n_wl][rows][S_slot][6])
-int launch_fitness_finish(const Problem *p, const double *part, int S, int world, int S_slot, int64_t rows,
-                          double *gains, double *out, cudaStream_t stream, int *launches, bool pdl);
+// stitch + objective (the layout of f.part is in the FinishArgs, qpm_finish.cuh)
+int launch_fitness_finish(const struct FinishArgs &f, double *out, cudaStream_t stream, int *launches, bool pdl);
+// a column shard's owned super-block partials into its all-gather slot
+int launch_prestitch(const Problem *p, const double *part, int S_loc, int seg_lo, int rank, int world, int SB_slot,
+                     int64_t rows, double *slot, cudaStream_t stream, int *launches, bool pdl);
 int launch_fitness_partials(const Problem *p, FitScratch *fs, const uint32_t *bits, int64_t row_words,
                             const int32_t *row_index, int64_t rows, int mode, cudaStream_t stream, int *launches,
                             bool pdl, int *S_out);

@@ -10,15 +10,18 @@ Scheme (a column variant of SURVEY.md §8(e)'s exact scheme):
   leader vote (leaders' columns are local), init_population, run_gwo's
   continuous move; so each rank runs them on its columns of all NP rows, with
   the stream positions of the global gene index (bit-identical draws);
-* each rank scans the fitness segments of its columns for all rows; the
-  segment partials (NP x 48 B per segment) are all-gathered and every rank
-  stitches and scores all rows in the single-GPU segment order (fast mode
-  fitness is bit-identical to one GPU);
+* each rank scans the fitness segments of its columns for all rows and
+  pre-stitches them into its stitch super-blocks (the fixed single-GPU tree:
+  min(8, S) contiguous super-blocks); those partials (NP x 48 B per owned
+  super-block, about NP x 8 x 48 B over all ranks) are all-gathered and every
+  rank finishes and scores all rows (fast-mode fitness bit-identical to one
+  GPU);
 * selection, leaders, statistics and the F update run replicated on every
   rank from identical data, so they need no further collective.
 
 Per generation a hybrid run all-gathers the partials twice (DE and wolf
-candidates); nothing else moves: no genome rows, no recomputation.  The
+candidates), 393 KB each at NP 1024 / 3.1 MB at NP 8192 (one wavelength);
+nothing else moves: no genome rows, no recomputation.  The
 collectives run inside the engine (libqpm_b200.so calls ncclAllGather on the
 engine stream, captured into the per-generation CUDA graph).  The NCCL
 communicator is bootstrapped from a unique id that rank 0 creates and
@@ -38,22 +41,24 @@ from .optimizer import DEParams, Engine, GWOParams, Individual, RunResult, Sched
 
 def shard_columns(D: int, world: int, rank: int, n_wl: int = 1, seg_chunks: int | None = None) -> tuple[int, int]:
     """Gene columns [g0, g1) of `rank` (the engine's split, qpm_engine_create):
-    rank k owns the fitness segments [floor(k S / W), floor((k+1) S / W)) of
-    the problem and the genes under them; a segment is seg_chunks 128-domain
-    chunks (one wavelength: 3, or 2 when that leaves fewer than 16 segments;
-    4 min(n_wl, 8) with several wavelengths; QPM_SEG_CHUNKS overrides it in
-    the library, pass seg_chunks here to match)."""
+    the problem's S fitness segments (seg_chunks 128-domain chunks each; by
+    default 3 for one wavelength, 2 when that leaves fewer than 16 segments,
+    4 min(n_wl, 8) with several) form B = min(8, S) stitch super-blocks,
+    super-block b = segments [floor(b S / B), floor((b+1) S / B)); rank k owns
+    super-blocks [floor(k B / W), floor((k+1) B / W)) and the genes under them."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside [0, {world})")
     words = -(-(-(-D // 32)) // 4) * 4
     nchunks = words // 4
     if seg_chunks is None:  # qpm_problem_create's default
         seg_chunks = 4 * min(n_wl, 8) if n_wl > 1 else (2 if -(-nchunks // 3) < 16 else 3)
-        seg_chunks = max(1, min(nchunks, seg_chunks))
+    seg_chunks = max(1, min(nchunks, seg_chunks))
     S = -(-nchunks // seg_chunks)
-    if S < world:
-        raise ValueError(f"{S} fitness segments cannot be split over {world} ranks")
-    lo, hi = rank * S // world, (rank + 1) * S // world
+    B = min(8, S)
+    if B < world:
+        raise ValueError(f"{S} fitness segments ({B} stitch super-blocks) cannot be split over {world} ranks")
+    sb0, sb1 = rank * B // world, (rank + 1) * B // world
+    lo, hi = sb0 * S // B, sb1 * S // B
     seg = seg_chunks * 128
     return lo * seg, min(D, hi * seg)
 
@@ -153,7 +158,7 @@ class EmulatedShards:
 
     Test harness for the sharded protocol: every kernel a real rank runs is
     run by its shard engine; the NCCL all-gather is replaced by device copies
-    of each shard's segment partials into the other shards' buffers.
+    of each shard's super-block partials into the other shards' buffers.
     """
 
     def __init__(self, objective, algorithm, world: int, **kw):

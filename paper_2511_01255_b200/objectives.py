@@ -80,9 +80,13 @@ class GpuPatternObjective:
     sequential arithmetic and is bit-identical to the reference.
     """
 
-    def __init__(self, spec: ObjectiveSpec, provider, thickness_um: float, count: int, mode: str = "fast"):
+    def __init__(self, spec: ObjectiveSpec, provider, thickness_um: float, count: int, mode: str = "fast",
+                 seg_chunks: int | None = None):
         if mode not in MODES:
             raise ValueError(f"mode must be one of {tuple(MODES)}, got {mode!r}")
+        if seg_chunks is not None and int(seg_chunks) < 1:
+            raise ValueError(f"seg_chunks must be >= 1, got {seg_chunks}")
+        self._seg_req = int(seg_chunks or 0)  # 0: the library's default for D and the wavelength count
         self.spec = spec
         self.thickness_um = float(thickness_um)
         self.count = int(count)
@@ -110,9 +114,14 @@ class GpuPatternObjective:
             ctypes.byref(handle), _native.QPM_PROCESS_THG if thg else _native.QPM_PROCESS_SHG,
             1 if self.spec.is_multi else 0, len(self.tables), self.count, e1.ctypes.data,
             b.ctypes.data if b is not None else None, w.ctypes.data, h.ctypes.data if h is not None else None,
-            float(self._scale), float(self.spec.g0), float(self.spec.beta)), "qpm_problem_create")
+            float(self._scale), float(self.spec.g0), float(self.spec.beta), self._seg_req), "qpm_problem_create")
         self._handle = handle
         self.row_words = int(L.qpm_problem_row_words(handle))
+        sc, S, nsb = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _native.check(L.qpm_problem_layout(handle, ctypes.byref(sc), ctypes.byref(S), ctypes.byref(nsb)),
+                      "qpm_problem_layout")
+        # fast-scan layout: segment length (128-domain chunks), segments, stitch super-blocks
+        self.seg_chunks, self.segments, self.super_blocks = sc.value, S.value, nsb.value
 
     @property
     def handle(self):
@@ -194,8 +203,11 @@ PatternObjective = GpuPatternObjective
 
 
 def make_objective(spec: ObjectiveSpec, provider, thickness_um: float, count: int,
-                   mode: str = "fast") -> GpuPatternObjective:
-    return GpuPatternObjective(spec, provider, thickness_um, count, mode=mode)
+                   mode: str = "fast", seg_chunks: int | None = None) -> GpuPatternObjective:
+    """objectives.make_objective (objectives.py:126-130) on the device; seg_chunks
+    optionally fixes the fast scan's segment length (multi-GPU runs pick one
+    whose segments split evenly over their ranks)."""
+    return GpuPatternObjective(spec, provider, thickness_um, count, mode=mode, seg_chunks=seg_chunks)
 
 
 def fitness_single(pattern, spec: ObjectiveSpec, provider, mode: str = "fast") -> float:

@@ -1,7 +1,7 @@
 """Fitness launches for several segment lengths in one process (for one ncu launch-list pass).
 
     python tools/fit_seg_probe.py [seg ...]
-QPM_SEG_CHUNKS is read when a problem is created, so each setting gets its own problem.
+The segment length is a problem parameter (make_objective(seg_chunks=...)), so each setting gets its own problem.
 """
 import os
 import sys
@@ -18,8 +18,8 @@ def main():
     segs = [int(a) for a in sys.argv[1:]] or [1, 2, 4]
     rows, d = 1024, 10_000
     for sc in segs:
-        os.environ["QPM_SEG_CHUNKS"] = str(sc)
-        obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, d)
+        obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, d,
+                               seg_chunks=sc)
         W = obj.row_words
         g = torch.Generator(device="cuda").manual_seed(0)
         bits = torch.randint(0, 2**31 - 1, (rows, W), dtype=torch.int32, device="cuda", generator=g)

@@ -25,6 +25,6 @@ python tools/bench_fitness.py --rows 4092 --d 20000 --nwl 64 --iters 3 > $E/fit_
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fit_fast -s 2 -c 1 \
     -o $E/prof_fit_c5 python tools/bench_fitness.py --rows 4092 --d 20000 --nwl 64 --iters 3 > $E/ncu_fit.log 2>&1
 # the bench's multi-GPU runs use 2-chunk fitness segments (even C2 split)
-for w in 2 4 8; do QPM_SEG_CHUNKS=2 timeout 400 python tools/shard_probe.py --world $w >> $E/shard_probe.jsonl 2>> $E/shard_probe.err; done
+for w in 2 4 8; do timeout 400 python tools/shard_probe.py --world $w --seg-chunks 2 >> $E/shard_probe.jsonl 2>> $E/shard_probe.err; done
 timeout 900 python tools/shard_probe.py --world 8 --d 100000 --warm 5 --gens 5 >> $E/shard_probe.jsonl 2>> $E/shard_probe.err
 echo DONE >> $E/pytest_gpu.log
