@@ -323,6 +323,18 @@ def fitness_kernel_roofline(q, torch, sm_count, peaks, iters=20):
                     "peak_basis": f"nominal FP64 CUDA-core peak ({sm_count} SMs x 64 DFMA/clk x 2 x sm_max_mhz "
                                   f"from MEASURED_PEAKS.json; no measured FP64 entry)",
                     "algorithmic_unit": f"{FLOP_PER_EVAL} flop per domain-eval x rows x D x wavelengths"})
+        # the binding on-chip resource of the quad-table scan: every (row,
+        # quad of 4 domains, wavelength) reads B, E and I (3 x 16 B) from
+        # shared memory; one 128-B wavefront per SM per clock
+        quads = (d + 3) // 4
+        smem_bytes = rows * quads * nwl * 3 * 16
+        smem_peak = sm_count * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        out[-1]["smem_roofline"] = {
+            "achieved": smem_bytes / sec / 1e12, "peak": smem_peak, "unit": "TB/s",
+            "frac": smem_bytes / sec / 1e12 / smem_peak,
+            "basis": f"48 B of table loads per (row, quad, wavelength) = {smem_bytes / 1e9:.2f} GB per launch; "
+                     f"peak {sm_count} SMs x 128 B/clk x sm_max_mhz (one shared-memory wavefront per clock); "
+                     f"the FP64 pipe needs 5 clk per warp-quad, shared memory 12"}
         del obj
     return out
 

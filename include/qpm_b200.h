@@ -260,6 +260,12 @@ int qpm_engine_partials_write(qpm_engine *e, int rank, const double *host_in);
  * further steps.  Replaces the reference's BatchEvaluationError failure
  * contract (parexec.py:27-33) on the multi-GPU path. */
 int qpm_engine_wait(qpm_engine *e, int64_t timeout_ms);
+/* Invariant checks (builds with -DQPM_CHECKS=1, libqpm_b200_checks.so): after
+ * every generation a kernel verifies the slot permutation, the planner's DE
+ * picks and j_rand, the leaders, finite fitness and trace, and the planner's
+ * generation counter; flags = violation bits (0 = clean), detail = the first
+ * violation (code << 24 | index).  QPM_ERR_STATE in other builds. */
+int qpm_engine_check_status(qpm_engine *e, uint32_t *flags, uint32_t *detail);
 int qpm_engine_cand_ptr(qpm_engine *e, double **cand_dev);
 int qpm_engine_stream(qpm_engine *e, void **stream);
 

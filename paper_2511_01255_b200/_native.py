@@ -29,7 +29,7 @@ EXPORTS = (
     "qpm_engine_init_finish",
     "qpm_engine_phases", "qpm_engine_run_phase", "qpm_engine_exchange_from", "qpm_engine_cand_ptr",
     "qpm_engine_stream", "qpm_engine_partials_info", "qpm_engine_partials_read", "qpm_engine_partials_write",
-    "qpm_engine_wait",
+    "qpm_engine_wait", "qpm_engine_check_status",
 )
 
 
@@ -129,6 +129,7 @@ def lib():
         "qpm_engine_partials_read": (I32, [P, P]),
         "qpm_engine_partials_write": (I32, [P, I32, P]),
         "qpm_engine_wait": (I32, [P, I64]),
+        "qpm_engine_check_status": (I32, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -16,6 +16,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqpm_b200.so")
+# the same sources with the per-generation invariant checks (-DQPM_CHECKS=1,
+# k_check_state); loaded only by tests/test_gpu_checks.py through QPM_LIB
+LIB_CHECKS = os.path.join(HERE, "libqpm_b200_checks.so")
 SOURCES = ["qpm_fitness.cu", "qpm_engine.cu"]
 HEADERS = ["qpm_common.cuh", "qpm_internal.cuh", "qpm_finish.cuh", os.path.join("..", "..", "include", "qpm_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -30,31 +33,37 @@ def nvcc() -> str:
     return path
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + ".tmp"
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    lib = LIB_CHECKS if checks else LIB
+    if not force and not _stale(lib):
+        return lib
+    tmp = lib + ".tmp"
     extra = os.environ.get("QPM_NVCC_EXTRA", "").split()  # tuning builds, e.g. -DQPM_DE_MINB=3
+    if checks:
+        extra = extra + ["-DQPM_CHECKS=1"]
     cmd = [nvcc()] + NVCC_FLAGS + extra + ARCH + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
-    log = os.path.join(HERE, "csrc", "ptxas.log")
-    with open(log, "w") as fh:
-        fh.write(res.stderr)
+    os.replace(tmp, lib)
+    if not checks:
+        log = os.path.join(HERE, "csrc", "ptxas.log")
+        with open(log, "w") as fh:
+            fh.write(res.stderr)
     if verbose:
         print(res.stderr, file=sys.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--checks" in sys.argv:
+        print(build(force="--force" in sys.argv, checks=True))

@@ -1614,6 +1614,89 @@ __global__ void k_finalize_best(RunConsts c, EngineState *st, const double *fit)
 
 __global__ void k_reset_flag(EngineState *st) { st->best_flag = 0; }
 
+// ---------------------------------------------------------------- state checks
+// QPM_CHECKS builds (libqpm_b200_checks.so, tests/test_gpu_checks.py): after
+// every generation one CTA verifies the engine's invariants and records the
+// first violation in a device word pair (the pool runs no compute-sanitizer;
+// these are the bounds checks and asserts the engine carries instead):
+//   1 slot ids in [0, 2 NP) and {slot_of} u {spare_of} a permutation of them
+//   2 the next generation's DE picks r1, r2, r3 distinct, != i, in [0, NP);
+//     m >= 3; j_rand in [0, Dg)
+//   4 leaders distinct and in [0, NP) (hybrid, gwo)
+//   8 every fitness finite (NaN / inf would break the strict-> selection)
+//  16 the trace row just written finite and its generation number right
+//  32 the generation counter g_plan of the planner equals g + 1 (hybrid, de)
+#ifndef QPM_CHECKS
+#define QPM_CHECKS 0
+#endif
+struct CheckArgs {
+    const EngineState *st;
+    const int32_t *slot_of, *spare_of;
+    const int4 *picks;
+    const int32_t *jrand;
+    const double *fit, *trace;
+    unsigned *err;  // [0] violation bits, [1] first detail: code << 24 | index
+};
+__device__ __forceinline__ void check_fail(unsigned *err, unsigned code, unsigned idx) {
+    atomicOr(err, code);
+    atomicCAS(err + 1, 0u, (code << 24) | (idx & 0xFFFFFFu));
+}
+//  64 a candidate's fitness differs from a recomputation of the same
+//     candidate rows after the fact (the scan / finish saw inconsistent data)
+__global__ void k_check_fitness(const double *cand, const double *again, int64_t n, unsigned *err) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && !(__double_as_longlong(cand[i]) == __double_as_longlong(again[i]))) check_fail(err, 64u, (unsigned)i);
+}
+__global__ void __launch_bounds__(kCtaThreads) k_check_state(RunConsts c, CheckArgs a) {
+    extern __shared__ uint32_t s_seen[];  // 2 NP bits
+    const int64_t NP = c.NP, nw = (2 * NP + 31) / 32;
+    for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) s_seen[w] = 0u;
+    __syncthreads();
+    const int64_t g = a.st->g;  // the generation computed next
+    for (int64_t i = threadIdx.x; i < NP; i += blockDim.x) {
+        const int32_t sl[2] = {a.slot_of[i], a.spare_of[i]};
+        for (int t = 0; t < 2; ++t) {
+            if (sl[t] < 0 || sl[t] >= 2 * NP) {
+                check_fail(a.err, 1u, (unsigned)i);
+                continue;
+            }
+            const uint32_t bit = 1u << (sl[t] & 31);
+            if (atomicOr(&s_seen[sl[t] >> 5], bit) & bit) check_fail(a.err, 1u, (unsigned)i);
+        }
+        if (!isfinite(a.fit[i])) check_fail(a.err, 8u, (unsigned)i);
+        if (c.algorithm != QPM_ALGO_GWO && g <= c.G) {
+            const int4 pk = a.picks[(g & 1) * NP + i];
+            const int32_t jr = a.jrand[(g & 1) * NP + i];
+            const bool ok = pk.x >= 0 && pk.x < NP && pk.y >= 0 && pk.y < NP && pk.z >= 0 && pk.z < NP &&
+                            pk.x != i && pk.y != i && pk.z != i && pk.x != pk.y && pk.x != pk.z && pk.y != pk.z &&
+                            pk.w >= 3 && jr >= 0 && jr < c.Dg;
+            if (!ok) check_fail(a.err, 2u, (unsigned)i);
+        }
+    }
+    __syncthreads();
+    for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) {
+        const int64_t lo = w * 32, n = 2 * NP - lo < 32 ? 2 * NP - lo : 32;
+        const uint32_t want = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+        if (s_seen[w] != want) check_fail(a.err, 1u, (unsigned)lo);
+    }
+    if (threadIdx.x == 0) {
+        if (c.algorithm != QPM_ALGO_DE) {
+            const int k = c.algorithm == QPM_ALGO_GWO ? 3 : c.k;
+            for (int t = 0; t < k; ++t) {
+                const int32_t l = a.st->leaders[t];
+                bool ok = l >= 0 && l < NP;
+                for (int u = 0; u < t; ++u) ok &= a.st->leaders[u] != l;
+                if (!ok && g > 1) check_fail(a.err, 4u, (unsigned)t);
+            }
+        }
+        const double *row = a.trace + (g - 1) * 5;
+        bool ok = g >= 1 && row[0] == (double)(g - 1);
+        for (int t = 1; t < 5; ++t) ok &= isfinite(row[t]);
+        if (!ok) check_fail(a.err, 16u, (unsigned)g);
+        if (c.algorithm != QPM_ALGO_GWO && g <= c.G && a.st->g_plan != g + 1) check_fail(a.err, 32u, (unsigned)g);
+    }
+}
+
 // ---------------------------------------------------------------- engine
 struct Engine {
     Problem *prob = nullptr;
@@ -1687,6 +1770,9 @@ struct Engine {
     bool init_pending = false;  // emulated shard: fitness scan of generation 0 done, exchange pending
     bool owns_stream = false;
     bool failed = false;  // a collective failed or timed out: the communicator was aborted
+    unsigned *check_err = nullptr;  // QPM_CHECKS builds: [2] first invariant violation
+    FitScratch check_fs;            // QPM_CHECKS builds: the candidates' fitness recomputed
+    double *check_fit = nullptr;
     int64_t device_bytes = 0;
     std::vector<std::pair<void *, size_t>> allocs;
 };
@@ -1974,6 +2060,30 @@ static int fit_finish(Engine *e, double *out, cudaStream_t s, int *n) {
                                  n, e->pdl);
 }
 
+// QPM_CHECKS builds: the candidates' fitness (cand, from cbits) recomputed by a
+// separate scan + finish and compared bit for bit (one GPU)
+static int enqueue_fit_check(Engine *e, cudaStream_t s, int *n) {
+    if (!QPM_CHECKS || !e->check_err || e->sharded()) return QPM_OK;
+    int rc = launch_fitness(e->prob, &e->check_fs, e->cbits, e->c.W, nullptr, e->c.NP, e->check_fit,
+                            e->P.fitness_mode, s, n, false);
+    if (rc) return rc;
+    k_check_fitness<<<(unsigned)((e->c.NP + 255) / 256), 256, 0, s>>>(e->cand, e->check_fit, e->c.NP, e->check_err);
+    QPM_LAUNCH_CHECK();
+    *n += 1;
+    return QPM_OK;
+}
+
+// QPM_CHECKS builds: the invariant check at the end of a generation (after the planner join)
+static int enqueue_check(Engine *e, cudaStream_t s, int *n) {
+    if (!QPM_CHECKS || !e->check_err) return QPM_OK;
+    CheckArgs a{e->st, e->slot_of, e->spare_of, e->picks, e->jrand, e->fit, e->trace, e->check_err};
+    const size_t smem = (size_t)((2 * e->c.NP + 31) / 32) * sizeof(uint32_t);
+    k_check_state<<<1, kCtaThreads, smem, s>>>(e->c, a);
+    QPM_LAUNCH_CHECK();
+    *n += 1;
+    return QPM_OK;
+}
+
 static int phase_count(const Engine *e) { return e->c.algorithm == QPM_ALGO_HYBRID ? 3 : 2; }
 
 // One generation = phases separated by exchanges of the candidates' fitness
@@ -2019,6 +2129,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
                                            e->best_bits);
             QPM_LAUNCH_CHECK();
             *n += 2;
+            return enqueue_check(e, s, n);
         }
         return QPM_OK;
     }
@@ -2080,11 +2191,12 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
     }
     if (phase == 1) {
         if (!hybrid) {
+            if ((rc = enqueue_fit_check(e, s, n))) return rc;  // the DE candidates (QPM_CHECKS)
             mark("select_stats");
             if ((rc = launch_select_stats(e, 0, s))) return rc;
             *n += 1;
             QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
-            return QPM_OK;
+            return enqueue_check(e, s, n);
         }
         if (fused_select(e)) {
             mark("finish_select_topk");
@@ -2095,6 +2207,7 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
                                   e->st, (const double *)e->cand, e->fit, e->slot_of, e->spare_of,
                                   TopkScratch{e->topk_idx, e->topk_cnt}, e->slot_tag));
         }
+        if ((rc = enqueue_fit_check(e, s, n))) return rc;  // the DE candidates (QPM_CHECKS)
         if (e->wolf_side) QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_wjoin, 0));  // this generation's planes
         mark("gwo_apply");
         QPM_CUDA_TRY(launch_k(e->pdl, c.k == 4 ? k_gwo_apply<4> : k_gwo_apply<3>,
@@ -2114,8 +2227,9 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
         if ((rc = launch_select_stats(e, 1, s))) return rc;
     }
     *n += 1;
+    if ((rc = enqueue_fit_check(e, s, n))) return rc;  // the wolf candidates (QPM_CHECKS)
     QPM_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_join, 0));  // join the planner
-    return QPM_OK;
+    return enqueue_check(e, s, n);
 }
 
 // one generation's launch sequence
@@ -2150,6 +2264,7 @@ static void engine_free(Engine *e) {
     if (e->graph_k) cudaGraphDestroy(e->graph_k);
     for (auto &pb : e->allocs) dev_cache_release(pb.first, pb.second);
     scratch_free(&e->fs);
+    scratch_free(&e->check_fs);
     if (e->lprob) qpm_problem_destroy(e->lprob);
     delete e;
 }
@@ -2364,6 +2479,10 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     QPM_ALLOC(e->topk_idx, (size_t)kTopkMaxCtas * kTopSlots);
     QPM_ALLOC(e->topk_cnt, 1);
     QPM_ALLOC(e->fs_cnt, 2);
+    if (QPM_CHECKS) {
+        QPM_ALLOC(e->check_err, 2);
+        QPM_ALLOC(e->check_fit, NP);
+    }
     if (QPM_SLOT_TAG) QPM_ALLOC(e->slot_tag, NP);
     if (e->world > 1) {
         QPM_ALLOC(e->gpart, (size_t)e->world * gpart_slot(e));
@@ -2375,6 +2494,10 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         return rc;
     }
     e->device_bytes += e->fs.bytes;
+    if (QPM_CHECKS && (rc = scratch_reserve(e->prob, &e->check_fs, NP)) != 0) {
+        engine_free(e);
+        return rc;
+    }
     std::vector<int32_t> tree_host;
     tree_host.insert(tree_host.end(), ht.leaf_off.begin(), ht.leaf_off.end());
     tree_host.insert(tree_host.end(), ht.kid.begin(), ht.kid.end());
@@ -2438,6 +2561,10 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     if (err == cudaSuccess) err = cudaMemsetAsync(e->slot_bin, 0, 2 * NP, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->topk_cnt, 0, sizeof(unsigned), e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->fs_cnt, 0, 2 * sizeof(unsigned), e->stream);
+    if (err == cudaSuccess && e->check_err) err = cudaMemsetAsync(e->check_err, 0, 2 * sizeof(unsigned), e->stream);
+    if (err == cudaSuccess && e->check_err)
+        err = cudaFuncSetAttribute(k_check_state, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(((2 * NP + 31) / 32) * sizeof(uint32_t)));
     if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
     if (err != cudaSuccess) {
         set_error("engine upload: %s", cudaGetErrorString(err));
@@ -2904,6 +3031,21 @@ int qpm_engine_partials_write(qpm_engine *h, int rank, const double *host_in) {
     QPM_CUDA_TRY(cudaMemcpyAsync(e->gpart + rank * n, host_in, sizeof(double) * n, cudaMemcpyHostToDevice,
                                  e->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return QPM_OK;
+}
+
+int qpm_engine_check_status(qpm_engine *h, uint32_t *flags, uint32_t *detail) {
+    QPM_ARG_CHECK(h && flags, "engine, flags");
+    Engine *e = h->e;
+    if (!e->check_err) {
+        set_error("qpm_engine_check_status: library built without QPM_CHECKS");
+        return QPM_ERR_STATE;
+    }
+    uint32_t w[2];
+    QPM_CUDA_TRY(cudaMemcpyAsync(w, e->check_err, sizeof(w), cudaMemcpyDeviceToHost, e->stream));
+    QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    *flags = w[0];
+    if (detail) *detail = w[1];
     return QPM_OK;
 }
 

@@ -61,6 +61,7 @@ TABLE = [("us", "gpu__time_duration.sum", 1e-3), ("DRAM_rd_MB", "dram__bytes_rea
          ("FP64%", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1),
          ("issue%", "smsp__issue_active.avg.pct_of_peak_sustained_active", 1),
          ("warps%", "sm__warps_active.avg.pct_of_peak_sustained_active", 1),
+         ("smem%", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", 1),
          ("regs", "launch__registers_per_thread", 1), ("grid", "launch__grid_size", 1)]
 
 

@@ -1,6 +1,6 @@
 """Repeat one C2-shape run several times and print a digest of each trace (determinism probe).
 
-    python tools/race_probe.py N 'QPM_WOLF=planner,QPM_PLAN_CTAS=592' [G]
+    python tools/race_probe.py N 'QPM_WOLF=planner,QPM_PLAN_CTAS=592' [G] [SEG_CHUNKS]
 """
 import hashlib
 import os
@@ -19,8 +19,10 @@ def main():
         k, v = kv.split("=")
         os.environ[k] = v
     G = int(sys.argv[3]) if len(sys.argv) > 3 else 300
+    seg = int(sys.argv[4]) if len(sys.argv) > 4 else None  # fitness segment length (chunks)
     torch.cuda.set_device(0)
-    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, 10_000)
+    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, 10_000,
+                           seg_chunks=seg)
     ref = None
     for r in range(n):
         eng = q.Engine(obj, "hybrid", pop_size=1024, generations=1000, seed=0, de=q.DEParams(), gwo=q.GWOParams(),

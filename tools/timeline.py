@@ -41,6 +41,8 @@ def main():
     eng = q.Engine(obj, args.algo, pop_size=args.np, generations=args.warm + args.gens + 10, seed=0,
                    de=q.DEParams(), gwo=q.GWOParams(), sch=q.Schedules())
     eng.init()
+    eng.prepare(max(args.gens, 10))  # graph replays from the first generation (as in bench.py)
+    eng.prepare(1)
     eng.step(args.warm)
     torch.cuda.synchronize()
     for f in fns:
