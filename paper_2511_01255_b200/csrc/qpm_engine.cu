@@ -846,6 +846,7 @@ template <int K>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_rows(RunConsts c, TrialArgs a, int ch) {
     QTRACE(0);
     pdl_wait();
+    pdl_trigger<1>();
     QTRACE_STARTED();
     constexpr int kWarps = kRowThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -877,6 +878,7 @@ template <int K>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts c, TrialArgs a) {
     QTRACE(0);
     pdl_wait();
+    pdl_trigger<1>();
     QTRACE_STARTED();
     const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
@@ -921,6 +923,7 @@ template <int K>
 __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
     QTRACE(4);
     pdl_wait();
+    pdl_trigger<8>();
     QTRACE_STARTED();
     // one thread per (individual, 32-gene word), flattened: short rows (a
     // column shard of a multi-GPU run) leave no idle lanes
@@ -1551,6 +1554,7 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
                                                                unsigned *cnt, uint32_t *__restrict__ slot_tag) {
     QTRACE(MODE == 0 ? 3 : 5);
     pdl_wait();
+    pdl_trigger<4>();
     QTRACE_STARTED();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t r = (int64_t)blockIdx.x * (fs_threads<MODE>() / 32) + warp;
@@ -1608,6 +1612,7 @@ __global__ void k_finalize_best(RunConsts c, EngineState *st, const double *fit)
     block_topk_k(fit, c.NP, 1, top);
     if (threadIdx.x == 0) {
         st->best_idx = top[0];
+        st->best_fit = __ldcg(fit + top[0]);  // read back with the state (one copy)
         st->best_flag = 1;
     }
 }
@@ -2556,7 +2561,10 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         err = cudaMemcpyAsync(e->tree_i, tree_host.data(), sizeof(int32_t) * tree_host.size(), cudaMemcpyHostToDevice,
                               e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->trace, 0, sizeof(double) * (P->G + 1) * 5, e->stream);
-    if (err == cudaSuccess) err = cudaMemsetAsync(e->genome, 0, sizeof(double) * 2 * NP * c.Dp, e->stream);
+    // (the genome pool is not cleared: init_population writes every gene of the
+    // current slots, a spare slot is written whole -- padding included -- by the
+    // trial or the continuous move before it becomes current, and ±1 slots are
+    // read from their bits; clearing cost 30 us at C2, ~4 ms at C3)
     if (err == cudaSuccess) err = cudaMemsetAsync(e->bits, 0, sizeof(uint32_t) * 2 * NP * c.W, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->slot_bin, 0, 2 * NP, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->topk_cnt, 0, sizeof(unsigned), e->stream);
@@ -2801,13 +2809,7 @@ int qpm_engine_read_best(qpm_engine *h, double *genome, int8_t *proj, double *fi
     if (genome) memcpy(genome, g.data(), sizeof(double) * c.D);
     if (proj)
         for (int64_t j = 0; j < c.D; ++j) proj[j] = ((b[j >> 5] >> (j & 31)) & 1u) ? -1 : 1;
-    if (fitness) {
-        if (c.algorithm == QPM_ALGO_GWO) {
-            *fitness = hs.best_fit;
-        } else {
-            QPM_CUDA_TRY(cudaMemcpy(fitness, e->fit + hs.best_idx, sizeof(double), cudaMemcpyDeviceToHost));
-        }
-    }
+    if (fitness) *fitness = hs.best_fit;  // run_gwo: best-ever; else the finalize's top-1
     return QPM_OK;
 }
 

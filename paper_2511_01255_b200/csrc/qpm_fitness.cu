@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kFitThreadsMax) k_fit_fast(const double2 *__re
     }
     QTRACE(1);
     pdl_wait();
+    pdl_trigger<2>();
     QTRACE_STARTED();
     QSTAMP(0);
     const uint4 *rb =

@@ -137,6 +137,19 @@ int launch_fitness(const Problem *p, FitScratch *fs, const uint32_t *bits, int64
 // dependents once every CTA has passed its wait made the C2 generation
 // 119.7 -> 133.3 us; the early-resident k_fit_finish CTAs doubled k_fit_fast.)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Optional early trigger (build knob QPM_PDL_TRIGGER, a bitmask: 1 trial, 2
+// fitness scan, 4 fused finish + selection, 8 wolf apply): the kernel lets its
+// dependent grid launch once every CTA has passed its wait, so the dependent's
+// CTAs are resident when it ends.  Safe because every kernel of the chain
+// waits (griddepcontrol.wait) before touching anything and before exiting:
+// a dependent's wait then covers the whole chain behind it.
+#ifndef QPM_PDL_TRIGGER
+#define QPM_PDL_TRIGGER 0
+#endif
+template <int BIT>
+__device__ __forceinline__ void pdl_trigger() {
+    if (QPM_PDL_TRIGGER & BIT) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // Device-side kernel timeline (development builds with -DQPM_TRACE only):
 // thread 0 of every CTA stamps %globaltimer at entry, after pdl_wait and at

@@ -42,6 +42,7 @@ def main():
     eng = q.Engine(obj, args.algo, pop_size=cfg["NP"], generations=cfg["G"], seed=0, de=q.DEParams(), gwo=gwo,
                    sch=q.Schedules())
     eng.init()
+    eng.prepare(args.gens)  # graph replays in the timed window (as bench.py)
     eng.step(args.warm)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
