@@ -257,18 +257,22 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
                 "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
                 "algorithmic_unit": f"{DE_BYTES_PER_GENE:.3f} B per gene (CR={CR}) x NP*D",
                 "note": "k_de_trial also draws the generation's crossover mask and the first two wolf draws "
-                        "(3 splitmix64 draws per gene, ~57 of its ~130 instructions per gene); it is "
-                        "integer-issue bound, see int_issue (ncu, profiles/r01/ncu_summary_r01_final.txt)"}
-        summ = os.path.join(ROOT, "profiles", "r01", "ncu_summary_r01_final.txt")
+                        "(3 splitmix64 draws per gene, ~19 SASS instructions each, of its ~133 per gene); it is "
+                        "integer-issue bound, see int_issue (ncu, profiles/r02/ncu_summary_r02.txt)"}
+        summ = os.path.join(ROOT, "profiles", "r02", "ncu_summary_r02.txt")
         if os.path.exists(summ):
-            for line in open(summ):  # tools/ncu_summary.py table: ... Minst ALU% FMAheavy% FP64% issue% warps% regs grid
-                if "k_de_trial" in line and not line.startswith("#"):
-                    f = line.split()
-                    roof["int_issue"] = {"issue_active_pct": float(f[-4]), "alu_pipe_pct": float(f[-7]),
-                                         "fmaheavy_pipe_pct_of_elapsed": float(f[-6]),
-                                         "warp_instr_per_launch": float(f[-8]) * 1e6,
+            hdr = None
+            for line in open(summ):  # tools/ncu_summary.py table (first table: the C2 generation)
+                f = line.split()
+                if f and f[0] == "kernel":
+                    hdr = f[1:]
+                elif hdr and "k_de_trial" in line and not line.startswith("#"):
+                    v = dict(zip(hdr, f[-len(hdr):]))
+                    roof["int_issue"] = {"issue_active_pct": float(v["issue%"]), "alu_pipe_pct": float(v["ALU%"]),
+                                         "fmaheavy_pipe_pct_of_elapsed": float(v["FMAheavy%"]),
+                                         "warp_instr_per_launch": float(v["Minst"]) * 1e6,
                                          "source": "ncu --set full, C2 late generation "
-                                                   "(profiles/r01/ncu_summary_r01_final.txt)"}
+                                                   "(profiles/r02/ncu_summary_r02.txt)"}
                     break
     else:
         nbytes = NP * D * 8
