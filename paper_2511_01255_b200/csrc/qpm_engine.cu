@@ -308,7 +308,7 @@ struct PlanArgs {
     uint64_t *keys;    // [2][NP]
     int4 *picks;       // [2][NP]  r1, r2, r3, m
     int32_t *jrand;    // [2][NP]
-    uint32_t *planes;  // [2][NP][W][8]
+    uint32_t *planes;  // [2][NP][W][kPlanes]
 };
 
 // z ^= z >> s with the shifts done as multiplies on the FMA pipe (the ALU
@@ -556,7 +556,7 @@ struct TrialArgs {
     const int4 *picks;       // [2][NP]
     const uint64_t *keys;    // [2][NP]
     const int32_t *jrand;    // [2][NP]
-    uint32_t *planes;        // [2][NP][W][8] wolf planes
+    uint32_t *planes;        // [2][NP][W][kPlanes] wolf planes (P0..P2 stored)
     const int32_t *slot_of, *spare_of;
     const uint32_t *slot_tag;  // [NP] slot_of[i] | slot_bin[slot_of[i]] << 31 (QPM_SLOT_TAG)
     uint8_t *slot_bin;
@@ -565,6 +565,8 @@ struct TrialArgs {
     uint32_t *cbits;  // [NP][W] the generation's candidate sign rows, dense by individual: scored from
                       // here (no slot indirection) and, multi-GPU, all-gathered from here
 };
+
+
 
 // The trial of row i over genes [jc, jc + kDeChunk) with the crossover mask
 // drawn inline (one splitmix64 per gene).  For K > 0 (run_hybrid)
@@ -917,7 +919,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(Run
 
 // ---------------------------------------------------------------- wolf update
 // One thread per (row, 32-gene word), one CTA row per individual: the candidate's sign word from the
-// leaders' words and the row's 8 planes (bit-sliced, ~30 logic ops per 32
+// leaders' words and the row's stored planes P0..P2 (bit-sliced, ~30 logic ops per 32
 // genes).  Leaders do not move (optimizer.py:454).
 template <int K>
 __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
@@ -1712,7 +1714,7 @@ struct Engine {
     double *genome = nullptr;
     uint32_t *bits = nullptr;
     uint8_t *slot_bin = nullptr;
-    uint32_t *planes = nullptr;  // [2][NP][W][8] by generation parity
+    uint32_t *planes = nullptr;  // [2][NP][W][kPlanes] by generation parity (kPlanes = 4)
     uint32_t *cbits = nullptr;   // [NP][W] wolf candidates staged for exchange
     GenThr *gthr = nullptr;
     cudaStream_t side = nullptr;  // low-priority planner stream
@@ -2396,10 +2398,15 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         e->plan_grid = sms * 2;
-        if (const char *v = getenv("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
-        const char *fork = getenv("QPM_PLAN_FORK");
+        // scheduling knobs for A/B measurement and the schedule tests: read
+        // only when QPM_DEV_KNOBS=1 (none changes a result: every combination
+        // reproduces the default trace bit for bit, tests/test_gpu_schedules.py)
+        const bool dev_knobs = getenv("QPM_DEV_KNOBS") && atoi(getenv("QPM_DEV_KNOBS")) != 0;
+        auto knob = [dev_knobs](const char *name) -> const char * { return dev_knobs ? getenv(name) : nullptr; };
+        if (const char *v = knob("QPM_PLAN_CTAS")) e->plan_grid = std::max(1, atoi(v));
+        const char *fork = knob("QPM_PLAN_FORK");
         if (fork) e->plan_after_trial = strcmp(fork, "trial") == 0;
-        if (const char *v = getenv("QPM_WOLF")) {
+        if (const char *v = knob("QPM_WOLF")) {
             e->wolf_in_planner = strcmp(v, "planner") == 0;
             e->wolf_mixed = strcmp(v, "mixed") == 0;
             e->wolf_side = strcmp(v, "side") == 0;
@@ -2409,19 +2416,19 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         // to run); QPM_PLAN_FORK=start keeps the start fork for the
         // race probe (tools/sanitize.sh)
         if (e->wolf_in_planner && !(fork && strcmp(fork, "start") == 0)) e->plan_after_trial = true;
-        if (const char *v = getenv("QPM_PDL")) e->pdl = atoi(v) != 0;
-        if (const char *v = getenv("QPM_GRAPH_GENS")) e->graph_gens = std::min(64, std::max(1, atoi(v)));
-        if (const char *v = getenv("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
+        if (const char *v = knob("QPM_PDL")) e->pdl = atoi(v) != 0;
+        if (const char *v = knob("QPM_GRAPH_GENS")) e->graph_gens = std::min(64, std::max(1, atoi(v)));
+        if (const char *v = knob("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
         e->topk_ctas = (int)std::min<int64_t>(kTopkMaxCtas, std::max<int64_t>(1, c.NP / 2048));
-        if (const char *v = getenv("QPM_TOPK_CTAS")) e->topk_ctas = std::min(kTopkMaxCtas, std::max(1, atoi(v)));
+        if (const char *v = knob("QPM_TOPK_CTAS")) e->topk_ctas = std::min(kTopkMaxCtas, std::max(1, atoi(v)));
         // fused finish + selection: its last CTA runs the whole-population part
         // alone, which pays up to ~2k rows (C2: 116.0 -> 113.8 us per
         // generation; NP 8192: 133 -> 149 us, alternating A/B)
         e->fused_select = c.NP <= 2048;
-        if (const char *v = getenv("QPM_FUSED_SELECT")) e->fused_select = atoi(v) != 0;
-        if (const char *v = getenv("QPM_DE_ITEM")) e->de_item = std::max(128, atoi(v) / 128 * 128);
-        auto cta_knob = [](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
-            if (const char *v = getenv(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
+        if (const char *v = knob("QPM_FUSED_SELECT")) e->fused_select = atoi(v) != 0;
+        if (const char *v = knob("QPM_DE_ITEM")) e->de_item = std::max(128, atoi(v) / 128 * 128);
+        auto cta_knob = [&knob](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
+            if (const char *v = knob(name)) dst = std::min(kCtaThreads, std::max(32, atoi(v) / 32 * 32));
         };
         cta_knob("QPM_TOPK_THREADS", e->topk_threads);
         cta_knob("QPM_STATS_THREADS", e->stats_threads);

@@ -380,8 +380,11 @@ constexpr uint32_t kChunkBytes = kChunkEntries * sizeof(double2);
 constexpr int kFitBufs = QPM_FIT_BUFS;  // table chunks in flight (a whole C2 segment is staged at once)
 constexpr int kFitSmem = kFitBufs * kChunkBytes;  // dynamic shared memory (48 KB)
 
+#ifndef QPM_FIT_MINB
+#define QPM_FIT_MINB 1  // (3: <= 85 registers; measured at the C5 shape)
+#endif
 template <bool THG>
-__global__ void __launch_bounds__(kFitThreadsMax) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,
+__global__ void __launch_bounds__(kFitThreadsMax, QPM_FIT_MINB) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,
                                                           int64_t nchunks, int seg_chunks, int S,
                                                           const uint32_t *bits, int64_t W,
                                                           const int32_t *row_index, int64_t rows,

@@ -191,7 +191,32 @@ def adaptive_f_update(state: AdaptiveState, params: DEParams, schedules: Schedul
 # ---------------------------------------------------------------------------
 
 def schedule_table(generations: int, de: DEParams, gwo: GWOParams, sch: Schedules) -> np.ndarray:
-    """[G+1, 8] per-generation scalars, computed with the reference's Python expressions."""
+    """[G+1, 8] per-generation scalars with the reference's float arithmetic.
+
+    Elementwise IEEE operations are done by numpy in the order the reference's
+    Python expressions use (bit-identical); the cosine envelope keeps Python's
+    math.cos (optimizer.py:290), which numpy's cos may differ from by an ulp."""
+    G = int(generations)
+    tab = np.zeros((G + 1, _native.SCHED_COLS), dtype=np.float64)
+    if G > 0:
+        prog = np.arange(G + 1, dtype=np.float64) / float(G)  # g / G, correctly rounded like Python's
+    else:
+        prog = np.zeros(1)
+    cos = np.array([math.cos(0.5 * math.pi * float(p)) for p in prog])
+    tab[:, _native.SCHED_F_ENV] = de.f_min + (de.f_max - de.f_min) * cos
+    tab[:, _native.SCHED_DECAY] = 1.0 - sch.decay_strength * prog * prog
+    if G > 0:
+        rest = 1.0 - prog
+        tab[:, _native.SCHED_P_DIST] = sch.p_dist0 * rest
+        tab[:, _native.SCHED_P_SL] = sch.p_sl0 * rest
+        tab[:, _native.SCHED_P_FLIP] = sch.p_flip0 * rest
+    tab[:, _native.SCHED_EARLY] = np.where(prog < sch.phase_split, 1.0, 0.0)
+    tab[:, _native.SCHED_A_NOW] = gwo.a_final + (gwo.a - gwo.a_final) * (1.0 - prog)
+    return tab
+
+
+def _schedule_table_reference(generations: int, de: DEParams, gwo: GWOParams, sch: Schedules) -> np.ndarray:
+    """The same table by the reference's per-generation Python expressions (tests compare the two)."""
     G = int(generations)
     tab = np.zeros((G + 1, _native.SCHED_COLS), dtype=np.float64)
     for g in range(G + 1):
@@ -345,10 +370,17 @@ def _check_wolf_rates(sch: Schedules, generations: int) -> None:
     rate leaves [0, 1]; the device takes the rates from a precomputed table, so
     the same check runs here, before generation 0, with the same message."""
     G = int(generations)
-    for g in range(1, G + 1):
-        for name, v in (("p_dist", sch.p_dist(g, G)), ("p_sl", sch.p_sl(g, G)), ("p_flip", sch.p_flip(g, G))):
-            if not (0.0 <= v <= 1.0):
-                raise ValueError(f"{name} must be in [0, 1], got {v}")
+    if G < 1:
+        return
+    rest = 1.0 - np.arange(1, G + 1, dtype=np.float64) / float(G)  # the rates p0 (1 - g/G), g = 1..G
+    for name, p0 in (("p_dist", sch.p_dist0), ("p_sl", sch.p_sl0), ("p_flip", sch.p_flip0)):
+        v = p0 * rest
+        bad = np.nonzero(~((v >= 0.0) & (v <= 1.0)))[0]
+        if bad.size:  # the first failing generation, in GWOParams' field order at that generation
+            g = int(bad[0]) + 1
+            for nm, val in (("p_dist", sch.p_dist(g, G)), ("p_sl", sch.p_sl(g, G)), ("p_flip", sch.p_flip(g, G))):
+                if not (0.0 <= val <= 1.0):
+                    raise ValueError(f"{nm} must be in [0, 1], got {val}")
 
 
 def _run(algorithm, objective, *, dimension, pop_size, generations, seed, de, gwo, sch, workers, bounds,

@@ -29,6 +29,7 @@ def main():
     from paper_2511_01255_b200 import _native
 
     torch.cuda.set_device(0)
+    os.environ["QPM_DEV_KNOBS"] = "1"  # the runs below pick scheduling knobs
     out = []
     for k, r in enumerate(RUNS):
         for key in ("QPM_WOLF", "QPM_PLAN_FORK"):

@@ -28,6 +28,7 @@ def q():
 def _trace(q, monkeypatch, env, algorithm="hybrid", D=3000, NP=96, G=40, leaders=4, mode="fast", graph=True):
     for k in KNOBS:
         monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("QPM_DEV_KNOBS", "1")  # the library reads its scheduling knobs only with this set
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, D, mode=mode)

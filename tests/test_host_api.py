@@ -157,3 +157,15 @@ def test_reduce_best_host_validation():
         reduce_best(np.arange(100.0), 65)
     with pytest.raises(ValueError, match="workers"):
         reduce_best([1.0, 2.0], 1, workers=0)
+
+
+def test_schedule_table_vectorised_equals_reference_expressions():
+    """The per-generation scalars uploaded to the device are the reference's
+    Python expressions (optimizer.py:157-171, 290, 563-564), bit for bit."""
+    from paper_2511_01255_b200.optimizer import _schedule_table_reference, schedule_table
+
+    for G in (0, 1, 2, 3, 7, 20, 999, 1000, 4097):
+        for sch in (q.Schedules(), q.Schedules(phase_split=0.3, decay_strength=0.7, p_dist0=0.3, p_flip0=0.9)):
+            for gwo in (q.GWOParams(), q.GWOParams(a=0.1, a_final=0.01)):
+                de = q.DEParams(f_min=0.02, f_max=0.3, f=0.1)
+                assert np.array_equal(schedule_table(G, de, gwo, sch), _schedule_table_reference(G, de, gwo, sch))

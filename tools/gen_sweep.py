@@ -13,6 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
+    os.environ.setdefault("QPM_DEV_KNOBS", "1")  # scheduling knobs are read only with this set
     import numpy as np
     import torch
 

@@ -16,6 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
+    os.environ.setdefault("QPM_DEV_KNOBS", "1")  # scheduling knobs are read only with this set
     ap = argparse.ArgumentParser()
     ap.add_argument("--gens", type=int, default=30)
     ap.add_argument("--np", type=int, default=1024)
