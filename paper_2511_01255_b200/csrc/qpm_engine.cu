@@ -49,6 +49,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -2252,13 +2253,70 @@ static int enqueue_generation(Engine *e, int *launches, StageMarks *pm = nullptr
     return QPM_OK;
 }
 
+// Process-wide pool of the planner's side streams and fork/join events:
+// engines created and destroyed back to back (run_hybrid in a loop, trials)
+// reuse them instead of creating a stream and four events per run.
+struct SideSet {
+    int device;
+    cudaStream_t side;
+    cudaEvent_t ev[4];
+};
+static std::mutex g_side_mu;
+static std::vector<SideSet> g_side_pool;
+
+static int side_acquire(Engine *e) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_side_mu);
+        for (size_t k = 0; k < g_side_pool.size(); ++k)
+            if (g_side_pool[k].device == dev) {
+                const SideSet ss = g_side_pool[k];
+                g_side_pool[k] = g_side_pool.back();
+                g_side_pool.pop_back();
+                e->side = ss.side;
+                e->ev_fork = ss.ev[0], e->ev_join = ss.ev[1], e->ev_wfork = ss.ev[2], e->ev_wjoin = ss.ev[3];
+                return QPM_OK;
+            }
+    }
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
+    if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_wfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_wjoin, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("planner stream/event creation failed");
+        return QPM_ERR_CUDA;
+    }
+    return QPM_OK;
+}
+
+// (the side stream is idle: engine_free synchronised it)
+static void side_release(Engine *e) {
+    if (!e->side) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (e->ev_fork && e->ev_join && e->ev_wfork && e->ev_wjoin) {
+        std::lock_guard<std::mutex> lk(g_side_mu);
+        if (g_side_pool.size() < 64) {
+            g_side_pool.push_back({dev, e->side, {e->ev_fork, e->ev_join, e->ev_wfork, e->ev_wjoin}});
+            e->side = nullptr;
+            e->ev_fork = e->ev_join = e->ev_wfork = e->ev_wjoin = nullptr;
+            return;
+        }
+    }
+    cudaStreamDestroy(e->side);
+    e->side = nullptr;
+}
+
 static void engine_free(Engine *e) {
     // the buffers go back to the block cache: nothing queued may still use them
     if (e->stream) cudaStreamSynchronize(e->stream);
     if (e->owns_stream && e->stream) cudaStreamDestroy(e->stream);
     if (e->side) {
         cudaStreamSynchronize(e->side);
-        cudaStreamDestroy(e->side);
+        side_release(e);  // back to the pool (with its events), or destroyed
     }
     if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
@@ -2324,18 +2382,9 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         }
         e->owns_stream = true;
     }
-    {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
-        if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
-            cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&e->ev_wfork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&e->ev_wjoin, cudaEventDisableTiming) != cudaSuccess) {
-            set_error("planner stream/event creation failed");
-            engine_free(e);
-            return QPM_ERR_CUDA;
-        }
+    if (side_acquire(e) != QPM_OK) {
+        engine_free(e);
+        return QPM_ERR_CUDA;
     }
     RunConsts &c = e->c;
     c.algorithm = P->algorithm;
@@ -2558,15 +2607,36 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         gth[g].early = sg[QPM_SCHED_EARLY] != 0.0 ? 1u : 0u;
         gth[g].pad = 0;
     }
-    cudaError_t err = cudaMemcpyAsync(e->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, e->stream);
-    if (err == cudaSuccess)
-        err = cudaMemcpyAsync(e->gthr, gth.data(), sizeof(GenThr) * gth.size(), cudaMemcpyHostToDevice, e->stream);
-    if (err == cudaSuccess)
-        err = cudaMemcpyAsync(e->sched, sched, sizeof(double) * (P->G + 1) * QPM_SCHED_COLS, cudaMemcpyHostToDevice,
-                              e->stream);
-    if (err == cudaSuccess)
-        err = cudaMemcpyAsync(e->tree_i, tree_host.data(), sizeof(int32_t) * tree_host.size(), cudaMemcpyHostToDevice,
-                              e->stream);
+    // the uploads go through a pinned per-thread staging buffer: asynchronous
+    // copies (a pageable source makes every cudaMemcpyAsync a staged,
+    // synchronous copy); the stream synchronisation below ends its use
+    const size_t b_st = sizeof(hs), b_gth = sizeof(GenThr) * gth.size(),
+                 b_sched = sizeof(double) * (P->G + 1) * QPM_SCHED_COLS, b_tree = sizeof(int32_t) * tree_host.size();
+    const size_t o_gth = round_up((int64_t)b_st, 256), o_sched = o_gth + round_up((int64_t)b_gth, 256),
+                 o_tree = o_sched + round_up((int64_t)b_sched, 256), b_all = o_tree + b_tree;
+    static thread_local char *pinned = nullptr;
+    static thread_local size_t pinned_bytes = 0;
+    if (pinned_bytes < b_all) {
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        pinned_bytes = 0;
+        if (cudaMallocHost(&pinned, std::max<size_t>(b_all, (size_t)1 << 20)) == cudaSuccess)
+            pinned_bytes = std::max<size_t>(b_all, (size_t)1 << 20);
+    }
+    const char *src_st = reinterpret_cast<const char *>(&hs), *src_gth = reinterpret_cast<const char *>(gth.data()),
+               *src_sched = reinterpret_cast<const char *>(sched),
+               *src_tree = reinterpret_cast<const char *>(tree_host.data());
+    if (pinned) {
+        memcpy(pinned, &hs, b_st);
+        memcpy(pinned + o_gth, gth.data(), b_gth);
+        memcpy(pinned + o_sched, sched, b_sched);
+        memcpy(pinned + o_tree, tree_host.data(), b_tree);
+        src_st = pinned, src_gth = pinned + o_gth, src_sched = pinned + o_sched, src_tree = pinned + o_tree;
+    }
+    cudaError_t err = cudaMemcpyAsync(e->st, src_st, b_st, cudaMemcpyHostToDevice, e->stream);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(e->gthr, src_gth, b_gth, cudaMemcpyHostToDevice, e->stream);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(e->sched, src_sched, b_sched, cudaMemcpyHostToDevice, e->stream);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(e->tree_i, src_tree, b_tree, cudaMemcpyHostToDevice, e->stream);
     if (err == cudaSuccess) err = cudaMemsetAsync(e->trace, 0, sizeof(double) * (P->G + 1) * 5, e->stream);
     // (the genome pool is not cleared: init_population writes every gene of the
     // current slots, a spare slot is written whole -- padding included -- by the

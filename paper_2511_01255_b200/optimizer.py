@@ -236,6 +236,18 @@ def _schedule_table_reference(generations: int, de: DEParams, gwo: GWOParams, sc
 # engine wrapper
 # ---------------------------------------------------------------------------
 
+_STREAMS: dict = {}  # device index -> idle high-priority streams (reused by later engines)
+
+
+def _stream_acquire(dev):
+    import torch
+
+    free = _STREAMS.setdefault(dev.index, [])
+    if free:
+        return free.pop()
+    return torch.cuda.Stream(dev, priority=min(torch.cuda.Stream.priority_range()))
+
+
 class Engine:
     """One device-resident run (thin owner of a qpm_engine handle)."""
 
@@ -255,8 +267,9 @@ class Engine:
         self.D = objective.dimension
         # a dedicated high-priority stream (CUDA graphs cannot be captured on the
         # legacy default stream; the engine's planner runs on a low-priority one)
+        self._pooled = stream is None
         if stream is None:
-            stream = torch.cuda.Stream(dev, priority=min(torch.cuda.Stream.priority_range()))
+            stream = _stream_acquire(dev)
         self.stream = stream
         mode = fitness_mode or objective.mode
         from .objectives import MODES
@@ -293,10 +306,12 @@ class Engine:
         h = getattr(self, "handle", None)
         if h is not None and h.value:
             try:
-                _native.lib().qpm_engine_destroy(h)
+                _native.lib().qpm_engine_destroy(h)  # synchronises the engine's stream
             except Exception:
                 pass
             self.handle = None
+            if getattr(self, "_pooled", False):
+                _STREAMS.setdefault(self.stream.device.index, []).append(self.stream)
 
     def init(self):
         _native.check(_native.lib().qpm_engine_init(self.handle), "qpm_engine_init")
