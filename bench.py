@@ -293,7 +293,8 @@ def fitness_kernel_roofline(q, torch, sm_count, peaks, iters=20):
     at the fitness-roofline shape north_star quotes its FP64 target on (C5:
     4,092 candidate rows = one generation of NP 2,048, 64 pump wavelengths,
     D = 2*10^4, multi_thg) and at the C2 engine shape (1,020 rows, one
-    wavelength, D = 10^4).  Random sign rows resident in HBM."""
+    wavelength, D = 10^4).  Random sign rows resident in HBM; each launch is the
+    segment scan + finish, `iters` of them replayed from one CUDA graph."""
     out = []
     for tag, rows, d, nwl, thick in (("C5", 2 * 2048 - 4, 20_000, 64, 0.5), ("C2", NP - 4, D, 1, THICKNESS_UM)):
         pumps = tuple(float(w) for w in np.linspace(1380.0, 1430.0, nwl)) if nwl > 1 else (PUMP_NM,)
@@ -310,14 +311,23 @@ def fitness_kernel_roofline(q, torch, sm_count, peaks, iters=20):
         s = torch.cuda.Stream()
         for _ in range(3):
             obj.evaluate_bits(bits, res, stream=s)
+        torch.cuda.synchronize()
+        # `iters` launches replayed from one CUDA graph: the C2-shape scan
+        # (~6 us) is shorter than a host-side launch through the API
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            for _ in range(iters):
+                obj.evaluate_bits(bits, res, stream=s)
+        graph.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(s)
-        for _ in range(iters):
-            obj.evaluate_bits(bits, res, stream=s)
+        with torch.cuda.stream(s):
+            graph.replay()
         e1.record(s)
         torch.cuda.synchronize()
         sec = e0.elapsed_time(e1) * 1e-3 / iters
+        del graph
         evals = rows * d * nwl
         achieved = evals * FLOP_PER_EVAL / sec / 1e12
         peak = sm_count * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
