@@ -160,12 +160,19 @@ class TestObjectives:
         assert obj.gains(signs)[0] == pytest.approx(30.0, rel=1e-12)
         assert obj.normalized_gains(signs)[0] == pytest.approx(1.0, rel=1e-12)
 
-    def test_monotone_in_each_gain_below_g0(self, q):
-        base = q.multi_objective([1.0, 2.0, 3.0], g0=5.0, beta=0.5)
-        for k in range(3):
-            g = [1.0, 2.0, 3.0]
-            g[k] += 0.5
-            assert q.multi_objective(g, g0=5.0, beta=0.5) < base or k == 2
+    def test_multi_objective_formula(self, q):
+        assert q.multi_objective([3.0, 3.0], g0=10.0, beta=1.0) == pytest.approx(14.0)
+        assert q.multi_objective([2.0, 4.0], g0=10.0, beta=2.0) == pytest.approx(18.0)
+        assert q.multi_objective([4.0], g0=10.0, beta=0.0) == pytest.approx(6.0)
+        assert q.multi_objective([0.2, 0.35, 0.4], g0=2.0, beta=1.0) < q.multi_objective([0.2, 0.3, 0.4], g0=2.0,
+                                                                                         beta=1.0)
+        assert q.multi_objective([0.3, 0.3], g0=2.0, beta=1.0) < q.multi_objective([0.2, 0.4], g0=2.0, beta=1.0)
+
+    def test_single_multi_consistency(self, q):
+        spec = q.ObjectiveSpec("single_thg", (1404.0,))
+        provider = q.MismatchTable({1404.0: q.PhaseMismatchPair(0.3, 0.7)})
+        single = q.fitness_single(q.DomainPattern(1.0, np.ones(12, dtype=np.int8)), spec, provider)
+        assert abs(-q.multi_objective([single], g0=0.0, beta=0.0)) == pytest.approx(single)
 
 
 # ------------------------------------------------------------ test_rng.py (device fill)
