@@ -260,6 +260,17 @@ int qpm_engine_partials_write(qpm_engine *e, int rank, const double *host_in);
  * further steps.  Replaces the reference's BatchEvaluationError failure
  * contract (parexec.py:27-33) on the multi-GPU path. */
 int qpm_engine_wait(qpm_engine *e, int64_t timeout_ms);
+/* Checkpoint / resume (the counter RNG needs no state): a
+ * synchronous host snapshot of an initialised engine -- state (g, F, window,
+ * baseline std, leaders, best-ever), fitness, trace rows 0..g, the current
+ * individuals (genome rows, sign bits, ±1 flags) in individual order and the
+ * best-row buffer.  qpm_engine_restore loads it into a freshly created engine
+ * of the same run (algorithm, mode, NP, D, G, seed, schedule, shard) in place
+ * of qpm_engine_init; the resumed run is bit-identical to an uninterrupted
+ * one.  No reference counterpart (the reference has no mid-run checkpoint). */
+int64_t qpm_engine_checkpoint_bytes(const qpm_engine *e);
+int qpm_engine_checkpoint(qpm_engine *e, void *host_buf, int64_t bytes);
+int qpm_engine_restore(qpm_engine *e, const void *host_buf, int64_t bytes);
 /* Invariant checks (builds with -DQPM_CHECKS=1, libqpm_b200_checks.so): after
  * every generation a kernel verifies the slot permutation, the planner's DE
  * picks and j_rand, the leaders, finite fitness and trace, and the planner's

@@ -29,7 +29,8 @@ EXPORTS = (
     "qpm_engine_init_finish",
     "qpm_engine_phases", "qpm_engine_run_phase", "qpm_engine_exchange_from", "qpm_engine_cand_ptr",
     "qpm_engine_stream", "qpm_engine_partials_info", "qpm_engine_partials_read", "qpm_engine_partials_write",
-    "qpm_engine_wait", "qpm_engine_check_status",
+    "qpm_engine_wait", "qpm_engine_check_status", "qpm_engine_checkpoint_bytes", "qpm_engine_checkpoint",
+    "qpm_engine_restore",
 )
 
 
@@ -130,6 +131,9 @@ def lib():
         "qpm_engine_partials_write": (I32, [P, I32, P]),
         "qpm_engine_wait": (I32, [P, I64]),
         "qpm_engine_check_status": (I32, [P, P, P]),
+        "qpm_engine_checkpoint_bytes": (I64, [P]),
+        "qpm_engine_checkpoint": (I32, [P, P, I64]),
+        "qpm_engine_restore": (I32, [P, P, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1622,6 +1622,49 @@ __global__ void k_finalize_best(RunConsts c, EngineState *st, const double *fit)
 
 __global__ void k_reset_flag(EngineState *st) { st->best_flag = 0; }
 
+// ---------------------------------------------------------------- checkpoint
+// Checkpoint / resume (a checkpoint is (g, F, window,
+// baseline_std, genome, fitness, best_prev); the counter RNG has no state).
+// The current individuals are gathered in individual order (±1 rows expanded
+// to f64, with their flags) and scattered back into slots 0..NP-1 on restore:
+// slot numbers carry no meaning, so the resumed run is bit-identical.
+__global__ void k_gather_rows(RunConsts c, const int32_t *slot_of, const uint8_t *slot_bin, const double *genome,
+                              const uint32_t *bits, double *out_g, uint32_t *out_b, uint8_t *out_bin) {
+    const int64_t i = blockIdx.y;
+    const int64_t slot = slot_of[i];
+    const RowRef r = row_ref(c, slot, slot_bin, genome, bits);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c.Dp; j += (int64_t)gridDim.x * blockDim.x) {
+        out_g[i * c.Dp + j] = j < c.D ? r.at((int)j) : 0.0;
+        if (j < c.W) out_b[i * c.W + j] = bits[slot * c.W + j];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out_bin[i] = slot_bin[slot];
+}
+
+__global__ void k_scatter_rows(RunConsts c, const double *in_g, const uint32_t *in_b, const uint8_t *in_bin,
+                               int32_t *slot_of, int32_t *spare_of, uint32_t *slot_tag, uint8_t *slot_bin,
+                               double *genome, uint32_t *bits) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c.Dp; j += (int64_t)gridDim.x * blockDim.x) {
+        genome[i * c.Dp + j] = in_g[i * c.Dp + j];
+        if (j < c.W) bits[i * c.W + j] = in_b[i * c.W + j];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint8_t bin = in_bin[i];
+        slot_of[i] = (int32_t)i;
+        spare_of[i] = (int32_t)(c.NP + i);
+        slot_bin[i] = bin;
+        slot_bin[c.NP + i] = 0;
+        if (slot_tag) slot_tag[i] = (uint32_t)i | (bin ? kBinTag : 0u);
+    }
+}
+
+struct CkptHeader {
+    char magic[8];  // "QPMCKPT1"
+    int32_t version, algorithm, fitness_mode, rank;
+    int32_t world, pad;
+    int64_t NP, D, W, G, seed, g0, g_done;
+};
+
 // ---------------------------------------------------------------- state checks
 // QPM_CHECKS builds (libqpm_b200_checks.so, tests/test_gpu_checks.py): after
 // every generation one CTA verifies the engine's invariants and records the
@@ -3110,6 +3153,139 @@ int qpm_engine_partials_write(qpm_engine *h, int rank, const double *host_in) {
     QPM_CUDA_TRY(cudaMemcpyAsync(e->gpart + rank * n, host_in, sizeof(double) * n, cudaMemcpyHostToDevice,
                                  e->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return QPM_OK;
+}
+
+static int64_t ckpt_bytes(const Engine *e) {
+    const RunConsts &c = e->c;
+    return (int64_t)sizeof(CkptHeader) + (int64_t)sizeof(EngineState) + c.NP * 8 /* fit */ +
+           (e->g_done + 1) * 5 * 8 /* trace */ + c.NP /* bin flags */ + c.NP * c.W * 4 + c.NP * c.Dp * 8 +
+           c.Dp * 8 + c.W * 4 /* best row */;
+}
+
+int64_t qpm_engine_checkpoint_bytes(const qpm_engine *h) { return h ? ckpt_bytes(h->e) : -1; }
+
+int qpm_engine_checkpoint(qpm_engine *h, void *host_buf, int64_t bytes) {
+    QPM_ARG_CHECK(h && host_buf, "engine, buffer");
+    Engine *e = h->e;
+    const RunConsts &c = e->c;
+    if (!e->initialized) {
+        set_error("qpm_engine_checkpoint before qpm_engine_init");
+        return QPM_ERR_STATE;
+    }
+    QPM_ARG_CHECK(bytes >= ckpt_bytes(e), "buffer smaller than qpm_engine_checkpoint_bytes()");
+    QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (e->side) QPM_CUDA_TRY(cudaStreamSynchronize(e->side));
+    char *p = static_cast<char *>(host_buf);
+    CkptHeader hd{};
+    memcpy(hd.magic, "QPMCKPT1", 8);
+    hd.version = 1;
+    hd.algorithm = c.algorithm;
+    hd.fitness_mode = e->P.fitness_mode;
+    hd.rank = e->rank;
+    hd.world = e->world;
+    hd.NP = c.NP, hd.D = c.D, hd.W = c.W, hd.G = c.G, hd.seed = (int64_t)c.seed, hd.g0 = c.g0, hd.g_done = e->g_done;
+    memcpy(p, &hd, sizeof(hd));
+    p += sizeof(hd);
+    QPM_CUDA_TRY(cudaMemcpy(p, e->st, sizeof(EngineState), cudaMemcpyDeviceToHost));
+    p += sizeof(EngineState);
+    QPM_CUDA_TRY(cudaMemcpy(p, e->fit, c.NP * 8, cudaMemcpyDeviceToHost));
+    p += c.NP * 8;
+    QPM_CUDA_TRY(cudaMemcpy(p, e->trace, (e->g_done + 1) * 5 * 8, cudaMemcpyDeviceToHost));
+    p += (e->g_done + 1) * 5 * 8;
+    const size_t gb = (size_t)c.NP * c.Dp * 8, bb = (size_t)c.NP * c.W * 4;
+    double *tg = (double *)dev_cache_alloc(gb);
+    uint32_t *tb = (uint32_t *)dev_cache_alloc(bb);
+    uint8_t *tf = (uint8_t *)dev_cache_alloc((size_t)c.NP);
+    int rc = QPM_OK;
+    if (!tg || !tb || !tf) {
+        set_error("out of device memory for the checkpoint staging");
+        rc = QPM_ERR_CUDA;
+    } else {
+        k_gather_rows<<<dim3(4, (unsigned)c.NP), 256, 0, e->stream>>>(c, e->slot_of, e->slot_bin, e->genome, e->bits, tg,
+                                                                     tb, tf);
+        if (cudaGetLastError() != cudaSuccess || cudaMemcpyAsync(p, tf, c.NP, cudaMemcpyDeviceToHost, e->stream) ||
+            cudaMemcpyAsync(p + c.NP, tb, bb, cudaMemcpyDeviceToHost, e->stream) ||
+            cudaMemcpyAsync(p + c.NP + bb, tg, gb, cudaMemcpyDeviceToHost, e->stream) ||
+            cudaMemcpyAsync(p + c.NP + bb + gb, e->best_genome, c.Dp * 8, cudaMemcpyDeviceToHost, e->stream) ||
+            cudaMemcpyAsync(p + c.NP + bb + gb + c.Dp * 8, e->best_bits, c.W * 4, cudaMemcpyDeviceToHost, e->stream) ||
+            cudaStreamSynchronize(e->stream) != cudaSuccess) {
+            set_error("checkpoint copy failed");
+            rc = QPM_ERR_CUDA;
+        }
+    }
+    cudaStreamSynchronize(e->stream);
+    dev_cache_release(tg, gb);
+    dev_cache_release(tb, bb);
+    dev_cache_release(tf, (size_t)c.NP);
+    return rc;
+}
+
+int qpm_engine_restore(qpm_engine *h, const void *host_buf, int64_t bytes) {
+    QPM_ARG_CHECK(h && host_buf, "engine, buffer");
+    Engine *e = h->e;
+    const RunConsts &c = e->c;
+    if (e->initialized || e->init_pending) {
+        set_error("qpm_engine_restore needs a freshly created engine (not initialised)");
+        return QPM_ERR_STATE;
+    }
+    const char *p = static_cast<const char *>(host_buf);
+    QPM_ARG_CHECK(bytes >= (int64_t)sizeof(CkptHeader), "buffer too small for a checkpoint");
+    CkptHeader hd;
+    memcpy(&hd, p, sizeof(hd));
+    QPM_ARG_CHECK(memcmp(hd.magic, "QPMCKPT1", 8) == 0 && hd.version == 1, "not a qpm engine checkpoint");
+    QPM_ARG_CHECK(hd.algorithm == c.algorithm && hd.fitness_mode == e->P.fitness_mode && hd.NP == c.NP &&
+                      hd.D == c.D && hd.W == c.W && hd.G == c.G && hd.seed == (int64_t)c.seed && hd.g0 == c.g0 &&
+                      hd.rank == e->rank && hd.world == e->world,
+                  "checkpoint of a different run (algorithm, mode, NP, D, G, seed or shard)");
+    QPM_ARG_CHECK(hd.g_done >= 0 && hd.g_done <= c.G, "checkpoint generation outside [0, G]");
+    e->g_done = hd.g_done;
+    QPM_ARG_CHECK(bytes >= ckpt_bytes(e), "truncated checkpoint");
+    p += sizeof(hd);
+    EngineState hs;
+    memcpy(&hs, p, sizeof(hs));
+    p += sizeof(hs);
+    hs.g_plan = hs.g;  // the planner re-draws the next generation below
+    QPM_CUDA_TRY(cudaMemcpyAsync(e->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, e->stream));
+    QPM_CUDA_TRY(cudaMemcpyAsync(e->fit, p, c.NP * 8, cudaMemcpyHostToDevice, e->stream));
+    p += c.NP * 8;
+    QPM_CUDA_TRY(cudaMemcpyAsync(e->trace, p, (hd.g_done + 1) * 5 * 8, cudaMemcpyHostToDevice, e->stream));
+    p += (hd.g_done + 1) * 5 * 8;
+    const size_t gb = (size_t)c.NP * c.Dp * 8, bb = (size_t)c.NP * c.W * 4;
+    double *tg = (double *)dev_cache_alloc(gb);
+    uint32_t *tb = (uint32_t *)dev_cache_alloc(bb);
+    uint8_t *tf = (uint8_t *)dev_cache_alloc((size_t)c.NP);
+    int rc = QPM_OK;
+    if (!tg || !tb || !tf) {
+        set_error("out of device memory for the checkpoint staging");
+        rc = QPM_ERR_CUDA;
+    } else if (cudaMemcpyAsync(tf, p, c.NP, cudaMemcpyHostToDevice, e->stream) ||
+               cudaMemcpyAsync(tb, p + c.NP, bb, cudaMemcpyHostToDevice, e->stream) ||
+               cudaMemcpyAsync(tg, p + c.NP + bb, gb, cudaMemcpyHostToDevice, e->stream) ||
+               cudaMemcpyAsync(e->best_genome, p + c.NP + bb + gb, c.Dp * 8, cudaMemcpyHostToDevice, e->stream) ||
+               cudaMemcpyAsync(e->best_bits, p + c.NP + bb + gb + c.Dp * 8, c.W * 4, cudaMemcpyHostToDevice,
+                               e->stream)) {
+        set_error("restore copy failed");
+        rc = QPM_ERR_CUDA;
+    } else {
+        k_scatter_rows<<<dim3(4, (unsigned)c.NP), 256, 0, e->stream>>>(c, tg, tb, tf, e->slot_of, e->spare_of,
+                                                                      e->slot_tag, e->slot_bin, e->genome, e->bits);
+        if (cudaGetLastError() != cudaSuccess) {
+            set_error("restore scatter launch failed");
+            rc = QPM_ERR_CUDA;
+        }
+    }
+    if (rc == QPM_OK && c.algorithm != QPM_ALGO_GWO) rc = enqueue_planner(e, e->stream);  // the next generation's draws
+    if (cudaStreamSynchronize(e->stream) != cudaSuccess && rc == QPM_OK) {
+        set_error("restore failed on the device");
+        rc = QPM_ERR_CUDA;
+    }
+    dev_cache_release(tg, gb);
+    dev_cache_release(tb, bb);
+    dev_cache_release(tf, (size_t)c.NP);
+    if (rc) return rc;
+    e->initialized = true;
+    e->init_pending = false;
     return QPM_OK;
 }
 

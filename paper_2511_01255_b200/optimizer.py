@@ -319,6 +319,19 @@ class Engine:
     def step(self, n: int, use_graph: bool = True):
         _native.check(_native.lib().qpm_engine_step(self.handle, int(n), int(use_graph)), "qpm_engine_step")
 
+    def checkpoint(self) -> bytes:
+        """A host snapshot of the run (qpm_engine_checkpoint); restore() it into a new
+        Engine created with the same arguments to resume bit-identically."""
+        n = int(_native.lib().qpm_engine_checkpoint_bytes(self.handle))
+        buf = np.empty(n, dtype=np.uint8)
+        _native.check(_native.lib().qpm_engine_checkpoint(self.handle, buf.ctypes.data, n), "qpm_engine_checkpoint")
+        return buf.tobytes()
+
+    def restore(self, data: bytes):
+        """Resume from checkpoint() bytes (instead of init())."""
+        buf = np.frombuffer(data, dtype=np.uint8)
+        _native.check(_native.lib().qpm_engine_restore(self.handle, buf.ctypes.data, buf.size), "qpm_engine_restore")
+
     def prepare(self, n: int):
         """Capture and upload the CUDA graphs a step(n) replays (keeps capture out of timed regions)."""
         _native.check(_native.lib().qpm_engine_prepare(self.handle, int(n)), "qpm_engine_prepare")
