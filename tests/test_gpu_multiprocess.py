@@ -123,3 +123,27 @@ def test_nccl_wait_timeout_aborts_and_refuses():
     assert "WAIT-OK" in out, out + res.stderr[-2000:]
     assert "TIMEOUT-RAISED True" in out, out + res.stderr[-2000:]
     assert "STEP-REFUSED True" in out, out + res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("algorithm,world", [("hybrid", 2), ("gwo", 3)])
+def test_distributed_trials_match_single_process(q, tmp_path, algorithm, world):
+    """run_trials(group=WORLD): each process runs its share of the seeds on the
+    real engine (all on cuda:0 here; one GPU per rank in production) and every
+    rank returns the single-process records and statistics bit for bit."""
+    trials, seed, D, NP, G = 7, 3, 300, 24, 30
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mp_trials_worker.py"), "--out", str(tmp_path), "--algorithm", algorithm,
+           "--trials", str(trials), "--seed", str(seed), "--D", str(D), "--NP", str(NP), "--G", str(G)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    ranks = [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(world)]
+    assert len({int(r["pid"]) for r in ranks}) == world
+    obj = q.make_objective(q.ObjectiveSpec("single_thg", (1404.0,)), q.default_dispersion(), 1.0, D)
+    stats, recs = q.run_trials(obj, algorithm, trials, seed, dimension=D, pop_size=NP, generations=G)
+    for r in ranks:
+        assert list(r["trial"]) == list(range(trials))
+        assert list(r["final"]) == [x.final_fitness for x in recs]
+        assert list(r["deff"]) == [x.deff_norm for x in recs]
+        assert list(r["stats"]) == [stats.trials, stats.average, stats.maximum, stats.minimum, stats.std,
+                                    stats.mean_deff_norm]
