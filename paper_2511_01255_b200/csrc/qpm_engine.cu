@@ -2387,6 +2387,22 @@ using namespace qpm;
 
 extern "C" {
 
+// A per-thread pinned host buffer of at least `bytes` (nullptr when pinned
+// memory is unavailable: callers then copy through pageable memory).  Used
+// between an enqueue and the stream synchronisation that ends its use.
+static char *pinned_staging(size_t bytes) {
+    static thread_local char *pinned = nullptr;
+    static thread_local size_t pinned_bytes = 0;
+    if (pinned_bytes < bytes) {
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        pinned_bytes = 0;
+        const size_t want = std::max<size_t>(bytes, (size_t)1 << 20);
+        if (cudaMallocHost(&pinned, want) == cudaSuccess) pinned_bytes = want;
+    }
+    return pinned;
+}
+
 int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params *P, const double *sched,
                       void *stream) {
     QPM_ARG_CHECK(out && prob && P && sched, "out, problem, params, sched");
@@ -2657,15 +2673,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
                  b_sched = sizeof(double) * (P->G + 1) * QPM_SCHED_COLS, b_tree = sizeof(int32_t) * tree_host.size();
     const size_t o_gth = round_up((int64_t)b_st, 256), o_sched = o_gth + round_up((int64_t)b_gth, 256),
                  o_tree = o_sched + round_up((int64_t)b_sched, 256), b_all = o_tree + b_tree;
-    static thread_local char *pinned = nullptr;
-    static thread_local size_t pinned_bytes = 0;
-    if (pinned_bytes < b_all) {
-        if (pinned) cudaFreeHost(pinned);
-        pinned = nullptr;
-        pinned_bytes = 0;
-        if (cudaMallocHost(&pinned, std::max<size_t>(b_all, (size_t)1 << 20)) == cudaSuccess)
-            pinned_bytes = std::max<size_t>(b_all, (size_t)1 << 20);
-    }
+    char *pinned = pinned_staging(b_all);
     const char *src_st = reinterpret_cast<const char *>(&hs), *src_gth = reinterpret_cast<const char *>(gth.data()),
                *src_sched = reinterpret_cast<const char *>(sched),
                *src_tree = reinterpret_cast<const char *>(tree_host.data());
@@ -2919,17 +2927,24 @@ int qpm_engine_read_best(qpm_engine *h, double *genome, int8_t *proj, double *fi
     QPM_ARG_CHECK(h, "engine");
     Engine *e = h->e;
     const RunConsts &c = e->c;
-    std::vector<double> g(c.Dp);
-    std::vector<uint32_t> b(c.W);
-    EngineState hs;
-    QPM_CUDA_TRY(cudaMemcpyAsync(g.data(), e->best_genome, sizeof(double) * c.Dp, cudaMemcpyDeviceToHost, e->stream));
-    QPM_CUDA_TRY(cudaMemcpyAsync(b.data(), e->best_bits, sizeof(uint32_t) * c.W, cudaMemcpyDeviceToHost, e->stream));
-    QPM_CUDA_TRY(cudaMemcpyAsync(&hs, e->st, sizeof(hs), cudaMemcpyDeviceToHost, e->stream));
+    // genome, bits and the best fitness through one pinned buffer, one synchronisation
+    const size_t bg = sizeof(double) * c.Dp, bb = sizeof(uint32_t) * c.W;
+    char *pin = pinned_staging(bg + bb + sizeof(double));
+    std::vector<char> pageable;
+    if (!pin) {
+        pageable.resize(bg + bb + sizeof(double));
+        pin = pageable.data();
+    }
+    QPM_CUDA_TRY(cudaMemcpyAsync(pin, e->best_genome, bg, cudaMemcpyDeviceToHost, e->stream));
+    QPM_CUDA_TRY(cudaMemcpyAsync(pin + bg, e->best_bits, bb, cudaMemcpyDeviceToHost, e->stream));
+    QPM_CUDA_TRY(cudaMemcpyAsync(pin + bg + bb, reinterpret_cast<const char *>(e->st) + offsetof(EngineState, best_fit),
+                                 sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
-    if (genome) memcpy(genome, g.data(), sizeof(double) * c.D);
+    const uint32_t *b = reinterpret_cast<const uint32_t *>(pin + bg);
+    if (genome) memcpy(genome, pin, sizeof(double) * c.D);
     if (proj)
         for (int64_t j = 0; j < c.D; ++j) proj[j] = ((b[j >> 5] >> (j & 31)) & 1u) ? -1 : 1;
-    if (fitness) *fitness = hs.best_fit;  // run_gwo: best-ever; else the finalize's top-1
+    if (fitness) memcpy(fitness, pin + bg + bb, sizeof(double));  // run_gwo: best-ever; else the finalize's top-1
     return QPM_OK;
 }
 
