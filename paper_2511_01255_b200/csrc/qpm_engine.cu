@@ -892,6 +892,309 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial(RunConsts
     de_trial_dispatch<K>(c, a, s_row, jc);
 }
 
+// ---------------------------------------------------------------- DE trial, TMA-staged
+// The same trial with its four source rows (x_i, x_r1, x_r2, x_r3) streamed
+// into shared memory by the bulk-copy engine (cp.async.bulk, one elected
+// thread, an mbarrier per stage) kTmaBufs stages ahead of the warps.  The
+// global-load version keeps at most 12 doubles per lane in flight and stalls
+// on them (long scoreboard, 64-register spills of the row pointers); here
+// 4 x 4 KB per stage and kTmaBufs stages per CTA are in flight while the warps
+// compute the stage's mask and wolf draws, which do not depend on the data.
+// A stage is 512 genes: warp w owns genes [64 w, 64 w + 64), lane l genes l
+// and l + 32, exactly the global-load kernel's per-warp step, so every draw,
+// every rounding and every stored word is the same.  Rows that are +/-1 slots
+// (bits only) are staged as their bit words (128 B per 1024 genes).
+#ifndef QPM_DE_TMA
+#define QPM_DE_TMA 1
+#endif
+#ifndef QPM_DE_TMA_STEPS
+#define QPM_DE_TMA_STEPS 2  // 64-gene warp steps per stage (a stage is 512 x this genes)
+#endif
+#ifndef QPM_DE_TMA_BUFS
+#define QPM_DE_TMA_BUFS 2
+#endif
+#ifndef QPM_DE_TMA_MINB
+#define QPM_DE_TMA_MINB 3  // CTAs per SM: 3 x (BUFS x 32 KB) of stage ring
+#endif
+constexpr int kTmaSteps = QPM_DE_TMA_STEPS;
+constexpr int kTmaStage = 512 * kTmaSteps;  // genes per stage
+constexpr int kTmaBufs = QPM_DE_TMA_BUFS;
+constexpr size_t kTmaSmem = (size_t)kTmaBufs * 4 * kTmaStage * sizeof(double);
+
+__device__ __forceinline__ uint32_t de_smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void de_mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(de_smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void de_mbar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(de_smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void de_bulk(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            de_smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(de_smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void de_mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(de_smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// the row's operands in registers for the whole item (the global-load kernel
+// reads them from the shared TrialRow per batch)
+struct TmaRow {
+    const void *src[4];  // x_i, x_r1, x_r2, x_r3: f64 rows, or bit rows for +/-1 slots (bit k of bin)
+    uint32_t bin;
+    double *out;
+    uint32_t *bout, *dout, *prow;
+    uint64_t key;
+    uint32_t p_mask;
+    int jr;
+    double F;
+    uint32_t Hsl, H2;  // top-31-bit thresholds of the social draw and of the second draw
+    bool early;
+};
+
+// wolf code of one gene on the high-word fast path (wolf_code_z<K, false>
+// with the thresholds pre-shifted); K = 4 only (the pick is the top two bits)
+__device__ __forceinline__ uint32_t wolf_code_fast4(const RunConsts &c, const TmaRow &w, uint64_t zs, uint64_t gsoc,
+                                                    uint64_t gnon, bool &tie) {
+    const uint64_t x1 = mix_pre2z(zs, c);
+    const bool soc = lt_top(w.Hsl, mix_hi2(x1), tie);
+    const uint64_t x2 = mix_pre2z(zs + (soc ? gsoc : gnon), c);
+    const uint32_t h2 = mix_hi2(x2);
+    const bool f2 = lt_top(w.H2, h2, tie);
+    return soc ? 1u | ((h2 >> 30) << 1) : (f2 ? 2u : 0u);
+}
+
+// one warp's kTmaSteps x 64 genes of a landed stage: genes j64 + 512 s + lane
+// + 32 q (s < kTmaSteps, q < 2), the global-load kernel's layout
+// a lane's gene of a staged row: the f64 value at offset o, or +/-1 from bit
+// `lane` of the staged bit word wi (warp-uniform: one broadcast load per 32 genes)
+__device__ __forceinline__ double tma_gene(const double *srow, uint32_t binrow, int o, int wi, int lane) {
+    if (!binrow) return srow[o];
+    return pm1(reinterpret_cast<const uint32_t *>(srow)[wi] >> lane);
+}
+
+template <bool FULL, bool BIN, int K>
+__device__ __forceinline__ void de_tma_warp(const RunConsts &c, const TrialRow &r, const TmaRow &w, const double *sx,
+                                            int j64, uint64_t *full, uint32_t parity, uint64_t gD, uint64_t gnon,
+                                            uint32_t Hcr) {
+    const int lane = threadIdx.x & 31;
+    const int D = (int)c.D;
+    const uint64_t zb = w.key + (uint64_t)(w.p_mask + (uint32_t)(j64 + lane)) * kGold;
+    uint32_t mb = 0u;  // bit 2 s + q: take the mutant
+    bool tie = false;
+#pragma unroll
+    for (int st = 0; st < kTmaSteps; ++st)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int jj = j64 + 512 * st + lane + 32 * q;
+            bool ti = false;
+            const uint64_t x = mix_pre2z(zb + (uint64_t)(512 * st + 32 * q) * kGold, c);
+            const bool take = lt_top(Hcr, mix_hi2(x), ti) || jj == w.jr;
+            if (FULL || jj < D) {
+                mb |= take ? 1u << (2 * st + q) : 0u;
+                tie |= ti;
+            }
+        }
+    if (__any_sync(0xffffffffu, tie) && tie) {
+        mb = 0u;
+#pragma unroll
+        for (int st = 0; st < kTmaSteps; ++st)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int jj = j64 + 512 * st + lane + 32 * q;
+                const uint64_t x = mix_pre2(w.key, w.p_mask + (uint32_t)jj, c);
+                if ((FULL || jj < D) && (passes_hi(c.thr_cr, x, mix_hi2(x)) || jj == w.jr)) mb |= 1u << (2 * st + q);
+            }
+    }
+    if (K > 0) {  // wolf planes of the same genes: no data dependence, drawn while the stage lands
+        uint32_t code[kTmaSteps][2];
+        bool wtie = false;
+#pragma unroll
+        for (int st = 0; st < kTmaSteps; ++st)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int jj = j64 + 512 * st + lane + 32 * q;
+                const uint64_t zs = zb + (uint64_t)(512 * st + 32 * q) * kGold + gD;
+                bool ti = false;
+                if (K == 4)
+                    code[st][q] = wolf_code_fast4(c, w, zs, gD, gnon, ti);
+                else
+                    code[st][q] = wolf_code_z<K, false>(c, r.t, zs, gD, gnon, w.early, ti);
+                if (!FULL && jj >= D) code[st][q] = 0u, ti = false;
+                wtie |= ti;
+            }
+        if (__any_sync(0xffffffffu, wtie) && wtie) {
+#pragma unroll
+            for (int st = 0; st < kTmaSteps; ++st)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int jj = j64 + 512 * st + lane + 32 * q;
+                    bool ti = false;
+                    if (FULL || jj < D)
+                        code[st][q] = wolf_code_z<K, true>(c, r.t, zb + (uint64_t)(512 * st + 32 * q) * kGold + gD, gD,
+                                                           gnon, w.early, ti);
+                }
+        }
+#pragma unroll
+        for (int st = 0; st < kTmaSteps; ++st) {
+            if (!FULL && j64 + 512 * st >= (int)c.Dp) break;  // (a 64-gene span lies wholly inside or outside Dp)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                store_planes(w.prow + (((j64 + 512 * st) >> 5) + q) * kPlanes, code[st][q], lane, q);
+        }
+    }
+    de_mbar_wait(full, parity);
+    const double *s0 = sx + (j64 & 511) + lane;  // this lane's first gene in the stage
+#pragma unroll
+    for (int st = 0; st < kTmaSteps; ++st) {
+        if (!FULL && j64 + 512 * st >= (int)c.Dp) break;
+        bool neg[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int j = j64 + 512 * st + lane + 32 * q;
+            const int o = 512 * st + 32 * q;
+            const bool tk = (mb >> (2 * st + q)) & 1u;
+            double y, p2, p3;
+            if (!BIN) {
+                y = s0[(tk ? kTmaStage : 0) + o];  // x_r1 where the mask takes the mutant, else x_i
+                p2 = s0[2 * kTmaStage + o];
+                p3 = s0[3 * kTmaStage + o];
+            } else {  // some rows are +/-1 slots: each row from its staged f64 values or bits
+                const int og = (j64 & 511) + lane + o;       // gene offset in the stage
+                const int wi = ((j64 & 511) >> 5) + 16 * st + q;  // its bit word (lane = bit)
+                const double yi = tma_gene(sx, w.bin & 1u, og, wi, lane);
+                const double y1 = tma_gene(sx + kTmaStage, w.bin & 2u, og, wi, lane);
+                y = tk ? y1 : yi;
+                p2 = tma_gene(sx + 2 * kTmaStage, w.bin & 4u, og, wi, lane);
+                p3 = tma_gene(sx + 3 * kTmaStage, w.bin & 8u, og, wi, lane);
+            }
+            neg[q] = false;
+            if (FULL || j < D) {
+                const double v = tk ? y + w.F * (p2 - p3) : y;
+                st_stream(w.out + j, v);
+                neg[q] = !(v >= 0.0);
+            } else {
+                w.out[j] = 0.0;  // padding genes [D, Dp)
+            }
+        }
+        const uint32_t w0 = __ballot_sync(0xffffffffu, neg[0]);
+        const uint32_t w1 = __ballot_sync(0xffffffffu, neg[1]);
+        if (lane < 2) {
+            const int wi = ((j64 + 512 * st) >> 5) + lane;
+            w.bout[wi] = lane ? w1 : w0;
+            if (w.dout) w.dout[wi] = lane ? w1 : w0;
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(RunConsts c, TrialArgs a) {
+    QTRACE(0);
+    pdl_wait();
+    pdl_trigger<1>();
+    QTRACE_STARTED();
+    extern __shared__ __align__(128) double s_stage[];  // [kTmaBufs][4 rows][kTmaStage]
+    __shared__ __align__(8) uint64_t full[kTmaBufs];
+    __shared__ uint32_t done[kTmaBufs];
+    __shared__ TrialRow s_row;
+    const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
+    const int64_t i = a.row_lo + blockIdx.x / nchunk;
+    const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
+    if (threadIdx.x == 0) {
+        trial_row_setup(c, a, a.st->g, i, s_row);
+        for (int b = 0; b < kTmaBufs; ++b) {
+            de_mbar_init(&full[b], 1);
+            done[b] = 0u;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const TrialRow &r = s_row;
+    TmaRow w;
+    w.src[0] = r.xi.p;
+    w.src[1] = r.x1.p;
+    w.src[2] = r.x2.p;
+    w.src[3] = r.x3.p;
+    w.bin = r.xi.bin | r.x1.bin << 1 | r.x2.bin << 2 | r.x3.bin << 3;
+    w.out = r.out;
+    w.bout = r.bout;
+    w.dout = r.dout;
+    w.prow = r.prow;
+    w.key = r.key;
+    w.p_mask = r.p_mask;
+    w.jr = r.jr;
+    w.F = r.F;
+    w.early = r.t.early != 0;
+    w.Hsl = top_thr(r.t.sl);
+    w.H2 = top_thr(w.early ? r.t.dist : r.t.flip);
+    const int jend = min(jc + kDeChunk, (int)c.Dp);
+    const int nst = (jend - jc + kTmaStage - 1) / kTmaStage;
+    auto issue = [&](int st) {
+        const int b = st % kTmaBufs;
+        const int j = jc + st * kTmaStage;
+        const int n = min(kTmaStage, jend - j);  // a multiple of 128 genes
+        const uint32_t fb = (uint32_t)(n * (int)sizeof(double)), bb = (uint32_t)(n / 8);  // f64 / bit bytes
+        double *dst = s_stage + (size_t)b * 4 * kTmaStage;
+        const int nb = __popc(w.bin);
+        de_mbar_expect(&full[b], (uint32_t)(4 - nb) * fb + (uint32_t)nb * bb);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if ((w.bin >> k) & 1u)
+                de_bulk(dst + k * kTmaStage, static_cast<const uint32_t *>(w.src[k]) + (j >> 5), bb, &full[b]);
+            else
+                de_bulk(dst + k * kTmaStage, static_cast<const double *>(w.src[k]) + j, fb, &full[b]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int st = 0; st < min(nst, kTmaBufs); ++st) issue(st);
+    const uint64_t gD = (uint64_t)(uint32_t)c.Dg * kGold;
+    const uint64_t gnon = (uint64_t)(uint32_t)(w.early ? 2 * c.Dg : 5 * c.Dg) * kGold;
+    const uint32_t Hcr = top_thr(c.thr_cr);
+    const int warp = threadIdx.x >> 5;
+#pragma unroll 1
+    for (int st = 0; st < nst; ++st) {
+        const int b = st % kTmaBufs;
+        const uint32_t parity = (uint32_t)((st / kTmaBufs) & 1);
+        const int j64 = jc + st * kTmaStage + warp * 64;
+        const double *sx = s_stage + (size_t)b * 4 * kTmaStage;
+        const bool fullw = j64 + 512 * (kTmaSteps - 1) + 64 <= (int)c.D;
+        if (w.bin) {
+            if (fullw)
+                de_tma_warp<true, true, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+            else
+                de_tma_warp<false, true, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+        } else if (fullw) {
+            de_tma_warp<true, false, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+        } else {
+            de_tma_warp<false, false, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+        }
+        // the last warp done with the buffer refills it (its reads are in
+        // registers; the bulk copy is ordered after them by the shared atomic)
+        if (st + kTmaBufs < nst) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                __threadfence_block();
+                if (atomicAdd(&done[b], 1u) == kRowThreads / 32 - 1) {
+                    done[b] = 0u;
+                    issue(st + kTmaBufs);
+                }
+            }
+        }
+    }
+    if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
+}
+
 // Horizontal fusion (QPM_WOLF=mixed): even CTAs run the trial
 // of a (row, kDeChunk) item (HBM-bound), odd CTAs draw the same item's wolf
 // planes (integer-ALU-bound).  The block scheduler keeps both kinds resident
@@ -1813,6 +2116,7 @@ struct Engine {
     int32_t *topk_idx = nullptr;       // [kTopkMaxCtas][kTopSlots] per-CTA lists
     unsigned *topk_cnt = nullptr;      // arrival counter
     int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
+    bool de_tma = QPM_DE_TMA != 0;          // TMA-staged trial rows (QPM_DE_TMA=0: global loads)
     int de_item = 1024;                      // genes per warp item on longer rows (QPM_DE_ITEM, multiple of 128)
     int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
@@ -2214,7 +2518,12 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             const bool k0 = !hybrid || e->wolf_in_planner || wolf_side;
             QPM_CUDA_TRY(launch_k(pdl_trial, k0 ? k_de_trial_rows<0> : (c.k == 4 ? k_de_trial_rows<4> : k_de_trial_rows<3>),
                                   dim3(row_ctas), dim3(kRowThreads), 0, s, c, all, ch));
-        } else if (!hybrid || e->wolf_in_planner || wolf_side)
+        } else if (e->de_tma && (!hybrid || e->wolf_in_planner || wolf_side))
+            QPM_CUDA_TRY(launch_k(pdl_trial, k_de_trial_tma<0>, dim3(items), dim3(kRowThreads), kTmaSmem, s, c, all));
+        else if (e->de_tma && !e->wolf_mixed)
+            QPM_CUDA_TRY(launch_k(pdl_trial, c.k == 4 ? k_de_trial_tma<4> : k_de_trial_tma<3>, dim3(items),
+                                  dim3(kRowThreads), kTmaSmem, s, c, all));
+        else if (!hybrid || e->wolf_in_planner || wolf_side)
             QPM_CUDA_TRY(launch_k(pdl_trial, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, all));
         else if (e->wolf_mixed)
             QPM_CUDA_TRY(launch_k(pdl_trial, c.k == 4 ? k_de_trial_mixed<4> : k_de_trial_mixed<3>, dim3(2 * items),
@@ -2527,6 +2836,7 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         if (const char *v = knob("QPM_PDL")) e->pdl = atoi(v) != 0;
         if (const char *v = knob("QPM_GRAPH_GENS")) e->graph_gens = std::min(64, std::max(1, atoi(v)));
         if (const char *v = knob("QPM_DE_ROWS")) e->de_rows_max_dp = atoll(v);
+        if (const char *v = knob("QPM_DE_TMA")) e->de_tma = atoi(v) != 0;
         e->topk_ctas = (int)std::min<int64_t>(kTopkMaxCtas, std::max<int64_t>(1, c.NP / 2048));
         if (const char *v = knob("QPM_TOPK_CTAS")) e->topk_ctas = std::min(kTopkMaxCtas, std::max(1, atoi(v)));
         // fused finish + selection: its last CTA runs the whole-population part
@@ -2560,6 +2870,21 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
             engine_free(e);
             return QPM_ERR_CUDA;
         }
+        // the TMA-staged trial's stage ring (static shared memory on top)
+        static std::once_flag tma_once;
+        static cudaError_t tma_err = cudaSuccess;
+        std::call_once(tma_once, [] {
+            const void *ks[3] = {(const void *)k_de_trial_tma<0>, (const void *)k_de_trial_tma<3>,
+                                 (const void *)k_de_trial_tma<4>};
+            for (const void *k : ks) {
+                cudaFuncAttributes ka{};
+                cudaError_t err = cudaFuncGetAttributes(&ka, k);
+                if (err == cudaSuccess)
+                    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+                if (err != cudaSuccess) tma_err = err;
+            }
+        });
+        if (tma_err != cudaSuccess) e->de_tma = false;  // (the global-load trial then runs)
         cudaFuncAttributes fb{};
         cudaFuncGetAttributes(&fb, k_finish_select<1>);
         if ((size_t)max_optin < stats_smem_bytes(c) + fb.sharedSizeBytes ||
