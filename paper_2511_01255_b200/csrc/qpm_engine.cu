@@ -1104,6 +1104,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
     pdl_wait();
     pdl_trigger<1>();
     QTRACE_STARTED();
+    QSTAMP(0);
     extern __shared__ __align__(128) double s_stage[];  // [kTmaBufs][4 rows][kTmaStage]
     __shared__ __align__(8) uint64_t full[kTmaBufs];
     __shared__ uint32_t done[kTmaBufs];
@@ -1120,6 +1121,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    QSTAMP(1);  // setup done (CTA 0)
     const TrialRow &r = s_row;
     TmaRow w;
     w.src[0] = r.xi.p;
@@ -1192,6 +1194,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
             }
         }
     }
+    QSTAMP(2);  // CTA 0 thread 0 done
     if (jc == 0 && threadIdx.x == 0) a.slot_bin[r.out_slot] = 0;
 }
 
@@ -1485,7 +1488,22 @@ __device__ void block_topk_k(const double *vals, int64_t n, int k, int32_t *out)
     Cand L[kTopSlots];
 #pragma unroll
     for (int t = 0; t < kTopSlots; ++t) L[t] = {0.0, -1};
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) topk_insert(L, Cand{__ldcg(vals + i), (int32_t)i});
+    // the loads of kBatch strides first, then the inserts: one L2 round trip
+    // per batch instead of one per element (C2: 4 elements per thread)
+    constexpr int kBatch = 4;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)kBatch * blockDim.x) {
+        double v[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            v[u] = i < n ? __ldcg(vals + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            if (i < n) topk_insert(L, Cand{v[u], (int32_t)i});
+        }
+    }
     block_topk_lists(L, k, out);
 }
 
@@ -1686,29 +1704,41 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
     // selection; every thread keeps its elements' final values for the max/min
     double mx = -INFINITY, mn = INFINITY;
     int64_t amx = n;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        double v = __ldcg(fit + i);  // (coherent: a fused caller's other CTAs wrote it)
-        if (mode != 3) {
-            bool is_leader = false;
+    constexpr int kBatch = 4;  // loads of kBatch strides issued together (one L2 round trip per batch)
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)kBatch * blockDim.x) {
+        double vb[kBatch];
 #pragma unroll
-            for (int t = 0; t < kMaxLeaders; ++t) is_leader |= lead[t] == i;
-            const double f = cand[i];
-            const int32_t a = slot_of[i], b = spare_of[i];  // with the values: one L2 round trip
-            if (!is_leader && (mode == 2 || f > v)) {
-                slot_of[i] = b;
-                spare_of[i] = a;
-                fit[i] = f;
-                if (mode == 1) slot_bin[b] = 1;
-                if (slot_tag) slot_tag[i] = (uint32_t)b | (mode == 1 ? kBinTag : 0u);
-                v = f;
+        for (int u = 0; u < kBatch; ++u) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            vb[u] = i < n ? __ldcg(fit + i) : 0.0;  // (coherent: a fused caller's other CTAs wrote it)
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x;
+            if (i >= n) break;
+            double v = vb[u];
+            if (mode != 3) {
+                bool is_leader = false;
+#pragma unroll
+                for (int t = 0; t < kMaxLeaders; ++t) is_leader |= lead[t] == i;
+                const double f = cand[i];
+                const int32_t a = slot_of[i], b = spare_of[i];
+                if (!is_leader && (mode == 2 || f > v)) {
+                    slot_of[i] = b;
+                    spare_of[i] = a;
+                    fit[i] = f;
+                    if (mode == 1) slot_bin[b] = 1;
+                    if (slot_tag) slot_tag[i] = (uint32_t)b | (mode == 1 ? kBinTag : 0u);
+                    v = f;
+                }
             }
+            if (on_chip) fv[i] = v;
+            if (v > mx || (v == mx && i < amx)) {  // max, lowest index on ties
+                mx = v;
+                amx = i;
+            }
+            mn = v < mn ? v : mn;
         }
-        if (on_chip) fv[i] = v;
-        if (v > mx || (v == mx && i < amx)) {  // max, lowest index on ties
-            mx = v;
-            amx = i;
-        }
-        mn = v < mn ? v : mn;
     }
     for (int off = 16; off > 0; off >>= 1) {
         const double omx = __shfl_down_sync(0xffffffffu, mx, off);
@@ -1862,6 +1892,7 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
     pdl_wait();
     pdl_trigger<4>();
     QTRACE_STARTED();
+    QSTAMP(0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t r = (int64_t)blockIdx.x * (fs_threads<MODE>() / 32) + warp;
     if (r < c.NP) {  // warp-uniform
@@ -1886,15 +1917,18 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
     __shared__ unsigned s_last;
     __threadfence();  // this CTA's selections, before its arrival
     __syncthreads();
+    QSTAMP(1);
     if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1u) + 1u == gridDim.x;
     __syncthreads();
     if (!s_last) return;
+    if (threadIdx.x == 0) QSTAMP_ANY(2);
     __threadfence();
     if (MODE == 0)
         block_topk_k(fit, c.NP, c.k, st->leaders);
     else
         select_stats_body(c, 3, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, false,
                           nullptr);
+    if (threadIdx.x == 0) QSTAMP_ANY(3);
     if (threadIdx.x == 0) *cnt = 0u;  // ready for the next launch (stream-ordered)
 }
 

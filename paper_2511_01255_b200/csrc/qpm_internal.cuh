@@ -207,6 +207,12 @@ static __device__ unsigned long long g_stamp[kTraceIds][64][8];
             ::qpm::g_stamp[qtrace_scope_.id][::qpm::g_tacc[qtrace_scope_.id].launch % 64][slot] =      \
                 ::qpm::gtimer();                                                                       \
     } while (0)
+// the same from a single calling thread of any CTA (e.g. a last-CTA tail)
+#define QSTAMP_ANY(slot)                                                                               \
+    do {                                                                                               \
+        ::qpm::g_stamp[qtrace_scope_.id][::qpm::g_tacc[qtrace_scope_.id].launch % 64][slot] =          \
+            ::qpm::gtimer();                                                                           \
+    } while (0)
 // host: reset the accumulators / copy the log of this translation unit
 static inline int trace_reset_tu() {
     std::vector<TraceAcc> init(kTraceIds, TraceAcc{~0ULL, ~0ULL, 0ULL, 0u, 0u});
@@ -225,6 +231,7 @@ static inline int trace_stamps_tu(unsigned long long *out) {
 #define QTRACE(id)
 #define QTRACE_STARTED()
 #define QSTAMP(slot)
+#define QSTAMP_ANY(slot)
 #endif
 
 template <typename... KArgs, typename... Args>

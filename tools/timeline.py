@@ -90,6 +90,11 @@ def main():
               f"{(rel[:, 2] - rel[:, 1]).mean():8.2f}")
     print("fit_fast CTA 0 stamps (us from start): bits, first table, loop end, stored =",
           [round(float(x), 2) for x in stamps(L)[1:5]])
+    print("de_trial CTA 0 stamps (us from start): setup done, thread 0 done =",
+          [round(float(x), 2) for x in stamps(L, "qpm_dev_trace_engine", 0)[1:3]])
+    for kid in (3, 5):
+        print(f"{NAMES[kid]} stamps (us from CTA 0 start): CTA 0 rows done, last CTA detected, last CTA done =",
+              [round(float(x), 2) for x in stamps(L, "qpm_dev_trace_engine", kid)[1:4]])
 
 
 
