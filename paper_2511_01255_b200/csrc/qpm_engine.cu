@@ -984,10 +984,11 @@ __device__ __forceinline__ double tma_gene(const double *srow, uint32_t binrow, 
     return pm1(reinterpret_cast<const uint32_t *>(srow)[wi] >> lane);
 }
 
-template <bool FULL, bool BIN, int K>
-__device__ __forceinline__ void de_tma_warp(const RunConsts &c, const TrialRow &r, const TmaRow &w, const double *sx,
-                                            int j64, uint64_t *full, uint32_t parity, uint64_t gD, uint64_t gnon,
-                                            uint32_t Hcr) {
+// the draws of one warp's kTmaSteps x 64 genes (mask bits returned, wolf
+// planes stored): no data dependence, so they run while the stage lands
+template <bool FULL, int K>
+__device__ __forceinline__ uint32_t de_tma_draws(const RunConsts &c, const TrialRow &r, const TmaRow &w, int j64,
+                                                 uint64_t gD, uint64_t gnon, uint32_t Hcr) {
     const int lane = threadIdx.x & 31;
     const int D = (int)c.D;
     const uint64_t zb = w.key + (uint64_t)(w.p_mask + (uint32_t)(j64 + lane)) * kGold;
@@ -1054,7 +1055,15 @@ __device__ __forceinline__ void de_tma_warp(const RunConsts &c, const TrialRow &
                 store_planes(w.prow + (((j64 + 512 * st) >> 5) + q) * kPlanes, code[st][q], lane, q);
         }
     }
-    de_mbar_wait(full, parity);
+    return mb;
+}
+
+// the trial values of the same genes from the landed stage sx
+template <bool FULL, bool BIN>
+__device__ __forceinline__ void de_tma_data(const RunConsts &c, const TmaRow &w, const double *sx, int j64,
+                                            uint32_t mb) {
+    const int lane = threadIdx.x & 31;
+    const int D = (int)c.D;
     const double *s0 = sx + (j64 & 511) + lane;  // this lane's first gene in the stage
 #pragma unroll
     for (int st = 0; st < kTmaSteps; ++st) {
@@ -1112,23 +1121,54 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
     const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
     const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
+    // Two-phase setup by thread 0.  Phase A (st->g -> keys / picks / thresholds)
+    // is all the draws need: the warps start drawing after it.  Phase B (the
+    // picked rows' slot tags, one dependent load later) gives the source rows;
+    // thread 0 then issues the first stages.  The other warps read the row
+    // pointers only after waiting on a stage's barrier, which orders thread 0's
+    // shared-memory writes (mbarrier arrive: release; wait: acquire).
+    int4 pk = make_int4(0, 0, 0, 0);
+    uint32_t tag_i = 0u;
     if (threadIdx.x == 0) {
-        trial_row_setup(c, a, a.st->g, i, s_row);
         for (int b = 0; b < kTmaBufs; ++b) {
             de_mbar_init(&full[b], 1);
             done[b] = 0u;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int64_t g = a.st->g;
+        const int64_t b = g & 1;
+        pk = a.picks[b * c.NP + i];
+        TrialRow &r = s_row;
+        r.key = a.keys[b * c.NP + i];
+        r.jr = a.jrand[b * c.NP + i] - (int)c.g0;  // j_rand relative to the shard (never matches outside it)
+        tag_i = a.slot_tag ? a.slot_tag[i] : 0u;
+        r.out_slot = a.spare_of[i];
+        r.out = a.genome + r.out_slot * c.Dp;
+        r.bout = a.bits + r.out_slot * c.W;
+        r.dout = a.cbits ? a.cbits + i * c.W : nullptr;
+        r.prow = a.planes + (b * c.NP + i) * c.W * kPlanes;
+        r.p_mask = (uint32_t)(pk.w + 2 + c.g0);  // m + 1 + (g0 + j), plus one: j counts this shard's genes
+        r.F = a.st->F;
+        r.t = a.gthr[g];
     }
     __syncthreads();
-    QSTAMP(1);  // setup done (CTA 0)
+    if (threadIdx.x == 0) {  // phase B
+        TrialRow &r = s_row;
+        if (a.slot_tag) {
+            r.xi = row_ref_tag(c, tag_i, a.genome, a.bits);
+            r.x1 = row_ref_tag(c, a.slot_tag[pk.x], a.genome, a.bits);
+            r.x2 = row_ref_tag(c, a.slot_tag[pk.y], a.genome, a.bits);
+            r.x3 = row_ref_tag(c, a.slot_tag[pk.z], a.genome, a.bits);
+        } else {
+            r.xi = row_ref(c, a.slot_of[i], a.slot_bin, a.genome, a.bits);
+            r.x1 = row_ref(c, a.slot_of[pk.x], a.slot_bin, a.genome, a.bits);
+            r.x2 = row_ref(c, a.slot_of[pk.y], a.slot_bin, a.genome, a.bits);
+            r.x3 = row_ref(c, a.slot_of[pk.z], a.slot_bin, a.genome, a.bits);
+        }
+    }
+    QSTAMP(1);  // setup phase A done (CTA 0)
     const TrialRow &r = s_row;
     TmaRow w;
-    w.src[0] = r.xi.p;
-    w.src[1] = r.x1.p;
-    w.src[2] = r.x2.p;
-    w.src[3] = r.x3.p;
-    w.bin = r.xi.bin | r.x1.bin << 1 | r.x2.bin << 2 | r.x3.bin << 3;
     w.out = r.out;
     w.bout = r.bout;
     w.dout = r.dout;
@@ -1142,6 +1182,14 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
     w.H2 = top_thr(w.early ? r.t.dist : r.t.flip);
     const int jend = min(jc + kDeChunk, (int)c.Dp);
     const int nst = (jend - jc + kTmaStage - 1) / kTmaStage;
+    // the source rows (valid in thread 0 after phase B, elsewhere after a stage wait)
+    auto load_src = [&]() {
+        w.src[0] = r.xi.p;
+        w.src[1] = r.x1.p;
+        w.src[2] = r.x2.p;
+        w.src[3] = r.x3.p;
+        w.bin = r.xi.bin | r.x1.bin << 1 | r.x2.bin << 2 | r.x3.bin << 3;
+    };
     auto issue = [&](int st) {
         const int b = st % kTmaBufs;
         const int j = jc + st * kTmaStage;
@@ -1158,8 +1206,10 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
                 de_bulk(dst + k * kTmaStage, static_cast<const double *>(w.src[k]) + j, fb, &full[b]);
         }
     };
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+        load_src();
         for (int st = 0; st < min(nst, kTmaBufs); ++st) issue(st);
+    }
     const uint64_t gD = (uint64_t)(uint32_t)c.Dg * kGold;
     const uint64_t gnon = (uint64_t)(uint32_t)(w.early ? 2 * c.Dg : 5 * c.Dg) * kGold;
     const uint32_t Hcr = top_thr(c.thr_cr);
@@ -1171,15 +1221,19 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
         const int j64 = jc + st * kTmaStage + warp * 64;
         const double *sx = s_stage + (size_t)b * 4 * kTmaStage;
         const bool fullw = j64 + 512 * (kTmaSteps - 1) + 64 <= (int)c.D;
+        const uint32_t mb = fullw ? de_tma_draws<true, K>(c, r, w, j64, gD, gnon, Hcr)
+                                  : de_tma_draws<false, K>(c, r, w, j64, gD, gnon, Hcr);
+        de_mbar_wait(&full[b], parity);
+        if (st == 0) load_src();
         if (w.bin) {
             if (fullw)
-                de_tma_warp<true, true, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+                de_tma_data<true, true>(c, w, sx, j64, mb);
             else
-                de_tma_warp<false, true, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+                de_tma_data<false, true>(c, w, sx, j64, mb);
         } else if (fullw) {
-            de_tma_warp<true, false, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+            de_tma_data<true, false>(c, w, sx, j64, mb);
         } else {
-            de_tma_warp<false, false, K>(c, r, w, sx, j64, &full[b], parity, gD, gnon, Hcr);
+            de_tma_data<false, false>(c, w, sx, j64, mb);
         }
         // the last warp done with the buffer refills it (its reads are in
         // registers; the bulk copy is ordered after them by the shared atomic)
@@ -1692,12 +1746,13 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
         for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
     }
     if (wait) pdl_wait();
+    // the state is copied to shared memory for the serial tail: its words are
+    // loaded here and stored after the fitness loads below are in flight
     __shared__ EngineState s_state;
-    {
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(st);
-        uint32_t *dst = reinterpret_cast<uint32_t *>(&s_state);
-        for (int t = threadIdx.x; t < (int)(sizeof(EngineState) / 4); t += blockDim.x) dst[t] = src[t];
-    }
+    constexpr int kStateWords = (int)(sizeof(EngineState) / 4);
+    const uint32_t *st_src = reinterpret_cast<const uint32_t *>(st);
+    uint32_t st_w0 = (int)threadIdx.x < kStateWords ? st_src[threadIdx.x] : 0u;
+    if (mode == 3 && threadIdx.x == 0) QSTAMP_ID(5, 4);
     int32_t lead[kMaxLeaders];
 #pragma unroll
     for (int t = 0; t < kMaxLeaders; ++t) lead[t] = (mode == 1 || mode == 2) && t < c.k ? st->leaders[t] : -1;
@@ -1711,6 +1766,11 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
         for (int u = 0; u < kBatch; ++u) {
             const int64_t i = i0 + (int64_t)u * blockDim.x;
             vb[u] = i < n ? __ldcg(fit + i) : 0.0;  // (coherent: a fused caller's other CTAs wrote it)
+        }
+        if (i0 == (int64_t)threadIdx.x) {  // first batch: the state words, now that the loads are issued
+            uint32_t *dst = reinterpret_cast<uint32_t *>(&s_state);
+            if ((int)threadIdx.x < kStateWords) dst[threadIdx.x] = st_w0;
+            for (int t = (int)threadIdx.x + (int)blockDim.x; t < kStateWords; t += blockDim.x) dst[t] = st_src[t];
         }
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
@@ -1739,6 +1799,11 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
             }
             mn = v < mn ? v : mn;
         }
+    }
+    if ((int64_t)threadIdx.x >= n) {  // (no batch ran in this thread)
+        uint32_t *dst = reinterpret_cast<uint32_t *>(&s_state);
+        if ((int)threadIdx.x < kStateWords) dst[threadIdx.x] = st_w0;
+        for (int t = (int)threadIdx.x + (int)blockDim.x; t < kStateWords; t += blockDim.x) dst[t] = st_src[t];
     }
     for (int off = 16; off > 0; off >>= 1) {
         const double omx = __shfl_down_sync(0xffffffffu, mx, off);
@@ -1775,14 +1840,23 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
     mx = __shfl_sync(0xffffffffu, mx, 0);
     mn = __shfl_sync(0xffffffffu, mn, 0);
     amx = __shfl_sync(0xffffffffu, amx, 0);
-    const double mean = block_pairwise(fv, c, ts) / (double)n;
+    if (mode == 3 && threadIdx.x == 0) QSTAMP_ID(5, 5);
+    // x / n: by an exact reciprocal multiply when n is a power of two (the
+    // same correctly rounded value, without the division sequence)
+    const bool n_pow2 = (n & (n - 1)) == 0;
+    const double inv_n = 1.0 / (double)n;
+    const double sum = block_pairwise(fv, c, ts);
+    const double mean = n_pow2 ? sum * inv_n : sum / (double)n;
+    if (mode == 3 && threadIdx.x == 0) QSTAMP_ID(5, 6);
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = fv[i] - mean;
         sq[i] = d * d;
     }
     __syncthreads();
-    const double var = block_pairwise(sq, c, ts) / (double)n;
+    const double ssq = block_pairwise(sq, c, ts);
+    const double var = n_pow2 ? ssq * inv_n : ssq / (double)n;
     if (threadIdx.x != 0) return;
+    if (mode == 3) QSTAMP_ID(5, 7);
     // serial tail on the shared-memory copy of the state (fetched at entry);
     // only the fields this kernel owns are written back (g_plan belongs to
     // the planner stream)

@@ -213,6 +213,11 @@ static __device__ unsigned long long g_stamp[kTraceIds][64][8];
         ::qpm::g_stamp[qtrace_scope_.id][::qpm::g_tacc[qtrace_scope_.id].launch % 64][slot] =          \
             ::qpm::gtimer();                                                                           \
     } while (0)
+// the same for an explicit kernel id, outside the kernel's own scope
+#define QSTAMP_ID(kid, slot)                                                                           \
+    do {                                                                                               \
+        ::qpm::g_stamp[kid][::qpm::g_tacc[kid].launch % 64][slot] = ::qpm::gtimer();                   \
+    } while (0)
 // host: reset the accumulators / copy the log of this translation unit
 static inline int trace_reset_tu() {
     std::vector<TraceAcc> init(kTraceIds, TraceAcc{~0ULL, ~0ULL, 0ULL, 0u, 0u});
@@ -232,6 +237,7 @@ static inline int trace_stamps_tu(unsigned long long *out) {
 #define QTRACE_STARTED()
 #define QSTAMP(slot)
 #define QSTAMP_ANY(slot)
+#define QSTAMP_ID(kid, slot)
 #endif
 
 template <typename... KArgs, typename... Args>

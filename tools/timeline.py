@@ -95,6 +95,8 @@ def main():
     for kid in (3, 5):
         print(f"{NAMES[kid]} stamps (us from CTA 0 start): CTA 0 rows done, last CTA detected, last CTA done =",
               [round(float(x), 2) for x in stamps(L, "qpm_dev_trace_engine", kid)[1:4]])
+    print("stats|fs<1> last-CTA stamps: state staged, selection + max done, mean done, var done =",
+          [round(float(x), 2) for x in stamps(L, "qpm_dev_trace_engine", 5)[4:8]])
 
 
 
