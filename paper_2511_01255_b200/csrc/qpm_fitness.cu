@@ -685,7 +685,22 @@ int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_word
     const int thg = p->process == QPM_PROCESS_THG;
     // rows per CTA: 256 for one wavelength (C2 109.8 -> 109.1 us/gen), 128
     // with many (C5 launch 2029 vs 2084 us with 256) -- alternating A/B
-    const int bt = p->n_wl == 1 ? kFitThreadsMax : kFitThreads;
+    int bt = p->n_wl == 1 ? kFitThreadsMax : kFitThreads;
+    // a launch that fits in one wave at one CTA per SM (C2: 27 segments x 4
+    // row blocks = 108 CTAs on 148 SMs) spreads its rows over as many row
+    // blocks as the idle SMs allow (C2: 5 blocks of 224 rows, 135 CTAs): the
+    // scan is latency-bound there, so fewer rows per SM end it sooner.  Rows
+    // are independent: the results do not depend on the CTA shape.
+    static const int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
+    const int64_t blocks = (rows + bt - 1) / bt;
+    const int64_t per_wave = sms / ((int64_t)p->S * p->n_wl);  // row blocks one wave holds
+    if (p->n_wl == 1 && blocks * p->S <= sms && per_wave > blocks)
+        bt = (int)std::max<int64_t>(64, ((rows + per_wave - 1) / per_wave + 31) / 32 * 32);
     const dim3 grid((unsigned)p->S, (unsigned)((rows + bt - 1) / bt), (unsigned)p->n_wl);
     QPM_CUDA_TRY(launch_k(pdl, thg ? k_fit_fast<true> : k_fit_fast<false>, grid, dim3(bt), kFitSmem, stream,
                           (const double2 *)p->qt, p->nquads, p->nchunks, p->seg_chunks, S_stride, bits, p->W, row_index,
