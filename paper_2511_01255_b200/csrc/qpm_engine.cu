@@ -2807,9 +2807,29 @@ extern "C" {
 // A per-thread pinned host buffer of at least `bytes` (nullptr when pinned
 // memory is unavailable: callers then copy through pageable memory).  Used
 // between an enqueue and the stream synchronisation that ends its use.
+// Copies out of the buffer may still be in flight from the previous user
+// (engine creation does not wait for its uploads): pinned_staging_busy(s)
+// records that, and the next pinned_staging call waits for it first.
+static thread_local cudaEvent_t t_staging_ev = nullptr;
+static thread_local bool t_staging_pending = false;
+static void pinned_staging_busy(cudaStream_t s) {
+    if (!t_staging_ev && cudaEventCreateWithFlags(&t_staging_ev, cudaEventDisableTiming) != cudaSuccess) {
+        t_staging_ev = nullptr;
+        cudaStreamSynchronize(s);  // (no event: wait here instead)
+        return;
+    }
+    if (cudaEventRecord(t_staging_ev, s) == cudaSuccess)
+        t_staging_pending = true;
+    else
+        cudaStreamSynchronize(s);
+}
 static char *pinned_staging(size_t bytes) {
     static thread_local char *pinned = nullptr;
     static thread_local size_t pinned_bytes = 0;
+    if (t_staging_pending) {
+        cudaEventSynchronize(t_staging_ev);
+        t_staging_pending = false;
+    }
     if (pinned_bytes < bytes) {
         if (pinned) cudaFreeHost(pinned);
         pinned = nullptr;
@@ -3134,12 +3154,15 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     if (err == cudaSuccess && e->check_err)
         err = cudaFuncSetAttribute(k_check_state, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(((2 * NP + 31) / 32) * sizeof(uint32_t)));
-    if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
     if (err != cudaSuccess) {
         set_error("engine upload: %s", cudaGetErrorString(err));
+        cudaStreamSynchronize(e->stream);
         engine_free(e);
         return QPM_ERR_CUDA;
     }
+    // no synchronisation: the uploads are stream-ordered before the engine's
+    // work; the staging buffer's next user waits for them (pinned_staging)
+    if (pinned) pinned_staging_busy(e->stream);
     auto *h = new qpm_engine();
     h->e = e;
     *out = h;

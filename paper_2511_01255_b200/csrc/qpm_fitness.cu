@@ -381,7 +381,7 @@ constexpr int kFitBufs = QPM_FIT_BUFS;  // table chunks in flight (a whole C2 se
 constexpr int kFitSmem = kFitBufs * kChunkBytes;  // dynamic shared memory (48 KB)
 
 #ifndef QPM_FIT_MINB
-#define QPM_FIT_MINB 1  // (3: <= 85 registers; measured at the C5 shape)
+#define QPM_FIT_MINB 2  // two 256-row CTAs per SM (<= 128 registers); 3 (<= 85) measured slower at C5, DESIGN.md §3
 #endif
 template <bool THG>
 __global__ void __launch_bounds__(kFitThreadsMax, QPM_FIT_MINB) k_fit_fast(const double2 *__restrict__ qt, int64_t nquads,

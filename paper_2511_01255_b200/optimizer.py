@@ -18,7 +18,7 @@ fitness rounding (~1e-14 relative).
 
 import ctypes
 import math
-from dataclasses import dataclass, replace
+from dataclasses import astuple, dataclass, replace
 
 import numpy as np
 
@@ -190,6 +190,23 @@ def adaptive_f_update(state: AdaptiveState, params: DEParams, schedules: Schedul
 # schedule table
 # ---------------------------------------------------------------------------
 
+_SCHED_CACHE: dict = {}
+
+
+def _schedule_cached(generations: int, de: DEParams, gwo: GWOParams, sch: Schedules) -> np.ndarray:
+    """schedule_table, memoised on the parameter values (read-only array): batched
+    trials and repeated runs of one configuration build it once."""
+    key = (int(generations), astuple(de), astuple(gwo), astuple(sch))
+    tab = _SCHED_CACHE.get(key)
+    if tab is None:
+        if len(_SCHED_CACHE) >= 64:
+            _SCHED_CACHE.clear()
+        tab = np.ascontiguousarray(schedule_table(generations, de, gwo, sch))
+        tab.flags.writeable = False
+        _SCHED_CACHE[key] = tab
+    return tab
+
+
 def schedule_table(generations: int, de: DEParams, gwo: GWOParams, sch: Schedules) -> np.ndarray:
     """[G+1, 8] per-generation scalars with the reference's float arithmetic.
 
@@ -291,7 +308,7 @@ class Engine:
         p.gwo_lo, p.gwo_hi, p.gwo_a0 = float(bounds[0]), float(bounds[1]), gwo.a
         p.shard_rank, p.shard_world = int(shard[0]), int(shard[1])
         self.params = p
-        self.sched = np.ascontiguousarray(schedule_table(self.G, de, gwo, sch))
+        self.sched = _schedule_cached(self.G, de, gwo, sch)
         h = ctypes.c_void_p()
         _native.check(_native.lib().qpm_engine_create(ctypes.byref(h), objective.handle, ctypes.byref(p),
                                                       self.sched.ctypes.data, self.stream.cuda_stream),

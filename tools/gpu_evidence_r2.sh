@@ -3,7 +3,7 @@
 # driver's settings and a long run, reference arm, BASELINE configs, e2e probe, launch list of
 # the bench command, ncu --set full of a late C2 generation, a C3 generation, C4 run_gwo,
 # C5 fitness, and the multi-GPU shard probe (emulated ranks + NCCL-rate exchange model).
-E=gpurun_out/ev2
+E=gpurun_out/${EV:-ev3}
 mkdir -p $E
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $E/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q --durations=15 > $E/pytest_gpu.log 2>&1; echo RC=$? >> $E/pytest_gpu.log
