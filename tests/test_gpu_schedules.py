@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 KNOBS = ("QPM_WOLF", "QPM_PLAN_FORK", "QPM_PLAN_CTAS", "QPM_PDL", "QPM_TOPK_THREADS", "QPM_STATS_THREADS",
          "QPM_TOPK_CTAS", "QPM_DE_ROWS", "QPM_DE_ITEM", "QPM_GRAPH_GENS",
-         "QPM_FUSED_SELECT")
+         "QPM_FUSED_SELECT", "QPM_DE_TMA")
 
 
 @pytest.fixture(scope="module")
@@ -59,6 +59,9 @@ VARIANTS = [
     {"QPM_WOLF": "planner", "QPM_PLAN_FORK": "trial"},
     {"QPM_WOLF": "planner", "QPM_PLAN_CTAS": "7"},
     {"QPM_WOLF": "planner", "QPM_PLAN_CTAS": "1000", "QPM_PLAN_FORK": "trial"},
+    {"QPM_DE_ROWS": "0"},                       # the TMA-staged trial at this row length
+    {"QPM_DE_ROWS": "0", "QPM_DE_TMA": "0"},    # the global-load trial
+    {"QPM_DE_ROWS": "0", "QPM_WOLF": "side"},   # the TMA-staged trial without wolf draws
 ]
 
 
@@ -107,7 +110,8 @@ def test_repeated_runs_are_identical(q, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{}, {"QPM_WOLF": "planner"}, {"QPM_WOLF": "planner", "QPM_PDL": "0"},
-                                 {"QPM_WOLF": "mixed"}, {"QPM_WOLF": "side"}, {"QPM_FUSED_SELECT": "0"}],
+                                 {"QPM_WOLF": "mixed"}, {"QPM_WOLF": "side"}, {"QPM_FUSED_SELECT": "0"},
+                                 {"QPM_DE_TMA": "0"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_c2_shape_runs_match_default(q, monkeypatch, env):
     """The C2 shape (NP 1024, D 10^4) for 600 generations, twice per schedule:
@@ -128,3 +132,15 @@ def test_large_population_multi_cta_selection(q, monkeypatch):
     assert np.array_equal(got, want)
     fused = _trace(q, monkeypatch, {"QPM_FUSED_SELECT": "1"}, D=1300, NP=8192, G=6)[0]  # 8 stats elements per thread
     assert np.array_equal(fused, want)
+
+
+@pytest.mark.parametrize("algorithm", ["hybrid", "de"])
+def test_tma_trial_equals_global_load_trial(q, monkeypatch, algorithm):
+    """The TMA-staged DE trial (k_de_trial_tma) and the global-load kernel
+    (k_de_trial) write the same trial rows, bits and wolf planes: whole runs,
+    population included, are bit-identical (a row length with a partial last
+    chunk and stage: D = 9,000, 2 chunks of 4,096 + 896 genes)."""
+    t_tma, g_tma = _trace(q, monkeypatch, {}, algorithm=algorithm, D=9000, NP=128, G=60)
+    t_glb, g_glb = _trace(q, monkeypatch, {"QPM_DE_TMA": "0"}, algorithm=algorithm, D=9000, NP=128, G=60)
+    assert np.array_equal(t_tma, t_glb)
+    assert np.array_equal(g_tma, g_glb)
