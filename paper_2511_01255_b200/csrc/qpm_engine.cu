@@ -1709,26 +1709,20 @@ __global__ void __launch_bounds__(kCtaThreads) k_topk_leaders(RunConsts c, Engin
 // np.mean / np.std, the convergence window and adaptive_f_update
 // (optimizer.py:277-299, 469-485), or run_gwo's a-row and best-ever tracking
 // (optimizer.py:586-589), and the trace row.  One CTA.
-__device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, EngineState *__restrict__ st,
-                                                  const double *__restrict__ sched, const double *cand,
-                                                  double *__restrict__ fit, int32_t *__restrict__ slot_of,
-                                                  int32_t *__restrict__ spare_of, uint8_t *__restrict__ slot_bin,
-                                                  double *__restrict__ scratch, const SumTree &tr,
-                                                  double *__restrict__ trace, const SumTreeInline &tri, bool wait,
-                                                  uint32_t *__restrict__ slot_tag) {
-    const int64_t n = c.NP;
-    // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
-    // then the pairwise-sum tree (values, leaf offsets, children, levels)
-    extern __shared__ double s_dyn[];
-    const bool on_chip = n <= kStatsSmemMaxNP;
-    double *fv = on_chip ? s_dyn : fit;
-    double *sq = on_chip ? s_dyn + n : scratch;
+// the statistics' dynamic shared memory: [fit (n), squared deviations (n)]
+// when n fits, then the pairwise-sum tree (values, leaf offsets, children, levels)
+__device__ __forceinline__ TreeSmem stats_tree_smem(const RunConsts &c, double *s_dyn) {
+    const bool on_chip = c.NP <= kStatsSmemMaxNP;
     TreeSmem ts;
-    ts.val = s_dyn + (on_chip ? 2 * n : 0);
+    ts.val = s_dyn + (on_chip ? 2 * c.NP : 0);
     ts.leaf_off = reinterpret_cast<int32_t *>(ts.val + 2 * c.n_leaf);
     ts.kid = ts.leaf_off + c.n_leaf + 1;
     ts.lvl = ts.kid + 2 * c.n_leaf;
-    // the tree is the engine's constant: staged before waiting on the predecessor
+    return ts;
+}
+// the tree is the engine's constant: staged before waiting on the predecessor
+__device__ __forceinline__ void stats_tree_stage(const RunConsts &c, const SumTree &tr, const SumTreeInline &tri,
+                                                 const TreeSmem &ts) {
     if (tri.n) {
         const int nl = c.n_leaf + 1, nk = 2 * (c.n_leaf - 1);
         for (int t = threadIdx.x; t < tri.n; t += blockDim.x) {
@@ -1745,6 +1739,24 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
         for (int t = threadIdx.x; t < 2 * (c.n_leaf - 1); t += blockDim.x) ts.kid[t] = tr.kid[t];
         for (int t = threadIdx.x; t <= c.n_levels; t += blockDim.x) ts.lvl[t] = tr.lvl[t];
     }
+}
+
+__device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, EngineState *__restrict__ st,
+                                                  const double *__restrict__ sched, const double *cand,
+                                                  double *__restrict__ fit, int32_t *__restrict__ slot_of,
+                                                  int32_t *__restrict__ spare_of, uint8_t *__restrict__ slot_bin,
+                                                  double *__restrict__ scratch, const SumTree &tr,
+                                                  double *__restrict__ trace, const SumTreeInline &tri, bool wait,
+                                                  uint32_t *__restrict__ slot_tag, bool staged = false) {
+    const int64_t n = c.NP;
+    // dynamic shared memory: [fit (n), squared deviations (n)] when n fits,
+    // then the pairwise-sum tree (values, leaf offsets, children, levels)
+    extern __shared__ double s_dyn[];
+    const bool on_chip = n <= kStatsSmemMaxNP;
+    double *fv = on_chip ? s_dyn : fit;
+    double *sq = on_chip ? s_dyn + n : scratch;
+    const TreeSmem ts = stats_tree_smem(c, s_dyn);
+    if (!staged) stats_tree_stage(c, tr, tri, ts);  // (the fused caller stages it at its entry)
     if (wait) pdl_wait();
     // the state is copied to shared memory for the serial tail: its words are
     // loaded here and stored after the fitness loads below are in flight
@@ -1963,6 +1975,8 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
                                                                double *__restrict__ trace, SumTreeInline tri,
                                                                unsigned *cnt, uint32_t *__restrict__ slot_tag) {
     QTRACE(MODE == 0 ? 3 : 5);
+    extern __shared__ double s_dyn[];
+    if (MODE == 1) stats_tree_stage(c, tr, tri, stats_tree_smem(c, s_dyn));  // every CTA: any may be the last
     pdl_wait();
     pdl_trigger<4>();
     QTRACE_STARTED();
@@ -1988,20 +2002,26 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
             }
         }
     }
+    // arrival: the barrier orders this CTA's selections before thread 0's
+    // acquire-release add (cumulative at gpu scope); the last CTA's thread 0
+    // acquires every other CTA's, and its barrier passes that on to the CTA
+    // (the grid-synchronisation pattern, one fence-free atomic per CTA)
     __shared__ unsigned s_last;
-    __threadfence();  // this CTA's selections, before its arrival
     __syncthreads();
     QSTAMP(1);
-    if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1u) + 1u == gridDim.x;
+    if (threadIdx.x == 0) {
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
+        s_last = prev + 1u == gridDim.x;
+    }
     __syncthreads();
     if (!s_last) return;
     if (threadIdx.x == 0) QSTAMP_ANY(2);
-    __threadfence();
     if (MODE == 0)
         block_topk_k(fit, c.NP, c.k, st->leaders);
     else
         select_stats_body(c, 3, st, sched, cand, fit, slot_of, spare_of, slot_bin, scratch, tr, trace, tri, false,
-                          nullptr);
+                          nullptr, true);
     if (threadIdx.x == 0) QSTAMP_ANY(3);
     if (threadIdx.x == 0) *cnt = 0u;  // ready for the next launch (stream-ordered)
 }
