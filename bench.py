@@ -256,10 +256,11 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_basis": f"hbm_gbs ({peaks_kind})",
                 "algorithmic_unit": f"{DE_BYTES_PER_GENE:.3f} B per gene (CR={CR}) x NP*D",
-                "note": "k_de_trial also draws the generation's crossover mask and the first two wolf draws "
-                        "(3 splitmix64 draws per gene, ~19 SASS instructions each, of its ~133 per gene); it is "
-                        "integer-issue bound, see int_issue (ncu, profiles/r02/ncu_summary_r02.txt)"}
-        summ = os.path.join(ROOT, "profiles", "r02", "ncu_summary_r02.txt")
+                "note": "k_de_trial_tma (source rows staged by TMA bulk copies) also draws the generation's "
+                        "crossover mask and the first two wolf draws (3 splitmix64 draws per gene, ~24 SASS "
+                        "instructions each, of its ~139 per gene); it is integer-issue bound, see int_issue "
+                        "(ncu, profiles/r02b/ncu_summary_r02b.txt)"}
+        summ = os.path.join(ROOT, "profiles", "r02b", "ncu_summary_r02b.txt")
         if os.path.exists(summ):
             hdr = None
             for line in open(summ):  # tools/ncu_summary.py table (first table: the C2 generation)
@@ -272,7 +273,7 @@ def stage_roofline(stages, ms_gen_total, peaks, peaks_kind, sm_count, traffic_db
                                          "fmaheavy_pipe_pct_of_elapsed": float(v["FMAheavy%"]),
                                          "warp_instr_per_launch": float(v["Minst"]) * 1e6,
                                          "source": "ncu --set full, C2 late generation "
-                                                   "(profiles/r02/ncu_summary_r02.txt)"}
+                                                   "(profiles/r02b/ncu_summary_r02b.txt)"}
                     break
     else:
         nbytes = NP * D * 8
