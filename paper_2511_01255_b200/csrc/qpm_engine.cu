@@ -1572,7 +1572,10 @@ struct TreeSmem {
     double *val;
 };
 
-__device__ double block_pairwise(const double *v, const RunConsts &c, const TreeSmem &ts) {
+// SQDEV: the sum of (v_i - m)^2 instead, each term formed as numpy's
+// `x = arr - mean; x = x * x` forms it (no separate squared-deviation pass)
+template <bool SQDEV = false>
+__device__ double block_pairwise(const double *v, const RunConsts &c, const TreeSmem &ts, double m = 0.0) {
     const int lane = threadIdx.x & 31, sub = lane & 7;
     const int groups = (int)(blockDim.x >> 3);
     for (int base = (int)(threadIdx.x >> 3) - (lane >> 3); base < c.n_leaf; base += groups) {
@@ -1581,7 +1584,7 @@ __device__ double block_pairwise(const double *v, const RunConsts &c, const Tree
         const int off = ok ? ts.leaf_off[l] : 0;
         const int len = ok ? ts.leaf_off[l + 1] - off : 0;
         const double *a = v + off;
-        const int m = len - len % 8;
+        const int mlen = len - len % 8;
         double r = 0.0;
         if (len >= 8) {
             // a leaf has <= 128 elements, so <= 16 per accumulator: every
@@ -1589,18 +1592,31 @@ __device__ double block_pairwise(const double *v, const RunConsts &c, const Tree
             // order (a dependent chain of adds instead of load-add round trips)
             double x[16];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) x[t] = sub + 8 * t < m ? a[sub + 8 * t] : 0.0;
+            for (int t = 0; t < 16; ++t) {
+                x[t] = sub + 8 * t < mlen ? a[sub + 8 * t] : 0.0;
+                if (SQDEV) {
+                    const double d = x[t] - m;
+                    x[t] = d * d;
+                }
+            }
             r = x[0];
 #pragma unroll
             for (int t = 1; t < 16; ++t)
-                if (sub + 8 * t < m) r += x[t];
+                if (sub + 8 * t < mlen) r += x[t];
         }
         r += __shfl_xor_sync(0xffffffffu, r, 1);
         r += __shfl_xor_sync(0xffffffffu, r, 2);
         r += __shfl_xor_sync(0xffffffffu, r, 4);
         if (ok && sub == 0) {
             double res = len >= 8 ? r : 0.0;
-            for (int i = m; i < len; ++i) res += a[i];
+            for (int i = mlen; i < len; ++i) {
+                double t = a[i];
+                if (SQDEV) {
+                    const double d = t - m;
+                    t = d * d;
+                }
+                res += t;
+            }
             ts.val[l] = res;
         }
     }
@@ -1754,7 +1770,6 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
     extern __shared__ double s_dyn[];
     const bool on_chip = n <= kStatsSmemMaxNP;
     double *fv = on_chip ? s_dyn : fit;
-    double *sq = on_chip ? s_dyn + n : scratch;
     const TreeSmem ts = stats_tree_smem(c, s_dyn);
     if (!staged) stats_tree_stage(c, tr, tri, ts);  // (the fused caller stages it at its entry)
     if (wait) pdl_wait();
@@ -1860,12 +1875,7 @@ __device__ __forceinline__ void select_stats_body(const RunConsts &c, int mode, 
     const double sum = block_pairwise(fv, c, ts);
     const double mean = n_pow2 ? sum * inv_n : sum / (double)n;
     if (mode == 3 && threadIdx.x == 0) QSTAMP_ID(5, 6);
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double d = fv[i] - mean;
-        sq[i] = d * d;
-    }
-    __syncthreads();
-    const double ssq = block_pairwise(sq, c, ts);
+    const double ssq = block_pairwise<true>(fv, c, ts, mean);  // (fv is published: block_pairwise ends in a barrier)
     const double var = n_pow2 ? ssq * inv_n : ssq / (double)n;
     if (threadIdx.x != 0) return;
     if (mode == 3) QSTAMP_ID(5, 7);
