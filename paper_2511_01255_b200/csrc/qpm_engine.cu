@@ -840,11 +840,15 @@ __device__ __forceinline__ void de_trial_dispatch(const RunConsts &c, const Tria
 }
 
 // Warp items (short rows -- a column shard of a multi-GPU run, Dp <=
-// kDeRowsMaxDp -- or QPM_DE_ROWS): each warp walks the genes [ch k, ch (k+1))
+// kDeRowsDefaultDp -- or QPM_DE_ROWS): each warp walks the genes [ch k, ch (k+1))
 // of one row (ch = whole row for short rows), eight items per CTA.  Each
 // warp resolves its own row (lane 0, broadcast through shared memory) with no
 // CTA barrier, so a row's setup latency hides under the other warps' work.
 constexpr int kDeRowsMaxDp = 4096;
+// the default switch to warp items: the TMA-staged row kernel wins above it
+// (emulated C2-shape shards, tools/shard_probe.py: W = 4 (2,560 genes) trial +
+// scan phase 129.5 -> 109.6 us with TMA; W = 8 (1,280 genes) 117.5 -> 135.3 us)
+constexpr int kDeRowsDefaultDp = 2048;
 template <int K>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_rows(RunConsts c, TrialArgs a, int ch) {
     QTRACE(0);
@@ -2253,7 +2257,7 @@ struct Engine {
     int S_cur = 1;                     // segments of the last one-GPU scan
     int32_t *topk_idx = nullptr;       // [kTopkMaxCtas][kTopSlots] per-CTA lists
     unsigned *topk_cnt = nullptr;      // arrival counter
-    int64_t de_rows_max_dp = kDeRowsMaxDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
+    int64_t de_rows_max_dp = kDeRowsDefaultDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
     bool de_tma = QPM_DE_TMA != 0;          // TMA-staged trial rows (QPM_DE_TMA=0: global loads)
     int de_item = 1024;                      // genes per warp item on longer rows (QPM_DE_ITEM, multiple of 128)
     int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)

@@ -701,6 +701,9 @@ int launch_fitness_scan(const Problem *p, const uint32_t *bits, int64_t row_word
     const int64_t per_wave = sms / ((int64_t)p->S * p->n_wl);  // row blocks one wave holds
     if (p->n_wl == 1 && blocks * p->S <= sms && per_wave > blocks)
         bt = (int)std::max<int64_t>(64, ((rows + per_wave - 1) / per_wave + 31) / 32 * 32);
+#ifdef QPM_FIT_BT_FORCE  // (A/B builds only)
+    if (p->n_wl == 1 && blocks * p->S <= sms) bt = QPM_FIT_BT_FORCE;
+#endif
     const dim3 grid((unsigned)p->S, (unsigned)((rows + bt - 1) / bt), (unsigned)p->n_wl);
     QPM_CUDA_TRY(launch_k(pdl, thg ? k_fit_fast<true> : k_fit_fast<false>, grid, dim3(bt), kFitSmem, stream,
                           (const double2 *)p->qt, p->nquads, p->nchunks, p->seg_chunks, S_stride, bits, p->W, row_index,
