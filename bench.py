@@ -400,6 +400,12 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        # a ~0.2 ms spin kernel ahead of the start event keeps the GPU busy
+        # while the host records the events and launches the K generations, so
+        # the window holds the generations back to back, not the host's launch
+        # latency (the same gate for every rank)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(2e-4 * 1.965e9))
         start.record(stream)
         eng.step(args.steps)
         end.record(stream)
