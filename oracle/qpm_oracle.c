@@ -267,6 +267,7 @@ typedef struct {
 static void qpo_eval_body(void *vctx, int64_t r) {
     qpo_eval_ctx *c = (qpo_eval_ctx *)vctx;
     double gains_stack[2 * 256];
+    gains_stack[0] = 0.0; /* (n_wl >= 1: silences gcc's maybe-uninitialized) */
     double *gains = c->P->n_wl <= 256 ? gains_stack : (double *)malloc(sizeof(double) * 2 * c->P->n_wl);
     c->out[r] = qpo_eval_row(c->P, c->signs + (size_t)r * c->P->D, gains);
     if (gains != gains_stack) free(gains);
