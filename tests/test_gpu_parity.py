@@ -273,3 +273,23 @@ def test_validation_errors(q):
         q.DEParams(cr=1.5)
     r = q.run_hybrid(obj, dimension=16, pop_size=8, generations=0, seed=3)
     assert len(r.trace) == 1
+
+
+@pytest.mark.parametrize("algorithm", ["hybrid", "de", "gwo"])
+@pytest.mark.parametrize("D,NP", [(2050, 5), (4097, 13), (6000, 7)])
+def test_odd_shapes_exact_vs_oracle(q, algorithm, D, NP):
+    """Row lengths around the trial's chunk / stage / word boundaries (2,050:
+    stages of 1,024 + 1,024 + 128 genes; 4,097: a 1-gene tail past a chunk;
+    6,000: a partial second chunk) and tiny odd populations: exact-mode runs
+    equal the oracle bit for bit (trace, best genome, projection, fitness)."""
+    G, seed = 12, 5
+    spec = q.ObjectiveSpec("single_thg", (1404.0,))
+    obj = q.make_objective(spec, q.default_dispersion(), 1.0, D, mode="exact")
+    res = q.run(algorithm, obj, dimension=D, pop_size=NP, generations=G, seed=seed)
+    t = obj.tables[0]
+    P = O.Problem("thg", t.e1[None], t.b[None], np.array([t.w]), np.array([t.hconst]), t.normalization)
+    trace, bg, bp, bf = O.run(P, algorithm, NP, G, seed)
+    assert np.array_equal(np.array(res.trace, dtype=np.float64), trace)
+    assert np.array_equal(res.best.genome, bg)
+    assert np.array_equal(res.best.projection, bp)
+    assert res.best.fitness == bf
