@@ -137,16 +137,15 @@ def cpu_baseline(threads: int = 0, target_s: float = 12.0, with_reference_packag
 
     tb = T.build_tables("thg", THICKNESS_UM, D, T.phase_mismatches(T.default_dispersion(25.0), PUMP_NM))
     P = O.Problem("thg", tb.e1[None], tb.b[None], np.array([tb.w]), np.array([tb.hconst]), tb.normalization)
-    t0 = time.perf_counter()
-    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=0)
-    t_init = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=2)
-    per_gen = max((time.perf_counter() - t0 - t_init) / 2, 1e-4)
+    # generation end times inside one run (the oracle stamps each trace row):
+    # a probe of 2 generations sizes the sample, the sample is timed from the
+    # end of generation 0 (init excluded) to the end of generation `gens`
+    stamps = np.zeros(G_RUN + 1)
+    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=2, gen_end_s=stamps)
+    per_gen = max((stamps[2] - stamps[0]) / 2, 1e-4)
     gens = int(min(max(target_s / per_gen, 3), 200))
-    t0 = time.perf_counter()
-    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=gens)
-    dt = time.perf_counter() - t0 - t_init
+    O.run(P, "hybrid", NP, G_RUN, SEED, threads=threads, stop_after=gens, gen_end_s=stamps)
+    dt = float(stamps[gens] - stamps[0])
     cores = threads if threads > 0 else O.max_threads()
     out = {"value": evals_per_generation() * gens / dt, "unit": UNIT, "cores": cores, "kind": "port",
            "sample": f"oracle/qpm_oracle.c run_hybrid C2 generations 1..{gens} of a {G_RUN}-generation run "
@@ -209,13 +208,11 @@ def run_reference(args):
     tb = T.build_tables("thg", THICKNESS_UM, D, T.phase_mismatches(T.default_dispersion(25.0), PUMP_NM))
     P = O.Problem("thg", tb.e1[None], tb.b[None], np.array([tb.w]), np.array([tb.hconst]), tb.normalization)
     G = max(G_RUN, args.warmup + args.steps)
-    t0 = time.perf_counter()
-    O.run(P, "hybrid", NP, G, SEED, stop_after=args.warmup)
-    t_w = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.run(P, "hybrid", NP, G, SEED, stop_after=args.warmup + args.steps)
-    t_wk = time.perf_counter() - t0
-    dt = max(t_wk - t_w, 1e-9)
+    # one run through generation W + K; the window is timed inside it from the
+    # oracle's per-generation stamps (end of generation W to end of W + K)
+    stamps = np.zeros(G + 1)
+    O.run(P, "hybrid", NP, G, SEED, stop_after=args.warmup + args.steps, gen_end_s=stamps)
+    dt = float(stamps[args.warmup + args.steps] - stamps[args.warmup])
     value = evals_per_generation() * args.steps / dt
     cores = O.max_threads()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,

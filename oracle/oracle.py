@@ -114,6 +114,7 @@ def lib():
                                           ctypes.c_int64, P]
         L.qpo_run.restype = ctypes.c_int64
         L.qpo_run.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(_Params), P, P, P, P]
+        L.qpo_run_timed.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(_Params), P, P, P, P, P]
         L.qpo_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -311,8 +312,10 @@ class RunSettings:
 
 
 def run(problem: Problem, algorithm: str, NP: int, G: int, seed: int, settings: RunSettings | None = None,
-        threads: int = 0, stop_after: int = -1):
-    """Returns (trace [rows, 5], best_genome, best_proj, best_fit)."""
+        threads: int = 0, stop_after: int = -1, gen_end_s: np.ndarray | None = None):
+    """Returns (trace [rows, 5], best_genome, best_proj, best_fit).  gen_end_s
+    (float64 [G+1], optional) receives the monotonic time at which each
+    generation's trace row was complete (benchmark windows inside one run)."""
     s = settings or RunSettings()
     D = problem.D
     p = _Params(ALGORITHMS[algorithm], NP, D, G, _wrap_seed(seed), s.f_max, s.f_min, s.cr, s.x_min, s.x_max,
@@ -326,7 +329,12 @@ def run(problem: Problem, algorithm: str, NP: int, G: int, seed: int, settings: 
     bp = np.empty(D, dtype=np.int8)
     bf = np.empty(1)
     cs = problem.c_struct()
-    n = lib().qpo_run(ctypes.byref(cs), ctypes.byref(p), _ptr(trace), _ptr(bg), _ptr(bp), _ptr(bf))
+    if gen_end_s is not None:
+        assert gen_end_s.dtype == np.float64 and gen_end_s.size >= G + 1
+        n = lib().qpo_run_timed(ctypes.byref(cs), ctypes.byref(p), _ptr(trace), _ptr(bg), _ptr(bp), _ptr(bf),
+                                _ptr(gen_end_s))
+    else:
+        n = lib().qpo_run(ctypes.byref(cs), ctypes.byref(p), _ptr(trace), _ptr(bg), _ptr(bp), _ptr(bf))
     return trace[:n], bg, bp, float(bf[0])
 
 

@@ -23,6 +23,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
@@ -546,8 +547,30 @@ static void qpo_gwoc_body(void *vctx, int64_t t) {
  * Full run.  trace: (G+1) x 5 rows (generation, best, mean, F|a, pop_std).
  * best_genome (D), best_proj (D), best_fit (1).  Returns number of trace rows.
  */
+static double qpo_now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static int64_t qpo_run_impl(const qpo_problem *P, const qpo_params *p, double *trace, double *best_genome,
+                            int8_t *best_proj, double *best_fit, double *t_end);
+
 int64_t qpo_run(const qpo_problem *P, const qpo_params *p, double *trace, double *best_genome,
                 int8_t *best_proj, double *best_fit) {
+    return qpo_run_impl(P, p, trace, best_genome, best_proj, best_fit, NULL);
+}
+
+/* The same run, with t_end[g] = monotonic seconds when generation g's trace
+ * row is complete (g = 0: the initial population): benchmark windows time
+ * generations w+1..w+k as t_end[w+k] - t_end[w] inside one run. */
+int64_t qpo_run_timed(const qpo_problem *P, const qpo_params *p, double *trace, double *best_genome,
+                      int8_t *best_proj, double *best_fit, double *t_end) {
+    return qpo_run_impl(P, p, trace, best_genome, best_proj, best_fit, t_end);
+}
+
+static int64_t qpo_run_impl(const qpo_problem *P, const qpo_params *p, double *trace, double *best_genome,
+                            int8_t *best_proj, double *best_fit, double *t_end) {
     const int64_t NP = p->NP, D = p->D, G = p->G;
     const int64_t stop = p->stop_after >= 0 && p->stop_after < G ? p->stop_after : G;
     const int threads = p->threads;
@@ -594,6 +617,7 @@ int64_t qpo_run(const qpo_problem *P, const qpo_params *p, double *trace, double
         *best_fit = fit[bi];
         qpo_trace_row(trace, 0, fit, NP, p->gwo_a, scratch, NULL, NULL, NULL);
         rows_out = 1;
+        if (t_end) t_end[0] = qpo_now_s();
         for (int64_t g = 1; g <= stop; ++g) {
             double progress = G ? (double)g / (double)G : 0.0;
             c.g = g;
@@ -621,6 +645,7 @@ int64_t qpo_run(const qpo_problem *P, const qpo_params *p, double *trace, double
             }
             qpo_trace_row(trace + 5 * g, g, fit, NP, c.a_now, scratch, NULL, NULL, NULL);
             rows_out = g + 1;
+            if (t_end) t_end[g] = qpo_now_s();
         }
         goto done;
     }
@@ -634,6 +659,7 @@ int64_t qpo_run(const qpo_problem *P, const qpo_params *p, double *trace, double
     int win_len = 0, win_head = 0;
     const int win_cap = p->conv_window > 1 ? p->conv_window : 1;
     rows_out = 1;
+    if (t_end) t_end[0] = qpo_now_s();
     const int k = p->leader_count;
     c.k = k;
 
@@ -701,6 +727,7 @@ int64_t qpo_run(const qpo_problem *P, const qpo_params *p, double *trace, double
         row[3] = F;
         memcpy(trace + 5 * g, row, sizeof(row));
         rows_out = g + 1;
+        if (t_end) t_end[g] = qpo_now_s();
     }
     {
         int64_t bi;
