@@ -481,9 +481,7 @@ def run_ours(args):
         mark("create")
         e3.init()
         mark("init")
-        e3.prepare(args.steps)
-        mark("graph_capture")
-        e3.step(args.steps)
+        e3.step(args.steps)  # as run_hybrid: eager launches below 256 generations, graphs captured inside above
         mark("generations")
         e3.finalize()
         e3.trace(0, args.steps + 1)
