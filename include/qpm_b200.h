@@ -28,6 +28,7 @@
  *                                      (optimizer.py:52-56), bit-packed
  *   qpm_reduce_best                 -> parexec.reduce_best (parexec.py:123-154)
  *   qpm_sweep_spectrum              -> physics.sweep_spectrum (physics.py:378-395),
+ *   qpm_wavelength_scalars          -> the per-wavelength Sellmeier / moment precompute (physics.py:97-339),
  *                                      batched over patterns
  *   qpm_brute_force                 -> bench.brute_force_oracle (bench.py:179-209)
  *                                      with bench.lexicographic_signs (:169-176)
@@ -146,6 +147,20 @@ int qpm_reduce_best(const double *values_dev, int64_t n, int k, int32_t *idx_out
  * |d| agrees with the reference to ~1e-12 relative.  Synchronous. */
 int qpm_sweep_spectrum(int process, double thickness, int64_t D, const int8_t *signs, int64_t P, const double *dk,
                        const double *w, const double *hphi, int64_t M, double *out);
+
+/* Per-wavelength scalars of a Sellmeier dispersion model on the device
+ * (replaces the host loop of physics.sweep_spectrum / ThgEvaluator over pump
+ * wavelengths: physics.py:97-110 refractive index, 184-197 mismatches,
+ * 224-270 moment integrals, 285-293 / 325-339 w and the cascade factor).
+ * sellmeier_terms[6] = {a1 + b1 ft, a6, a2 + b2 ft, (a3 + b3 ft)**2, a4 + b4 ft,
+ * a5**2} with ft = (T - 24.5)(T + 570.82), computed by the caller (Python's
+ * x**2 is libm pow).  wavelengths_nm: host [M] (the caller checks the model's
+ * validity range).  Out (host [M][2]): dk = (dk1, dk2) bit-identical to the
+ * host formula; w (w1 for SHG, w12 for THG) and hphi = t^2 phi(i dk1 t, i dk2 t)
+ * within ~1e-16 relative (device exp/sincos).  QPM_ERR_ARG with *bad_index =
+ * the first wavelength whose n^2 <= 1; else *bad_index = -1.  Synchronous. */
+int qpm_wavelength_scalars(int process, double thickness, const double *sellmeier_terms, const double *wavelengths_nm,
+                           int64_t M, double *dk, double *w, double *hphi, int64_t *bad_index);
 
 /* ------------------------------------------------------ exhaustive search */
 /* Global optimum over all 2^n sign patterns of a problem with D = n (n <= 63):

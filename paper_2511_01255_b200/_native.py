@@ -11,6 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libqpm_b200.so")
 
+QPM_OK, QPM_ERR_ARG, QPM_ERR_CUDA, QPM_ERR_STATE, QPM_ERR_NCCL = 0, -1, -2, -3, -4
 QPM_PROCESS_SHG, QPM_PROCESS_THG = 0, 1
 QPM_MODE_FAST, QPM_MODE_EXACT = 0, 1
 QPM_ALGO = {"hybrid": 0, "de": 1, "gwo": 2}
@@ -22,6 +23,7 @@ EXPORTS = (
     "qpm_last_error", "qpm_version", "qpm_device_info", "qpm_release_cached_memory", "qpm_fold_key", "qpm_uniform_fill",
     "qpm_problem_create", "qpm_problem_destroy", "qpm_problem_row_words", "qpm_problem_layout", "qpm_pack_signs",
     "qpm_fitness_bits", "qpm_evaluate_block_host", "qpm_sum_block_host", "qpm_reduce_best", "qpm_brute_force", "qpm_sweep_spectrum",
+    "qpm_wavelength_scalars",
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
     "qpm_engine_step", "qpm_engine_prepare", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
     "qpm_engine_read_best", "qpm_engine_read_population", "qpm_engine_profile", "qpm_engine_launches_per_generation",
@@ -103,6 +105,7 @@ def lib():
         "qpm_reduce_best": (I32, [P, I64, I32, P, P]),
         "qpm_brute_force": (I32, [P, I32, I32, I64, P, P, P]),
         "qpm_sweep_spectrum": (I32, [I32, ctypes.c_double, I64, P, I64, P, P, P, I64, P]),
+        "qpm_wavelength_scalars": (I32, [I32, ctypes.c_double, P, P, I64, P, P, P, P]),
         "qpm_engine_create": (I32, [P, P, ctypes.POINTER(RunParams), P, P]),
         "qpm_engine_destroy": (I32, [P]),
         "qpm_engine_device_bytes": (I64, [P]),

@@ -925,6 +925,133 @@ static int host_path_reserve(Problem *p, int64_t rows) {
     return problem_reserve(p, rows);
 }
 
+// ---------------------------------------------------------------- per-wavelength scalars
+// Sellmeier dispersion and the per-domain moment integrals of many pump
+// wavelengths on the device (reference physics.py:97-110,
+// 147-197, 224-270, restated host-side in tables.py).  The wavelength-free
+// Sellmeier terms come from the host (Python's pole**2 is libm pow, which is
+// not always x*x), so n(lambda) and the mismatches dk1, dk2 are the host's
+// bit for bit (IEEE + - * / sqrt, no contraction: -fmad=false).  The moment
+// integrals replay CPython's complex arithmetic (component products without
+// FMA, _Py_c_quot's scaled division, cmath.exp as exp(re) (cos, sin)); device
+// exp/sin/cos are within an ulp of libm, so w and the cascade factor agree to
+// ~1e-16 relative.
+struct SellmeierTerms {
+    double v[6];
+};
+struct Cx {
+    double re, im;
+};
+__device__ __forceinline__ Cx cx_mul(Cx a, Cx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ __forceinline__ Cx cx_sub(Cx a, Cx b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ Cx cx_add(Cx a, Cx b) { return {a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ Cx cx_divr(Cx a, double c) { return {a.re / c, a.im / c}; }  // complex / real
+__device__ __forceinline__ Cx cx_div(Cx a, Cx b) {  // CPython _Py_c_quot
+    const double abr = fabs(b.re), abi = fabs(b.im);
+    if (abr >= abi) {
+        if (abr == 0.0) return {0.0, 0.0};
+        const double ratio = b.im / b.re;
+        const double denom = b.re + b.im * ratio;
+        return {(a.re + a.im * ratio) / denom, (a.im - a.re * ratio) / denom};
+    }
+    const double ratio = b.re / b.im;
+    const double denom = b.re * ratio + b.im;
+    return {(a.re * ratio + a.im) / denom, (a.im * ratio - a.re) / denom};
+}
+__device__ __forceinline__ Cx cx_exp(Cx z) {  // cmath.exp, finite arguments
+    const double l = exp(z.re);
+    if (z.im == 0.0) return {l, z.im};
+    double sn, cs;
+    sincos(z.im, &sn, &cs);
+    return {l * cs, l * sn};
+}
+__device__ __forceinline__ double cx_abs(Cx z) { return hypot(z.re, z.im); }
+__device__ __forceinline__ Cx cx_neg(Cx z) { return {-z.re, -z.im}; }
+
+constexpr double kSeriesCutoff = 0.25, kPhiCutoff = 1e-6, kSeriesTol = 1e-20;
+
+__device__ Cx dev_moment0(Cx x) {  // tables.moment0
+    if (cx_abs(x) < kSeriesCutoff) {
+        Cx acc = {0.0, 0.0}, term = {1.0, 0.0};
+        for (int m = 0; cx_abs(term) > kSeriesTol && m < 200; ) {
+            acc = cx_add(acc, cx_divr(term, (double)(m + 1)));
+            ++m;
+            term = cx_mul(term, cx_divr(cx_neg(x), (double)m));
+        }
+        return acc;
+    }
+    const Cx e = cx_exp(cx_neg(x));
+    return cx_div(Cx{1.0 - e.re, 0.0 - e.im}, x);
+}
+__device__ Cx dev_moment(int n, Cx x) {  // tables.moment
+    if (n == 0) return dev_moment0(x);
+    if (cx_abs(x) < 2.0 * kSeriesCutoff) {
+        Cx acc = {0.0, 0.0}, term = {1.0, 0.0};
+        for (int m = 0; cx_abs(term) / (double)(n + m + 1) > kSeriesTol && m < 200; ) {
+            acc = cx_add(acc, cx_divr(term, (double)(n + m + 1)));
+            ++m;
+            term = cx_mul(term, cx_divr(cx_neg(x), (double)m));
+        }
+        return acc;
+    }
+    const Cx decay = cx_exp(cx_neg(x));
+    Cx val = dev_moment0(x);
+    for (int p = 1; p <= n; ++p) val = cx_div(cx_sub(Cx{(double)p * val.re, (double)p * val.im}, decay), x);
+    return val;
+}
+__device__ Cx dev_cascade(Cx x1, Cx x2) {  // tables.cascade_factor
+    if (cx_abs(x1) < kPhiCutoff) {
+        const Cx a = dev_moment(1, x2);
+        const Cx b = cx_divr(cx_mul(x1, dev_moment(2, x2)), 2.0);
+        const Cx c = cx_divr(cx_mul(cx_mul(x1, x1), dev_moment(3, x2)), 6.0);
+        return cx_add(cx_sub(a, b), c);
+    }
+    return cx_div(cx_sub(dev_moment0(x2), dev_moment0(cx_add(x1, x2))), x1);
+}
+
+// n(lambda) from the host's wavelength-free terms: sm = {a1 + b1 ft, a6,
+// a2 + b2 ft, (a3 + b3 ft)**2, a4 + b4 ft, a5**2}; flags n^2 <= 1 in *bad
+__device__ __forceinline__ double dev_index(const double *sm, double wl_um, int *bad) {
+    const double w2 = wl_um * wl_um;
+    double n2 = sm[0] - sm[1] * w2;
+    if (sm[2] != 0.0) n2 += sm[2] / (w2 - sm[3]);
+    if (sm[4] != 0.0) n2 += sm[4] / (w2 - sm[5]);
+    if (!(n2 > 1.0)) *bad = 1;
+    return sqrt(n2);
+}
+
+__global__ void k_wavelength_scalars(int thg, double t, SellmeierTerms st, const double *__restrict__ wl_nm,
+                                     int64_t M, double2 *__restrict__ dk, double2 *__restrict__ w,
+                                     double2 *__restrict__ hphi, int *__restrict__ bad_index) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const double two_pi = 2.0 * 3.141592653589793;  // 2.0 * np.pi
+    const double lam = wl_nm[m] * 1e-3;
+    int bad = 0;
+    const double kp = two_pi * dev_index(st.v, lam, &bad) / lam;
+    const double lh = lam / 2.0, lt = lam / 3.0;
+    const double ksh = two_pi * dev_index(st.v, lh, &bad) / lh;
+    const double kth = two_pi * dev_index(st.v, lt, &bad) / lt;
+    if (bad) atomicMin(bad_index, (int)m);
+    const double dk1 = ksh - 2.0 * kp, dk2 = kth - ksh - kp;
+    dk[m] = make_double2(dk1, dk2);
+    const Cx x1 = {0.0 * dk1 - 0.0, dk1 * t};  // 1j * dk1 * t as CPython forms it
+    const Cx m1 = dev_moment0(x1);
+    const Cx w1 = {t * m1.re, t * m1.im};
+    if (!thg) {
+        w[m] = make_double2(w1.re, w1.im);
+        hphi[m] = make_double2(0.0, 0.0);
+        return;
+    }
+    const Cx x2 = {0.0 * dk2 - 0.0, dk2 * t};
+    const Cx m2 = dev_moment0(x2);
+    const Cx w12 = cx_mul(w1, Cx{t * m2.re, t * m2.im});
+    const Cx cf = dev_cascade(x1, x2);
+    const double tt = t * t;
+    w[m] = make_double2(w12.re, w12.im);
+    hphi[m] = make_double2(tt * cf.re, tt * cf.im);
+}
+
 }  // namespace qpm
 
 using namespace qpm;
@@ -1120,6 +1247,60 @@ int qpm_evaluate_block_host(qpm_problem *h, const int8_t *signs, int64_t rows, d
     QPM_CUDA_TRY(cudaMemcpyAsync(out, p.hp_out, (size_t)rows * sizeof(double), cudaMemcpyDeviceToHost, p.hp_stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(p.hp_stream));
     return QPM_OK;
+}
+
+int qpm_wavelength_scalars(int process, double thickness, const double *sellmeier_terms, const double *wavelengths_nm,
+                           int64_t M, double *dk, double *w, double *hphi, int64_t *bad_index) {
+    QPM_ARG_CHECK(process == QPM_PROCESS_SHG || process == QPM_PROCESS_THG, "process");
+    QPM_ARG_CHECK(sellmeier_terms && wavelengths_nm && dk && w && hphi && bad_index, "buffers");
+    QPM_ARG_CHECK(M >= 1 && M <= (1LL << 31) - 1, "wavelength count");
+    SellmeierTerms st;
+    for (int k = 0; k < 6; ++k) st.v[k] = sellmeier_terms[k];
+    const size_t lb = (size_t)M * sizeof(double), tb = (size_t)M * sizeof(double2);
+    double *d_wl = (double *)dev_cache_alloc(lb);
+    double2 *d_dk = (double2 *)dev_cache_alloc(tb), *d_w = (double2 *)dev_cache_alloc(tb);
+    double2 *d_h = (double2 *)dev_cache_alloc(tb);
+    int *d_bad = (int *)dev_cache_alloc(sizeof(int));
+    int rc = QPM_OK;
+    if (!d_wl || !d_dk || !d_w || !d_h || !d_bad) {
+        set_error("out of device memory");
+        rc = QPM_ERR_CUDA;
+    }
+    cudaStream_t s = nullptr;
+    int h_bad = INT32_MAX;
+    if (!rc && (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaMemcpyAsync(d_wl, wavelengths_nm, lb, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                cudaMemcpyAsync(d_bad, &h_bad, sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess)) {
+        set_error("wavelength upload failed");
+        rc = QPM_ERR_CUDA;
+    }
+    if (!rc) {
+        k_wavelength_scalars<<<(unsigned)((M + 127) / 128), 128, 0, s>>>(process == QPM_PROCESS_THG, thickness, st, d_wl,
+                                                                        M, d_dk, d_w, d_h, d_bad);
+        if (cudaGetLastError() != cudaSuccess || cudaMemcpyAsync(dk, d_dk, tb, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(w, d_w, tb, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(hphi, d_h, tb, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            set_error("wavelength scalars kernel failed");
+            rc = QPM_ERR_CUDA;
+        }
+    }
+    if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+    dev_cache_release(d_wl, lb);
+    dev_cache_release(d_dk, tb);
+    dev_cache_release(d_w, tb);
+    dev_cache_release(d_h, tb);
+    dev_cache_release(d_bad, sizeof(int));
+    *bad_index = rc ? -1 : (h_bad == INT32_MAX ? -1 : (int64_t)h_bad);
+    if (!rc && h_bad != INT32_MAX) {
+        set_error("Sellmeier model yields n^2 <= 1 for pump wavelength index %d", h_bad);
+        rc = QPM_ERR_ARG;
+    }
+    return rc;
 }
 
 int qpm_sweep_spectrum(int process, double thickness, int64_t D, const int8_t *signs, int64_t P, const double *dk,

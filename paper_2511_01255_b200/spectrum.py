@@ -4,7 +4,9 @@
 The reference builds the phase tables exp(-i dk z) of every wavelength on the
 host and scores one pattern per wavelength.  Here the per-wavelength scalars
 (dk from the dispersion provider, w = t m0(i dk t) products, the cascade
-factor) come from the same host code as the reference (tables.py), and the
+factor) are computed on the device for a Sellmeier model
+(`qpm_wavelength_scalars`: dk bit-identical to tables.py, w and the cascade
+factor within ~1e-16) or taken from an explicit mismatch table, and the
 O(D) tables are generated inside the kernel (`qpm_sweep_spectrum`), one CTA
 per (wavelength, pattern), so many wavelengths and many patterns are scored
 in one launch without uploading tables.  Device sincos differs from libm by at
@@ -17,9 +19,45 @@ import ctypes
 import numpy as np
 
 from . import _native
-from .tables import DomainPattern, cascade_factor, moment0
+from .tables import DispersionModel, DomainPattern, cascade_factor, moment0, phase_mismatches
 
 PROCESS_IDS = {"shg": _native.QPM_PROCESS_SHG, "thg": _native.QPM_PROCESS_THG}
+
+
+def _sellmeier_terms(model: DispersionModel) -> np.ndarray:
+    """The wavelength-free terms of tables.refractive_index, with Python's own
+    arithmetic (its pole**2 is libm pow): the device finishes n(lambda) from
+    them bit for bit."""
+    k = model.coefficient
+    temp = model.temperature_c
+    ft = (temp - 24.5) * (temp + 570.82)
+    return np.array([k("a1") + k("b1") * ft, k("a6"), k("a2") + k("b2") * ft, (k("a3") + k("b3") * ft) ** 2,
+                     k("a4") + k("b4") * ft, k("a5") ** 2], dtype=np.float64)
+
+
+def _device_wavelength_scalars(model: DispersionModel, wavelengths_nm, thickness_um: float, process: str):
+    """(dk, w, hphi) [M, 2] of a Sellmeier model computed on the device
+    (qpm_wavelength_scalars): dk bit-identical to the host loop, w / hphi to
+    ~1e-16.  Out-of-range wavelengths raise the reference's ValueError."""
+    wls = np.asarray(wavelengths_nm, dtype=np.float64)
+    lo, hi = model.wavelength_range_um
+    lam = wls * 1e-3
+    bad = (lam < lo) | (lam > hi) | (lam / 2.0 < lo) | (lam / 2.0 > hi) | (lam / 3.0 < lo) | (lam / 3.0 > hi)
+    if bad.any():  # the host formula raises the reference's message for the first offending wavelength
+        phase_mismatches(model, float(wls[int(np.argmax(bad))]))
+    M = len(wls)
+    dk = np.empty((M, 2))
+    w = np.empty((M, 2))
+    hphi = np.empty((M, 2))
+    bad_index = ctypes.c_int64(-1)
+    terms = _sellmeier_terms(model)
+    rc = _native.lib().qpm_wavelength_scalars(PROCESS_IDS[process], float(thickness_um), terms.ctypes.data,
+                                              wls.ctypes.data, M, dk.ctypes.data, w.ctypes.data, hphi.ctypes.data,
+                                              ctypes.byref(bad_index))
+    if rc == _native.QPM_ERR_ARG and bad_index.value >= 0:
+        phase_mismatches(model, float(wls[bad_index.value]))  # raises the reference's n^2 <= 1 message
+    _native.check(rc, "qpm_wavelength_scalars")
+    return dk, w, hphi
 
 
 def _wavelength_scalars(provider, wavelengths_nm, thickness_um: float, process: str):
@@ -55,7 +93,10 @@ def sweep_spectra(signs2d, thickness_um: float, provider, wavelengths_nm, proces
     if not wls:
         return out
     _native.require_cuda()
-    dk, w, hphi = _wavelength_scalars(provider, wls, thickness_um, process)
+    if isinstance(provider, DispersionModel):  # Sellmeier and moment integrals on the device
+        dk, w, hphi = _device_wavelength_scalars(provider, wls, thickness_um, process)
+    else:  # explicit mismatch tables: the provider's own values
+        dk, w, hphi = _wavelength_scalars(provider, wls, thickness_um, process)
     _native.check(_native.lib().qpm_sweep_spectrum(PROCESS_IDS[process], float(thickness_um), D,
                                                    signs.ctypes.data, P, dk.ctypes.data, w.ctypes.data,
                                                    hphi.ctypes.data, len(wls), out.ctypes.data),

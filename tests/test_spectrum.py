@@ -76,3 +76,41 @@ def test_device_spectra_batched_equal_single():
         for p in (0, 6):
             one = np.array(q.sweep_spectrum(q.DomainPattern(0.8, signs[p]), q.default_dispersion(), wls, process))
             assert np.array_equal(batch[p], one[:, 1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("process", ["thg", "shg"])
+@pytest.mark.parametrize("temperature", [25.0, 81.5])
+def test_device_wavelength_scalars_match_host(process, temperature):
+    """Sellmeier dispersion and the moment integrals on the device
+    (qpm_wavelength_scalars) against the host formulas the reference uses:
+    the mismatches bit-identical, w and the cascade factor within 1e-14."""
+    import paper_2511_01255_b200 as q
+    from paper_2511_01255_b200.spectrum import _device_wavelength_scalars, _wavelength_scalars
+
+    model = q.default_dispersion(temperature)
+    wls = np.concatenate([np.linspace(1250.0, 4900.0, 997), [1404.0, 1380.0, 1430.0]])
+    for t in (1.0, 0.37, 25.0):  # series and closed-form branches of the moment integrals
+        dk_d, w_d, h_d = _device_wavelength_scalars(model, wls, t, process)
+        dk_h, w_h, h_h = _wavelength_scalars(model, wls, t, process)
+        assert np.array_equal(dk_d, dk_h)
+        np.testing.assert_allclose(w_d, w_h, rtol=1e-14, atol=1e-14 * np.abs(w_h).max())
+        np.testing.assert_allclose(h_d, h_h, rtol=1e-14, atol=1e-14 * max(np.abs(h_h).max(), 1e-300))
+
+
+@pytest.mark.gpu
+def test_device_wavelength_scalars_errors_and_tables():
+    import paper_2511_01255_b200 as q
+
+    pat = q.DomainPattern(1.0, np.where(np.arange(64) % 3 == 0, -1, 1).astype(np.int8))
+    with pytest.raises(ValueError, match="below the model's valid minimum"):
+        q.sweep_spectrum(pat, q.default_dispersion(), [1404.0, 1100.0], "thg")  # 1100/3 nm is out of range
+    with pytest.raises(ValueError, match="above the model's valid maximum"):
+        q.sweep_spectrum(pat, q.default_dispersion(), [6000.0], "shg")
+    # an explicit mismatch table keeps the host path and agrees with the model at its own values
+    model = q.default_dispersion()
+    wls = [1380.0, 1404.0, 1430.0]
+    table = q.MismatchTable({w: model.mismatches_at(w) for w in wls})
+    a = np.array(q.sweep_spectrum(pat, model, wls, "thg"))
+    b = np.array(q.sweep_spectrum(pat, table, wls, "thg"))
+    np.testing.assert_allclose(a, b, rtol=1e-13)
