@@ -24,18 +24,22 @@
 // One hybrid generation (ten per CUDA graph, everything reading g and F from
 // device memory):
 //   k_plan_rows     (side stream, one generation ahead) keys + DE indices
-//   k_de_trial      crossover mask, trial genome + bits, and the first two
-//                   wolf draws of every gene as bit-planes (integer-issue
-//                   bound, HBM traffic in its shadow); k_de_trial_rows for
-//                   short rows (column shards)
-//   fitness         segmented quad-table scan + warp-parallel stitch
-//   k_select_topk   greedy selection + top-k leaders
+//   k_de_trial_tma  crossover mask, trial genome + bits, and the first two
+//                   wolf draws of every gene as bit-planes, the source rows
+//                   staged by TMA bulk copies (integer-issue bound, HBM
+//                   traffic in its shadow); k_de_trial_rows for short rows
+//                   (column shards), k_de_trial with global loads (QPM_DE_TMA=0)
+//   k_fit_fast      segmented quad-table scan
+//   k_finish_select<0>  stitch + greedy selection; the last CTA: top-k leaders
 //   k_gwo_apply     leader vote per gene from the planes (+ the third draw
 //                   where the outcome depends on it) -> candidate bits
-//   fitness
-//   k_select_stats  wolf selection + np.max/mean/std replica + F update
-// Multi-GPU (column shards): the fitness scans write segment partials, which
-// are all-gathered (NCCL, in the graph) and stitched on every rank.
+//   k_fit_fast
+//   k_finish_select<1>  stitch + wolf selection; the last CTA: np.max/mean/std
+//                   replica, window, F update, trace row
+// (NP > 2048: k_fit_finish + k_select_topk / k_select_stats instead of the
+// fused finish/selection kernels.)  Multi-GPU (column shards): each rank
+// pre-stitches its super-blocks (k_prestitch); the partials are all-gathered
+// (NCCL, in the graph) and every rank finishes all rows.
 // Decisions reproduce the reference bit-for-bit given the same fitness:
 //   - stream positions follow SURVEY.md Appendix A (de_mutate rejection
 //     draws 0..m-1, j_rand at m, mask m+1..m+D, wolf block from m+1+D), with
