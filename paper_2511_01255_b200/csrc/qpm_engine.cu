@@ -1980,11 +1980,16 @@ __global__ void __launch_bounds__(kCtaThreads) k_select_stats(RunConsts c, int m
 #ifndef QPM_FS_THREADS1
 #define QPM_FS_THREADS1 QPM_FS_THREADS
 #endif
+#ifndef QPM_FS_WIDE
+#define QPM_FS_WIDE 1  // fused finish/selection for NP > 2048 too (1024-thread CTAs)
+#endif
 // fused finish + selection CTA: <0> (leaders) and <1> (statistics)
 template <int MODE>
 __host__ __device__ constexpr int fs_threads() { return MODE == 0 ? QPM_FS_THREADS : QPM_FS_THREADS1; }
-template <int MODE>
-__global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts c, FinishArgs f, EngineState *__restrict__ st,
+// THREADS: fs_threads<MODE>() (NP <= 2048), or kCtaThreads for large
+// populations, whose last CTA then has the single-CTA kernels' width
+template <int MODE, int THREADS = fs_threads<MODE>()>
+__global__ void __launch_bounds__(THREADS) k_finish_select(RunConsts c, FinishArgs f, EngineState *__restrict__ st,
                                                                const double *__restrict__ sched, double *cand,
                                                                double *__restrict__ fit, int32_t *__restrict__ slot_of,
                                                                int32_t *__restrict__ spare_of,
@@ -2000,7 +2005,7 @@ __global__ void __launch_bounds__(fs_threads<MODE>()) k_finish_select(RunConsts 
     QTRACE_STARTED();
     QSTAMP(0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t r = (int64_t)blockIdx.x * (fs_threads<MODE>() / 32) + warp;
+    const int64_t r = (int64_t)blockIdx.x * (THREADS / 32) + warp;
     if (r < c.NP) {  // warp-uniform
         const double g = finish_row(f, r, lane);
         if (lane == 0) {
@@ -2263,6 +2268,7 @@ struct Engine {
     unsigned *topk_cnt = nullptr;      // arrival counter
     int64_t de_rows_max_dp = kDeRowsDefaultDp;  // warp-item trial kernel up to this row length (QPM_DE_ROWS)
     bool de_tma = QPM_DE_TMA != 0;          // TMA-staged trial rows (QPM_DE_TMA=0: global loads)
+    bool fs_wide = false;                   // fused finish/selection with 1024-thread CTAs (large NP)
     int de_item = 1024;                      // genes per warp item on longer rows (QPM_DE_ITEM, multiple of 128)
     int stats_threads = kCtaThreads;  // k_select_stats block (QPM_STATS_THREADS)
     bool pdl = true;                // programmatic dependent launch on the main chain (QPM_PDL=0 disables)
@@ -2541,6 +2547,21 @@ static FinishArgs fused_finish_args(const Engine *e) {
 }
 static int launch_finish_select(Engine *e, int mode, cudaStream_t s) {
     const RunConsts &c = e->c;
+    if (e->fs_wide) {  // large populations: 32 rows per CTA, a 1024-thread last CTA
+        constexpr int rw = kCtaThreads / 32;
+        const dim3 grid((unsigned)((c.NP + rw - 1) / rw));
+        if (mode == 0)
+            QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<0, kCtaThreads>, grid, dim3(kCtaThreads), 0, s, c,
+                                  fused_finish_args(e), e->st, (const double *)e->sched, e->cand, e->fit, e->slot_of,
+                                  e->spare_of, e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline, e->fs_cnt,
+                                  e->slot_tag));
+        else
+            QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<1, kCtaThreads>, grid, dim3(kCtaThreads), stats_smem_bytes(c),
+                                  s, c, fused_finish_args(e), e->st, (const double *)e->sched, e->cand, e->fit,
+                                  e->slot_of, e->spare_of, e->slot_bin, e->scratch, e->tree, e->trace, e->tree_inline,
+                                  e->fs_cnt + 1, e->slot_tag));
+        return QPM_OK;
+    }
     constexpr int r0 = fs_threads<0>() / 32, r1 = fs_threads<1>() / 32;
     if (mode == 0)
         QPM_CUDA_TRY(launch_k(e->pdl, k_finish_select<0>, dim3((unsigned)((c.NP + r0 - 1) / r0)), dim3(fs_threads<0>()), 0,
@@ -3008,7 +3029,11 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         // fused finish + selection: its last CTA runs the whole-population part
         // alone, which pays up to ~2k rows (C2: 116.0 -> 113.8 us per
         // generation; NP 8192: 133 -> 149 us, alternating A/B)
-        e->fused_select = c.NP <= 2048;
+        // ... and with 1024-thread CTAs up to 4,096 rows (C4 391.1 -> 388.2
+        // us/gen; emulated NP 4096 shards 193 -> 187 us); at 8,192 the
+        // multi-CTA top-k kernel is faster than one wide last CTA
+        e->fused_select = c.NP <= 2048 || (QPM_FS_WIDE && c.NP <= 4096);
+        e->fs_wide = c.NP > 2048;
         if (const char *v = knob("QPM_FUSED_SELECT")) e->fused_select = atoi(v) != 0;
         if (const char *v = knob("QPM_DE_ITEM")) e->de_item = std::max(128, atoi(v) / 128 * 128);
         auto cta_knob = [&knob](const char *name, int &dst) {  // multiple of 32 in [32, kCtaThreads]
@@ -3051,12 +3076,17 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
             }
         });
         if (tma_err != cudaSuccess) e->de_tma = false;  // (the global-load trial then runs)
-        cudaFuncAttributes fb{};
+        cudaFuncAttributes fb{}, fw{};
         cudaFuncGetAttributes(&fb, k_finish_select<1>);
-        if ((size_t)max_optin < stats_smem_bytes(c) + fb.sharedSizeBytes ||
-            cudaFuncSetAttribute(k_finish_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 max_optin - (int)fb.sharedSizeBytes) != cudaSuccess)
-            e->fused_select = false;  // (the statistics then run in k_select_stats)
+        cudaFuncGetAttributes(&fw, k_finish_select<1, kCtaThreads>);
+        const bool narrow_ok = (size_t)max_optin >= stats_smem_bytes(c) + fb.sharedSizeBytes &&
+                               cudaFuncSetAttribute(k_finish_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    max_optin - (int)fb.sharedSizeBytes) == cudaSuccess;
+        const bool wide_ok = (size_t)max_optin >= stats_smem_bytes(c) + fw.sharedSizeBytes &&
+                             cudaFuncSetAttribute(k_finish_select<1, kCtaThreads>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  max_optin - (int)fw.sharedSizeBytes) == cudaSuccess;
+        if (!(e->fs_wide ? wide_ok : narrow_ok)) e->fused_select = false;  // (the statistics then run in k_select_stats)
     }
 
     const int64_t NP = c.NP;

@@ -127,11 +127,15 @@ def test_c2_shape_runs_match_default(q, monkeypatch, env):
 def test_large_population_multi_cta_selection(q, monkeypatch):
     """NP = 8192 selects the leaders with several CTAs (last-CTA merge) and
     short rows take the warp-per-row trial: same trace as one CTA / chunked CTAs."""
-    want = _trace(q, monkeypatch, {"QPM_TOPK_CTAS": "1", "QPM_DE_ROWS": "0"}, D=1300, NP=8192, G=6)[0]
-    got = _trace(q, monkeypatch, {}, D=1300, NP=8192, G=6)[0]
+    want = _trace(q, monkeypatch, {"QPM_TOPK_CTAS": "1", "QPM_DE_ROWS": "0", "QPM_FUSED_SELECT": "0"},
+                  D=1300, NP=8192, G=6)[0]
+    got = _trace(q, monkeypatch, {"QPM_FUSED_SELECT": "0"}, D=1300, NP=8192, G=6)[0]
     assert np.array_equal(got, want)
-    fused = _trace(q, monkeypatch, {"QPM_FUSED_SELECT": "1"}, D=1300, NP=8192, G=6)[0]  # 8 stats elements per thread
+    fused = _trace(q, monkeypatch, {"QPM_FUSED_SELECT": "1"}, D=1300, NP=8192, G=6)[0]  # 1024-thread fused kernels
     assert np.array_equal(fused, want)
+    odd = _trace(q, monkeypatch, {}, D=1300, NP=3000, G=6)[0]  # wide fused by default: a partial last CTA,
+    odd_ref = _trace(q, monkeypatch, {"QPM_FUSED_SELECT": "0"}, D=1300, NP=3000, G=6)[0]  # non-power-of-two stats
+    assert np.array_equal(odd, odd_ref)
 
 
 @pytest.mark.parametrize("algorithm", ["hybrid", "de"])
