@@ -485,8 +485,7 @@ def run_ours(args):
         e3.step(args.steps)  # as run_hybrid: eager launches below 256 generations, graphs captured inside above
         mark("generations")
         e3.finalize()
-        e3.trace(0, args.steps + 1)
-        e3.best()
+        e3.result(args.steps + 1)  # trace rows + best individual, as run_hybrid reads them
         mark("finalize_readback")
         del e3
         mark("destroy")

@@ -228,6 +228,10 @@ int qpm_engine_generation(const qpm_engine *e, int64_t *g_done);
 /* copies (synchronous on the engine stream) */
 int qpm_engine_read_trace(qpm_engine *e, int64_t first_row, int64_t n_rows, double *host_rows);
 int qpm_engine_read_best(qpm_engine *e, double *genome, int8_t *proj, double *fitness);
+/* qpm_engine_read_best and qpm_engine_read_trace in one call (one pinned
+ * staging copy, one synchronisation): what optimizer.run returns. */
+int qpm_engine_read_result(qpm_engine *e, int64_t first_row, int64_t n_rows, double *host_rows, double *genome,
+                           int8_t *proj, double *fitness);
 int qpm_engine_read_population(qpm_engine *e, double *genome, double *fitness);
 /* ------------------------------------------------------------ multi-GPU
  * One process per GPU; the genes are sharded in contiguous column ranges

@@ -26,7 +26,7 @@ EXPORTS = (
     "qpm_wavelength_scalars",
     "qpm_engine_create", "qpm_engine_destroy", "qpm_engine_device_bytes", "qpm_engine_init",
     "qpm_engine_step", "qpm_engine_prepare", "qpm_engine_finalize", "qpm_engine_generation", "qpm_engine_read_trace",
-    "qpm_engine_read_best", "qpm_engine_read_population", "qpm_engine_profile", "qpm_engine_launches_per_generation",
+    "qpm_engine_read_best", "qpm_engine_read_result", "qpm_engine_read_population", "qpm_engine_profile", "qpm_engine_launches_per_generation",
     "qpm_engine_fitness_ptr", "qpm_nccl_unique_id", "qpm_engine_set_comm", "qpm_engine_columns",
     "qpm_engine_init_finish",
     "qpm_engine_phases", "qpm_engine_run_phase", "qpm_engine_exchange_from", "qpm_engine_cand_ptr",
@@ -116,6 +116,7 @@ def lib():
         "qpm_engine_generation": (I32, [P, P]),
         "qpm_engine_read_trace": (I32, [P, I64, I64, P]),
         "qpm_engine_read_best": (I32, [P, P, P, P]),
+        "qpm_engine_read_result": (I32, [P, I64, I64, P, P, P, P]),
         "qpm_engine_read_population": (I32, [P, P, P]),
         "qpm_engine_profile": (I32, [P, I64, P, P, P, I32]),
         "qpm_engine_launches_per_generation": (I32, [P]),

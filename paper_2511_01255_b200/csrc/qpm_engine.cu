@@ -3447,29 +3447,48 @@ int qpm_engine_read_trace(qpm_engine *h, int64_t first_row, int64_t n_rows, doub
     return QPM_OK;
 }
 
-int qpm_engine_read_best(qpm_engine *h, double *genome, int8_t *proj, double *fitness) {
-    QPM_ARG_CHECK(h, "engine");
-    Engine *e = h->e;
+// the best individual (and optionally trace rows) through one pinned buffer
+// and one synchronisation
+static int read_result(Engine *e, int64_t first_row, int64_t n_rows, double *host_rows, double *genome, int8_t *proj,
+                       double *fitness) {
     const RunConsts &c = e->c;
-    // genome, bits and the best fitness through one pinned buffer, one synchronisation
-    const size_t bg = sizeof(double) * c.Dp, bb = sizeof(uint32_t) * c.W;
-    char *pin = pinned_staging(bg + bb + sizeof(double));
+    const size_t bg = sizeof(double) * c.Dp, bb = sizeof(uint32_t) * c.W, bt = sizeof(double) * 5 * n_rows;
+    const size_t total = bg + bb + sizeof(double) + bt;
+    char *pin = pinned_staging(total);
     std::vector<char> pageable;
     if (!pin) {
-        pageable.resize(bg + bb + sizeof(double));
+        pageable.resize(total);
         pin = pageable.data();
     }
     QPM_CUDA_TRY(cudaMemcpyAsync(pin, e->best_genome, bg, cudaMemcpyDeviceToHost, e->stream));
     QPM_CUDA_TRY(cudaMemcpyAsync(pin + bg, e->best_bits, bb, cudaMemcpyDeviceToHost, e->stream));
     QPM_CUDA_TRY(cudaMemcpyAsync(pin + bg + bb, reinterpret_cast<const char *>(e->st) + offsetof(EngineState, best_fit),
                                  sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (n_rows)
+        QPM_CUDA_TRY(cudaMemcpyAsync(pin + bg + bb + sizeof(double), e->trace + first_row * 5, bt,
+                                     cudaMemcpyDeviceToHost, e->stream));
     QPM_CUDA_TRY(cudaStreamSynchronize(e->stream));
     const uint32_t *b = reinterpret_cast<const uint32_t *>(pin + bg);
     if (genome) memcpy(genome, pin, sizeof(double) * c.D);
     if (proj)
         for (int64_t j = 0; j < c.D; ++j) proj[j] = ((b[j >> 5] >> (j & 31)) & 1u) ? -1 : 1;
     if (fitness) memcpy(fitness, pin + bg + bb, sizeof(double));  // run_gwo: best-ever; else the finalize's top-1
+    if (n_rows) memcpy(host_rows, pin + bg + bb + sizeof(double), bt);
     return QPM_OK;
+}
+
+int qpm_engine_read_best(qpm_engine *h, double *genome, int8_t *proj, double *fitness) {
+    QPM_ARG_CHECK(h, "engine");
+    return read_result(h->e, 0, 0, nullptr, genome, proj, fitness);
+}
+
+int qpm_engine_read_result(qpm_engine *h, int64_t first_row, int64_t n_rows, double *host_rows, double *genome,
+                           int8_t *proj, double *fitness) {
+    QPM_ARG_CHECK(h, "engine");
+    Engine *e = h->e;
+    QPM_ARG_CHECK(first_row >= 0 && n_rows >= 0 && first_row + n_rows <= e->c.G + 1 && (n_rows == 0 || host_rows),
+                  "trace rows");
+    return read_result(e, first_row, n_rows, host_rows, genome, proj, fitness);
 }
 
 int qpm_engine_read_population(qpm_engine *h, double *genome, double *fitness) {

@@ -395,6 +395,17 @@ class Engine:
                                                          fit.ctypes.data), "qpm_engine_read_best")
         return Individual(genome=genome, projection=proj, fitness=float(fit[0]))
 
+    def result(self, n_rows: int):
+        """(trace rows [0, n_rows), best individual) with one copy and one synchronisation."""
+        trace = np.empty((n_rows, 5), dtype=np.float64)
+        genome = np.empty(self.Dl, dtype=np.float64)
+        proj = np.empty(self.Dl, dtype=np.int8)
+        fit = np.empty(1, dtype=np.float64)
+        _native.check(_native.lib().qpm_engine_read_result(self.handle, 0, n_rows, trace.ctypes.data,
+                                                           genome.ctypes.data, proj.ctypes.data, fit.ctypes.data),
+                      "qpm_engine_read_result")
+        return trace, Individual(genome=genome, projection=proj, fitness=float(fit[0]))
+
     def population(self):
         """(genome [NP, Dl], fitness [NP]); a column shard returns its columns."""
         genome = np.empty((self.NP, self.Dl), dtype=np.float64)
@@ -405,7 +416,8 @@ class Engine:
 
 
 def _trace_rows(arr: np.ndarray) -> list:
-    return [make_trace_row(*row) for row in arr]
+    # tolist() hands back Python floats in one call (make_trace_row's types)
+    return [(int(g), best, mean, f, sd) for g, best, mean, f, sd in arr.tolist()]
 
 
 def _check_wolf_rates(sch: Schedules, generations: int) -> None:
@@ -450,8 +462,8 @@ def _run(algorithm, objective, *, dimension, pop_size, generations, seed, de, gw
     eng.init()
     eng.step(generations, use_graph=use_graph)
     eng.finalize()
-    trace = eng.trace(0, generations + 1)
-    return RunResult(best=eng.best(), trace=_trace_rows(trace))
+    trace, best = eng.result(generations + 1)
+    return RunResult(best=best, trace=_trace_rows(trace))
 
 
 def run_hybrid(objective, *, dimension: int, pop_size: int, generations: int, seed: int,
