@@ -1,6 +1,6 @@
 #!/bin/bash
 # final round-2 evidence (outputs in gpurun_out/fin/)
-E=gpurun_out/fin
+E=gpurun_out/${EV:-fin}
 mkdir -p $E
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $E/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q --durations=10 > $E/pytest_gpu.log 2>&1; echo RC=$? >> $E/pytest_gpu.log
