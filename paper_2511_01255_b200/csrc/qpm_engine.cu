@@ -1290,6 +1290,10 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_MINB) k_de_trial_mixed(Run
 // One thread per (row, 32-gene word), one CTA row per individual: the candidate's sign word from the
 // leaders' words and the row's stored planes P0..P2 (bit-sliced, ~30 logic ops per 32
 // genes).  Leaders do not move (optimizer.py:454).
+#ifndef QPM_APPLY_ILP
+#define QPM_APPLY_ILP 2
+#endif
+constexpr int kApplyIlp = QPM_APPLY_ILP;  // third draws in flight per thread
 template <int K>
 __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialArgs a) {
     QTRACE(4);
@@ -1343,27 +1347,27 @@ __global__ void __launch_bounds__(kApplyThreads) k_gwo_apply(RunConsts c, TrialA
         const uint64_t key = a.keys[b * c.NP + i];
         const uint32_t base = (uint32_t)a.picks[b * c.NP + i].w + 2 + (uint32_t)(c.Dg + c.g0) + (uint32_t)(w * 32);
         const uint32_t D = (uint32_t)c.Dg;  // stream layout
-        // two genes per iteration: independent draws interleave
+        // kApplyIlp genes per iteration: independent draws interleave
         while (need) {
-            int bit[2];
-            bool have[2];
+            int bit[kApplyIlp];
+            bool have[kApplyIlp];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kApplyIlp; ++h) {
                 have[h] = need != 0u;
                 bit[h] = have[h] ? __ffs(need) - 1 : 0;
                 need &= need - 1;
             }
-            uint64_t x3[2];
-            uint32_t h3[2];
-            bool state[2];
+            uint64_t x3[kApplyIlp];
+            uint32_t h3[kApplyIlp];
+            bool state[kApplyIlp];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kApplyIlp; ++h) {
                 state[h] = !early || ((f2 >> bit[h]) & 1u);
                 x3[h] = mix_pre2(key, base + (uint32_t)bit[h] + (state[h] ? 3 * D : 4 * D), c);
                 h3[h] = mix_hi2(x3[h]);
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kApplyIlp; ++h) {
                 if (!have[h]) continue;
                 if (state[h]) {
                     pl[2] |= ((h3[h] >> 31) == 0u ? 1u : 0u) << bit[h];  // u < 0.5
