@@ -114,3 +114,32 @@ def test_device_wavelength_scalars_errors_and_tables():
     a = np.array(q.sweep_spectrum(pat, model, wls, "thg"))
     b = np.array(q.sweep_spectrum(pat, table, wls, "thg"))
     np.testing.assert_allclose(a, b, rtol=1e-13)
+
+
+@pytest.mark.parametrize("temperature", [25.0, 81.5, -10.0])
+def test_sellmeier_terms_restate_the_host_index(temperature):
+    """The wavelength-free terms the device receives (_sellmeier_terms) finish
+    n(lambda) bit-identically to tables.refractive_index (CPU check of the
+    device formula's arithmetic order)."""
+    from paper_2511_01255_b200.spectrum import _sellmeier_terms
+
+    model = T.default_dispersion(temperature)
+    sm = _sellmeier_terms(model)
+    for wl in np.linspace(0.41, 4.99, 501):
+        w2 = wl * wl
+        n2 = sm[0] - sm[1] * w2
+        if sm[2] != 0.0:
+            n2 += sm[2] / (w2 - sm[3])
+        if sm[4] != 0.0:
+            n2 += sm[4] / (w2 - sm[5])
+        assert float(np.sqrt(n2)) == T.refractive_index(model, float(wl))
+
+
+def test_schedule_tables_memoised_read_only():
+    from paper_2511_01255_b200 import optimizer as opt
+
+    a = opt._schedule_cached(30, opt.DEParams(), opt.GWOParams(), opt.Schedules())
+    b = opt._schedule_cached(30, opt.DEParams(), opt.GWOParams(), opt.Schedules())
+    c = opt._schedule_cached(30, opt.DEParams(f_max=0.2), opt.GWOParams(), opt.Schedules())
+    assert a is b and c is not a and not a.flags.writeable
+    assert np.array_equal(a, opt.schedule_table(30, opt.DEParams(), opt.GWOParams(), opt.Schedules()))
