@@ -276,11 +276,12 @@ def test_validation_errors(q):
 
 
 @pytest.mark.parametrize("algorithm", ["hybrid", "de", "gwo"])
-@pytest.mark.parametrize("D,NP", [(2050, 5), (4097, 13), (6000, 7)])
+@pytest.mark.parametrize("D,NP", [(2050, 5), (4097, 13), (6000, 7), (40_000, 6)])
 def test_odd_shapes_exact_vs_oracle(q, algorithm, D, NP):
     """Row lengths around the trial's chunk / stage / word boundaries (2,050:
     stages of 1,024 + 1,024 + 128 genes; 4,097: a 1-gene tail past a chunk;
-    6,000: a partial second chunk) and tiny odd populations: exact-mode runs
+    6,000: a partial second chunk; 40,000: the 8,192-gene chunks of long rows)
+    and tiny odd populations: exact-mode runs
     equal the oracle bit for bit (trace, best genome, projection, fitness)."""
     G, seed = 12, 5
     spec = q.ObjectiveSpec("single_thg", (1404.0,))
