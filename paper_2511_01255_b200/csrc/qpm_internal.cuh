@@ -94,6 +94,8 @@ struct Problem {
     uint32_t *hp_bits = nullptr;
     double *hp_out = nullptr;
     int64_t hp_rows = 0;
+    uint32_t *hp_pinned = nullptr;  // host-packed bit rows (pinned) of the host paths
+    int64_t hp_pinned_rows = 0;
     cudaStream_t hp_stream = nullptr;
     int64_t device_bytes = 0;
     // serialises the host-synchronous entry points (evaluate_block_host,
