@@ -928,6 +928,7 @@ constexpr int kTmaSteps = QPM_DE_TMA_STEPS;
 constexpr int kTmaStage = 512 * kTmaSteps;  // genes per stage
 constexpr int kTmaBufs = QPM_DE_TMA_BUFS;
 constexpr size_t kTmaSmem = (size_t)kTmaBufs * 4 * kTmaStage * sizeof(double);
+constexpr int64_t kTmaLongRows = 32768;  // rows at least this long take 8,192-gene items
 
 __device__ __forceinline__ uint32_t de_smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void de_mbar_init(uint64_t *bar, uint32_t count) {
@@ -1115,7 +1116,10 @@ __device__ __forceinline__ void de_tma_data(const RunConsts &c, const TmaRow &w,
     }
 }
 
-template <int K>
+// CHUNK: genes per CTA item (4,096; 8,192 for rows of >= 32,768 genes: C3
+// 6.67 -> 6.60 ms/gen, while C2's 10,112-gene rows keep 4,096 -- 8,192 would
+// leave a 1,920-gene second item per row)
+template <int K, int CHUNK = kDeChunk>
 __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(RunConsts c, TrialArgs a) {
     QTRACE(0);
     pdl_wait();
@@ -1126,9 +1130,9 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
     __shared__ __align__(8) uint64_t full[kTmaBufs];
     __shared__ uint32_t done[kTmaBufs];
     __shared__ TrialRow s_row;
-    const int nchunk = (int)((c.Dp + kDeChunk - 1) / kDeChunk);
+    const int nchunk = (int)((c.Dp + CHUNK - 1) / CHUNK);
     const int64_t i = a.row_lo + blockIdx.x / nchunk;
-    const int jc = (int)(blockIdx.x % nchunk) * kDeChunk;
+    const int jc = (int)(blockIdx.x % nchunk) * CHUNK;
     // Two-phase setup by thread 0.  Phase A (st->g -> keys / picks / thresholds)
     // is all the draws need: the warps start drawing after it.  Phase B (the
     // picked rows' slot tags, one dependent load later) gives the source rows;
@@ -1188,7 +1192,7 @@ __global__ void __launch_bounds__(kRowThreads, QPM_DE_TMA_MINB) k_de_trial_tma(R
     w.early = r.t.early != 0;
     w.Hsl = top_thr(r.t.sl);
     w.H2 = top_thr(w.early ? r.t.dist : r.t.flip);
-    const int jend = min(jc + kDeChunk, (int)c.Dp);
+    const int jend = min(jc + CHUNK, (int)c.Dp);
     const int nst = (jend - jc + kTmaStage - 1) / kTmaStage;
     // the source rows (valid in thread 0 after phase B, elsewhere after a stage wait)
     auto load_src = [&]() {
@@ -2689,11 +2693,16 @@ static int enqueue_phase(Engine *e, int phase, int *n, StageMarks *pm) {
             const bool k0 = !hybrid || e->wolf_in_planner || wolf_side;
             QPM_CUDA_TRY(launch_k(pdl_trial, k0 ? k_de_trial_rows<0> : (c.k == 4 ? k_de_trial_rows<4> : k_de_trial_rows<3>),
                                   dim3(row_ctas), dim3(kRowThreads), 0, s, c, all, ch));
-        } else if (e->de_tma && (!hybrid || e->wolf_in_planner || wolf_side))
-            QPM_CUDA_TRY(launch_k(pdl_trial, k_de_trial_tma<0>, dim3(items), dim3(kRowThreads), kTmaSmem, s, c, all));
-        else if (e->de_tma && !e->wolf_mixed)
-            QPM_CUDA_TRY(launch_k(pdl_trial, c.k == 4 ? k_de_trial_tma<4> : k_de_trial_tma<3>, dim3(items),
-                                  dim3(kRowThreads), kTmaSmem, s, c, all));
+        } else if (e->de_tma && ((!hybrid || e->wolf_in_planner || wolf_side) || !e->wolf_mixed)) {
+            const bool long_rows = c.Dp >= kTmaLongRows;
+            const int kw = (!hybrid || e->wolf_in_planner || wolf_side) ? 0 : c.k;
+            const unsigned ti = (unsigned)(NP * ((c.Dp + (long_rows ? 8192 : kDeChunk) - 1) /
+                                                 (long_rows ? 8192 : kDeChunk)));
+            auto kern = long_rows ? (kw == 0 ? k_de_trial_tma<0, 8192> : kw == 4 ? k_de_trial_tma<4, 8192>
+                                                                                  : k_de_trial_tma<3, 8192>)
+                                  : (kw == 0 ? k_de_trial_tma<0> : kw == 4 ? k_de_trial_tma<4> : k_de_trial_tma<3>);
+            QPM_CUDA_TRY(launch_k(pdl_trial, kern, dim3(ti), dim3(kRowThreads), kTmaSmem, s, c, all));
+        }
         else if (!hybrid || e->wolf_in_planner || wolf_side)
             QPM_CUDA_TRY(launch_k(pdl_trial, k_de_trial<0>, dim3(items), dim3(kRowThreads), 0, s, c, all));
         else if (e->wolf_mixed)
@@ -3069,8 +3078,9 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
         static std::once_flag tma_once;
         static cudaError_t tma_err = cudaSuccess;
         std::call_once(tma_once, [] {
-            const void *ks[3] = {(const void *)k_de_trial_tma<0>, (const void *)k_de_trial_tma<3>,
-                                 (const void *)k_de_trial_tma<4>};
+            const void *ks[6] = {(const void *)k_de_trial_tma<0>, (const void *)k_de_trial_tma<3>,
+                                 (const void *)k_de_trial_tma<4>, (const void *)k_de_trial_tma<0, 8192>,
+                                 (const void *)k_de_trial_tma<3, 8192>, (const void *)k_de_trial_tma<4, 8192>};
             for (const void *k : ks) {
                 cudaFuncAttributes ka{};
                 cudaError_t err = cudaFuncGetAttributes(&ka, k);
