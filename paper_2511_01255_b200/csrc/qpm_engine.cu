@@ -3059,47 +3059,53 @@ int qpm_engine_create(qpm_engine **out, qpm_problem *prob, const qpm_run_params 
     c.n_leaf = (int32_t)ht.leaf_off.size() - 1;
     c.n_levels = (int32_t)ht.lvl.size() - 1;
     {
-        // the attribute is per function and process-wide: raise it to the
-        // device's opt-in maximum once, whatever the engine's size
-        int dev = 0, max_optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, k_select_stats);
-        const size_t need = stats_smem_bytes(c) + fa.sharedSizeBytes;
-        if ((size_t)max_optin < need ||
-            cudaFuncSetAttribute(k_select_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 max_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
-            set_error("k_select_stats needs %zu bytes of shared memory (device: %d)", need, max_optin);
-            engine_free(e);
-            return QPM_ERR_CUDA;
-        }
-        // the TMA-staged trial's stage ring (static shared memory on top)
-        static std::once_flag tma_once;
-        static cudaError_t tma_err = cudaSuccess;
-        std::call_once(tma_once, [] {
+        // the attributes are per function: raised to the device's opt-in
+        // maximum once per process (one device per process), whatever the
+        // engine's size; each engine then only checks its own need
+        struct SmemAttrs {
+            int max_optin = 0;
+            size_t st_static = 0, fs_static = 0, fw_static = 0;
+            bool st_ok = false, fs_ok = false, fw_ok = false, tma_ok = false;
+        };
+        static SmemAttrs sa;
+        static std::once_flag attrs_once;
+        std::call_once(attrs_once, [] {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sa.max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncAttributes fa{}, fb{}, fw{};
+            cudaFuncGetAttributes(&fa, k_select_stats);
+            cudaFuncGetAttributes(&fb, k_finish_select<1>);
+            cudaFuncGetAttributes(&fw, k_finish_select<1, kCtaThreads>);
+            sa.st_static = fa.sharedSizeBytes;
+            sa.fs_static = fb.sharedSizeBytes;
+            sa.fw_static = fw.sharedSizeBytes;
+            sa.st_ok = cudaFuncSetAttribute(k_select_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            sa.max_optin - (int)fa.sharedSizeBytes) == cudaSuccess;
+            sa.fs_ok = cudaFuncSetAttribute(k_finish_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            sa.max_optin - (int)fb.sharedSizeBytes) == cudaSuccess;
+            sa.fw_ok = cudaFuncSetAttribute(k_finish_select<1, kCtaThreads>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            sa.max_optin - (int)fw.sharedSizeBytes) == cudaSuccess;
+            // the TMA-staged trial's stage ring (static shared memory on top)
             const void *ks[6] = {(const void *)k_de_trial_tma<0>, (const void *)k_de_trial_tma<3>,
                                  (const void *)k_de_trial_tma<4>, (const void *)k_de_trial_tma<0, 8192>,
                                  (const void *)k_de_trial_tma<3, 8192>, (const void *)k_de_trial_tma<4, 8192>};
-            for (const void *k : ks) {
-                cudaFuncAttributes ka{};
-                cudaError_t err = cudaFuncGetAttributes(&ka, k);
-                if (err == cudaSuccess)
-                    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-                if (err != cudaSuccess) tma_err = err;
-            }
+            sa.tma_ok = true;
+            for (const void *k : ks)
+                if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem) != cudaSuccess)
+                    sa.tma_ok = false;
+            cudaGetLastError();  // (a failed attribute call is reported through the flags)
         });
-        if (tma_err != cudaSuccess) e->de_tma = false;  // (the global-load trial then runs)
-        cudaFuncAttributes fb{}, fw{};
-        cudaFuncGetAttributes(&fb, k_finish_select<1>);
-        cudaFuncGetAttributes(&fw, k_finish_select<1, kCtaThreads>);
-        const bool narrow_ok = (size_t)max_optin >= stats_smem_bytes(c) + fb.sharedSizeBytes &&
-                               cudaFuncSetAttribute(k_finish_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    max_optin - (int)fb.sharedSizeBytes) == cudaSuccess;
-        const bool wide_ok = (size_t)max_optin >= stats_smem_bytes(c) + fw.sharedSizeBytes &&
-                             cudaFuncSetAttribute(k_finish_select<1, kCtaThreads>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  max_optin - (int)fw.sharedSizeBytes) == cudaSuccess;
+        const size_t need = stats_smem_bytes(c) + sa.st_static;
+        if ((size_t)sa.max_optin < need || !sa.st_ok) {
+            set_error("k_select_stats needs %zu bytes of shared memory (device: %d)", need, sa.max_optin);
+            engine_free(e);
+            return QPM_ERR_CUDA;
+        }
+        if (!sa.tma_ok) e->de_tma = false;  // (the global-load trial then runs)
+        const bool narrow_ok = sa.fs_ok && (size_t)sa.max_optin >= stats_smem_bytes(c) + sa.fs_static;
+        const bool wide_ok = sa.fw_ok && (size_t)sa.max_optin >= stats_smem_bytes(c) + sa.fw_static;
         if (!(e->fs_wide ? wide_ok : narrow_ok)) e->fused_select = false;  // (the statistics then run in k_select_stats)
     }
 
